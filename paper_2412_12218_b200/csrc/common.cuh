@@ -1,0 +1,182 @@
+// Shared device/host helpers for the sm_100a FTC-GNN aggregation path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "sgtk_cuda.h"
+
+namespace sgtkcu {
+
+// ---------------------------------------------------------------------------
+// Host-side error plumbing.  Internal code throws Status; the C ABI catches it
+// and returns the code (capi.cpp).  Nothing throws across the C boundary.
+// ---------------------------------------------------------------------------
+struct Status : std::runtime_error {
+  int code;
+  Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void raise(int code, const std::string& msg) {
+  throw Status(code, msg);
+}
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    raise(SGTK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CU(x) ::sgtkcu::cuda_check((x), #x)
+#define CU_LAUNCH(what) ::sgtkcu::cuda_check(cudaGetLastError(), what)
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
+constexpr int kWinRows = 16;  // internal row-window height (MMA M)
+
+// Feature-chunk width a warp owns in the SpMM / fused AGNN kernels.
+inline int pick_dc(uint64_t d) {
+  if (d <= 16) return 16;
+  if (d <= 32) return 32;
+  return 64;
+}
+
+// Device memory owned by RAII (graph handles, workspaces).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t b) { alloc(b); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t b) {
+    release();
+    if (b) {
+      cudaError_t e = cudaMalloc(&p, b);
+      if (e != cudaSuccess) {
+        p = nullptr;
+        raise(SGTK_ERR_CUDA, "cudaMalloc(" + std::to_string(b) + " B): " +
+                                 cudaGetErrorString(e));
+      }
+    }
+    bytes = b;
+  }
+  void ensure(size_t b) { if (b > bytes) alloc(b); }
+  void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace sgtkcu
+
+// ---------------------------------------------------------------------------
+// Device helpers
+// ---------------------------------------------------------------------------
+#ifdef __CUDACC__
+namespace sgtkcu {
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+// tf32_round_value (tile_exec.cpp:131-142), bit-exact: RNE to 10 mantissa
+// bits with saturation at the largest finite TF32 value.  Integer ops only.
+__device__ __forceinline__ float tf32_rne(float v) {
+  uint32_t u = __float_as_uint(v);
+  if ((u & 0x7F800000u) == 0x7F800000u) return v;
+  u = (u + 0x0FFFu + ((u >> 13) & 1u)) & 0xFFFFE000u;
+  if ((u & 0x7F800000u) == 0x7F800000u) u = (u & 0x80000000u) | 0x7F7FE000u;
+  return __uint_as_float(u);
+}
+
+// Hardware round-to-nearest (ties away) TF32: used for the "hi" half of the
+// 3xTF32 split, where only |x - hi| small matters, not the tie rule.
+__device__ __forceinline__ uint32_t tf32_rna_bits(float v) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return r;
+}
+
+// D += A(16x8 tf32, row) * B(8x8 tf32, col), fp32 accumulate.
+__device__ __forceinline__ void mma_tf32(float (&c)[4], uint32_t a0, uint32_t a1,
+                                         uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// Operand split per precision: TF32 -> (rne(x), 0); FP32 -> (hi, lo) with
+// x = hi + lo exactly in fp32 (3xTF32 emulation); BF16 handled separately.
+template <int PREC>
+__device__ __forceinline__ void split_operand(float x, uint32_t& hi, uint32_t& lo) {
+  if constexpr (PREC == SGTK_TF32) {
+    hi = __float_as_uint(tf32_rne(x));
+    lo = 0u;
+  } else {
+    hi = tf32_rna_bits(x);
+    lo = __float_as_uint(x - __uint_as_float(hi));
+  }
+}
+
+// ---- vectorised segment loads/stores (N floats, N in {2,4,8,16}) ----------
+template <int N, bool VEC>
+__device__ __forceinline__ void load_seg(float (&dst)[N], const float* __restrict__ src,
+                                         int valid) {
+  if (VEC && valid >= N) {
+    if constexpr (N == 2) {
+      float2 v = __ldg(reinterpret_cast<const float2*>(src));
+      dst[0] = v.x; dst[1] = v.y;
+    } else {
+#pragma unroll
+      for (int i = 0; i < N / 4; ++i) {
+        float4 v = __ldg(reinterpret_cast<const float4*>(src) + i);
+        dst[4 * i + 0] = v.x; dst[4 * i + 1] = v.y;
+        dst[4 * i + 2] = v.z; dst[4 * i + 3] = v.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) dst[i] = i < valid ? __ldg(src + i) : 0.0f;
+  }
+}
+
+template <int N, bool VEC>
+__device__ __forceinline__ void store_seg(float* __restrict__ dst, const float (&v)[N],
+                                          int valid) {
+  if (VEC && valid >= N) {
+    if constexpr (N == 2) {
+      *reinterpret_cast<float2*>(dst) = make_float2(v[0], v[1]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < N / 4; ++i)
+        reinterpret_cast<float4*>(dst)[i] =
+            make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (i < valid) dst[i] = v[i];
+  }
+}
+
+// First index in [lo, hi) with key[idx] >= v (keys ascending).
+__device__ __forceinline__ uint64_t lower_bound_u32(const uint32_t* __restrict__ key,
+                                                    uint64_t lo, uint64_t hi,
+                                                    uint32_t v) {
+  while (lo < hi) {
+    uint64_t mid = (lo + hi) >> 1;
+    if (key[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+}  // namespace sgtkcu
+#endif  // __CUDACC__

@@ -1,0 +1,165 @@
+// Model forwards on the device: GCN (gnn.cpp:33-52) and AGNN (gnn.cpp:93-119).
+//
+// GCN per layer: h <- relu?(A h W).  The reference aggregates first,
+// (A h) W (gnn.cpp:43-44); when d_out < d_in the same product is cheaper as
+// A (h W) (the SpMM then gathers d_out-wide rows instead of d_in-wide ones:
+// at Cora 1433->16 that is 90x fewer gathered bytes).  `order` selects.
+//
+// AGNN per layer (mode 0, the reference chain):
+//   l2norm -> inv_norm[N]            (z never materialised; the SDDMM scales
+//                                      rows by inv_norm as it loads them)
+//   SDDMM(16-wide tiles) * beta      -> logits[E], CSR order
+//   edge_softmax (in place)          -> attention[E]
+//   SpMM(8-wide tiles, attention)    -> h_next
+// mode 1: the fused single-pass kernel (agnn_fused.cu): logits and attention
+// never touch HBM.
+
+#include <algorithm>
+
+#include "kernels.cuh"
+
+namespace sgtkcu {
+namespace {
+
+__global__ void relu_nonfinite_kernel(float* __restrict__ x, uint64_t rows, uint64_t cols,
+                                      uint64_t ld, int relu, uint32_t* __restrict__ nonfinite) {
+  bool bad = false;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows * cols;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / cols, c = i - r * cols;
+    float v = x[r * ld + c];
+    if (relu) {
+      v = v > 0.0f ? v : 0.0f;
+      x[r * ld + c] = v;
+    }
+    bad |= !isfinite(v);
+  }
+  if (nonfinite && __any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
+}
+
+inline uint64_t ld4(uint64_t d) { return (d + 3) / 4 * 4; }
+inline uint64_t align256(uint64_t b) { return (b + 255) / 256 * 256; }
+
+}  // namespace
+
+void relu_nonfinite_launch(float* x, uint64_t rows, uint64_t cols, uint64_t ld, int relu,
+                           uint32_t* nonfinite, cudaStream_t s) {
+  if (!rows || !cols) return;
+  const uint64_t n = rows * cols;
+  unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, 148 * 32));
+  relu_nonfinite_kernel<<<blocks, 256, 0, s>>>(x, rows, cols, ld, relu, nonfinite);
+  CU_LAUNCH("relu_nonfinite_kernel");
+}
+
+std::vector<uint32_t> split_plan_host(const sgtk_graph* g, double ratio) {
+  if (!(ratio >= 0.0 && ratio <= 1.0)) raise(SGTK_ERR_RANGE, "split ratio must be within [0, 1]");
+  std::vector<uint32_t> cut(g->bp_host.size());
+  for (size_t w = 0; w < cut.size(); ++w)
+    cut[w] = uint32_t(std::floor(ratio * double(g->bp_host[w])));
+  return cut;
+}
+
+uint64_t gcn_workspace(const sgtk_graph* g, uint32_t L, const uint64_t* dims) {
+  uint64_t mx = 0;
+  for (uint32_t l = 0; l <= L; ++l) mx = std::max(mx, ld4(dims[l]));
+  return 3 * align256(g->n_rows * mx * 4) + 256;
+}
+
+void gcn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint32_t L,
+                 const uint64_t* dims, const float* weights, const int* relu,
+                 const uint32_t* cut, int prec, int order, void* ws, uint64_t ws_bytes, float* out,
+                 uint64_t ldo, cudaStream_t s) {
+  const uint64_t N = g->n_rows;
+  if (L == 0) raise(SGTK_ERR_SHAPE, "gcn_forward: no layers");
+  if (ws_bytes < gcn_workspace(g, L, dims)) raise(SGTK_ERR_SHAPE, "gcn_forward: workspace too small");
+  uint64_t mx = 0;
+  for (uint32_t l = 0; l <= L; ++l) mx = std::max(mx, ld4(dims[l]));
+  char* base = static_cast<char*>(ws);
+  const uint64_t slab = align256(N * mx * 4);
+  float* buf[2] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + slab)};
+  float* tmp = reinterpret_cast<float*>(base + 2 * slab);
+  uint32_t* flag = reinterpret_cast<uint32_t*>(base + 3 * slab);
+  CU(cudaMemsetAsync(flag, 0, 4, s));
+
+  const float* h = x;
+  uint64_t ldh = ldx;
+  const float* w = weights;
+  for (uint32_t l = 0; l < L; ++l) {
+    const uint64_t din = dims[l], dout = dims[l + 1];
+    const bool last = l + 1 == L;
+    float* dst = last ? out : buf[l & 1];
+    const uint64_t ldd = last ? ldo : ld4(dout);
+    const bool alt = order == 1 || (order == 2 && dout < din);
+    if (!alt) {  // reference order: (A h) W
+      spmm_launch(g, h, ldh, din, cut, nullptr, prec, tmp, ld4(din), flag, s);
+      gemm_launch(tmp, ld4(din), w, N, din, dout, relu[l], prec, dst, ldd, s);
+      if (last) relu_nonfinite_launch(dst, N, dout, ldd, 0, flag, s);
+    } else {      // A (h W), ReLU after the aggregation
+      gemm_launch(h, ldh, w, N, din, dout, 0, prec, tmp, ld4(dout), s);
+      spmm_launch(g, tmp, ld4(dout), dout, cut, nullptr, prec, dst, ldd, flag, s);
+      if (relu[l] || last) relu_nonfinite_launch(dst, N, dout, ldd, relu[l], flag, s);
+    }
+    w += din * dout;
+    h = dst;
+    ldh = ldd;
+  }
+  uint32_t hf = 0;
+  CU(cudaMemcpyAsync(&hf, flag, 4, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (hf) raise(SGTK_ERR_NONFINITE, "gcn_forward: output contains NaN or Inf");
+}
+
+uint64_t agnn_workspace(const sgtk_graph* g, uint64_t d) {
+  return 2 * align256(g->n_rows * ld4(d) * 4) + align256(g->n_rows * 4) +
+         align256(std::max<uint64_t>(g->nnz, 1) * 4) + align256(16 * 4) + align256(g->internal.W * 4);
+}
+
+void agnn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d, uint32_t L,
+                  const float* betas, const uint32_t* cut, int prec, int mode, void* ws,
+                  uint64_t ws_bytes, float* out, uint64_t ldo, uint64_t* zero_rows_host,
+                  cudaStream_t s) {
+  const uint64_t N = g->n_rows;
+  if (ws_bytes < agnn_workspace(g, d)) raise(SGTK_ERR_SHAPE, "agnn_forward: workspace too small");
+  char* p = static_cast<char*>(ws);
+  const uint64_t ldb = ld4(d);
+  float* buf[2];
+  buf[0] = reinterpret_cast<float*>(p); p += align256(N * ldb * 4);
+  buf[1] = reinterpret_cast<float*>(p); p += align256(N * ldb * 4);
+  float* inv = reinterpret_cast<float*>(p); p += align256(N * 4);
+  float* logits = reinterpret_cast<float*>(p); p += align256(std::max<uint64_t>(g->nnz, 1) * 4);
+  uint64_t* zeros = reinterpret_cast<uint64_t*>(p); p += align256(16 * 4);
+  uint32_t* cut16 = reinterpret_cast<uint32_t*>(p);
+  CU(cudaMemsetAsync(zeros, 0, 8, s));
+  (void)cut16;
+
+  if (L == 0) {
+    CU(cudaMemcpy2DAsync(out, ldo * 4, x, ldx * 4, d * 4, N, cudaMemcpyDeviceToDevice, s));
+  }
+  const float* h = x;
+  uint64_t ldh = ldx;
+  for (uint32_t l = 0; l < L; ++l) {
+    const bool last = l + 1 == L;
+    float* dst = last ? out : buf[l & 1];
+    const uint64_t ldd = last ? ldo : ldb;
+    l2norm_launch(h, N, d, ldh, nullptr, 0, inv, zeros, s);
+    if (mode == 1) {
+      agnn_fused_launch(g, h, ldh, d, inv, betas[l], prec, dst, ldd, s);
+    } else {
+      // The reference's SDDMM runs on reblock(t, 16) with make_split_plan(t16, ratio)
+      // (gnn.cpp:101-102); the 8-wide cut carried over to 16-wide tiles is
+      // the same ratio up to floor rounding.
+      sddmm_launch(g, h, ldh, h, ldh, d, cut, nullptr, /*unit_values=*/true, prec, inv,
+                   betas[l], logits, s);
+      edge_softmax_launch(g, logits, logits, s);
+      spmm_launch(g, h, ldh, d, cut, logits, prec, dst, ldd, nullptr, s);
+    }
+    h = dst;
+    ldh = ldd;
+  }
+  if (zero_rows_host) {
+    CU(cudaMemcpyAsync(zero_rows_host, zeros, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+  }
+}
+
+}  // namespace sgtkcu

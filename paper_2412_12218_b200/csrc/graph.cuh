@@ -1,0 +1,109 @@
+// Device-resident TransformedGraph + the condensed tile format (host struct).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+
+namespace sgtkcu {
+
+// One warp-task of the tiled kernels: tiles [t0, t1) of 16-row window `window`
+// (internal 16-row geometry).  slot != kNoSlot: the window is split into
+// several units whose partial 16 x d outputs are reduced in slot order.
+struct WorkUnit {
+  uint32_t window;
+  uint32_t t0;
+  uint32_t t1;
+  uint32_t slot;
+};
+
+// A split window: partial slots [slot0, slot0 + count) reduce into its rows.
+struct ReduceItem {
+  uint32_t window;
+  uint32_t slot0;
+  uint32_t count;
+  uint32_t pad;
+};
+
+struct UnitPlan {
+  std::shared_ptr<DevBuf> units, reduce;
+  uint32_t n_units = 0, n_reduce = 0, n_slots = 0, max_tiles = 0;
+};
+
+// Translator output for one row-window height (the reference fields).
+struct Windows {
+  uint32_t blk_h = 16;
+  uint64_t W = 0, U = 0;
+  std::shared_ptr<DevBuf> e2c;  // u32[E] window-relative rank
+  std::shared_ptr<DevBuf> wo;   // u64[W+1]
+  std::shared_ptr<DevBuf> wuc;  // u32[U]
+  std::vector<uint32_t> ucount_host;  // unique columns per window
+  std::vector<uint64_t> wo_host;
+};
+
+// POD view handed to kernels.
+struct DevGraph {
+  uint64_t n_rows, n_cols, nnz, W;
+  const uint64_t* np;
+  const uint32_t* el;
+  const float* vals;
+  const uint32_t* e2c;  // internal (16-row) ranks
+  const uint64_t* wo;
+  const uint32_t* wuc;
+  const uint64_t* toff8;
+  const uint4* bm8;     // per 8-wide tile: 16 rows x 8 bits (byte r = row r)
+  const uint64_t* toff16;
+  const uint4* bm16;    // per 16-wide tile: 2 x uint4 (u16 per row)
+};
+
+}  // namespace sgtkcu
+
+struct sgtk_graph {
+  uint64_t n_rows = 0, n_cols = 0, nnz = 0;
+  uint32_t blk_h = 16, blk_w = 8;
+  bool has_values = false;
+  int device = 0;
+
+  std::shared_ptr<sgtkcu::DevBuf> np, el, vals, e2r;
+  sgtkcu::Windows user;      // reference fields at the user's geometry
+  sgtkcu::Windows internal;  // 16-row windows the kernels run on (== user if blk_h == 16)
+  std::vector<uint32_t> bp_host;  // block_partition at (blk_h, blk_w)
+  uint64_t block_counter = 0;
+  std::shared_ptr<sgtkcu::DevBuf> bp;  // u32[W] at (blk_h, blk_w)
+
+  // condensed tile format (internal windows)
+  uint64_t T8 = 0, T16 = 0;
+  std::shared_ptr<sgtkcu::DevBuf> toff8, bm8, toff16, bm16;
+  sgtkcu::UnitPlan plan8, plan16;
+
+  // workspace for host-buffer entry points and forwards (mutable scratch)
+  mutable std::shared_ptr<sgtkcu::DevBuf> scratch;
+
+  sgtkcu::DevGraph view() const {
+    sgtkcu::DevGraph v{};
+    v.n_rows = n_rows;
+    v.n_cols = n_cols;
+    v.nnz = nnz;
+    v.W = internal.W;
+    v.np = np->as<uint64_t>();
+    v.el = el->as<uint32_t>();
+    v.vals = has_values ? vals->as<float>() : nullptr;
+    v.e2c = internal.e2c->as<uint32_t>();
+    v.wo = internal.wo->as<uint64_t>();
+    v.wuc = internal.wuc->as<uint32_t>();
+    v.toff8 = toff8->as<uint64_t>();
+    v.bm8 = bm8->as<uint4>();
+    v.toff16 = toff16->as<uint64_t>();
+    v.bm16 = bm16->as<uint4>();
+    return v;
+  }
+};
+
+namespace sgtkcu {
+// Per-window tile-threshold (in 8- or 16-wide internal tiles) derived from a
+// user-geometry cut array; nullptr cut => all tiles on the tensor-core path.
+// Returns a device array u32[W_internal] or nullptr (owned by `keep`).
+const uint32_t* internal_cut(const sgtk_graph* g, const uint32_t* cut_dev,
+                             int tile_w, cudaStream_t s, DevBuf& keep);
+}  // namespace sgtkcu

@@ -1,0 +1,40 @@
+// Internal launchers shared across translation units (host side).
+#pragma once
+
+#include "graph.cuh"
+
+namespace sgtkcu {
+
+sgtk_graph* graph_create(const uint64_t* np, const uint32_t* el, const float* vals, uint64_t n_rows,
+                         uint64_t n_cols, uint64_t nnz, uint32_t blk_h, uint32_t blk_w, int kind,
+                         cudaStream_t s);
+sgtk_graph* graph_import(const uint64_t* np, const uint32_t* el, const float* vals,
+                         uint64_t n_rows, uint64_t nnz, uint32_t blk_h, uint32_t blk_w,
+                         const uint32_t* e2c, const uint64_t* wo, const uint32_t* wuc,
+                         cudaStream_t s);
+sgtk_graph* graph_reblock(const sgtk_graph* src, uint32_t blk_w, cudaStream_t s);
+
+void spmm_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
+                 const uint32_t* cut_dev, const float* ev, int prec, float* out, uint64_t ldo,
+                 uint32_t* nonfinite, cudaStream_t s);
+void sddmm_launch(const sgtk_graph* g, const float* x, uint64_t ldx, const float* y, uint64_t ldy,
+                  uint64_t d, const uint32_t* cut16_dev, const float* ev, bool unit_values,
+                  int prec, const float* inv_norm, float scale, float* out, cudaStream_t s);
+void edge_softmax_launch(const sgtk_graph* g, const float* logits, float* out, cudaStream_t s);
+void l2norm_launch(const float* h, uint64_t rows, uint64_t cols, uint64_t ldh, float* z,
+                   uint64_t ldz, float* inv, uint64_t* zeros, cudaStream_t s);
+void gcn_normalize_launch(const uint64_t* np, const uint32_t* el, uint64_t n, float* vals,
+                          cudaStream_t s);
+void tf32_launch(const float* in, float* out, uint64_t n, cudaStream_t s);
+void gemm_launch(const float* a, uint64_t lda, const float* w, uint64_t m, uint64_t k, uint64_t n,
+                 int relu, int prec, float* out, uint64_t ldo, cudaStream_t s);
+void relu_nonfinite_launch(float* x, uint64_t rows, uint64_t cols, uint64_t ld, int relu,
+                           uint32_t* nonfinite, cudaStream_t s);
+void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, uint64_t d,
+                       const float* inv_norm, float beta, int prec, float* out, uint64_t ldo,
+                       cudaStream_t s);
+
+// Host-side split plan (make_split_plan, tile_exec.cpp:150-161).
+std::vector<uint32_t> split_plan_host(const sgtk_graph* g, double ratio);
+
+}  // namespace sgtkcu
