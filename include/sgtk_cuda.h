@@ -54,7 +54,7 @@ typedef enum sgtk_status {
 
 /* tile_exec.hpp:12-15 Precision; BF16 is an additive value. */
 typedef enum sgtk_precision {
-  SGTK_FP32 = 0, /* fp32-accurate: 3xTF32 split MMA, fp32 accumulate      */
+  SGTK_FP32 = 0, /* fp32-accurate: 4-term TF32 split MMA, fp32 accumulate */
   SGTK_TF32 = 1, /* operands RNE-rounded to TF32 (tile_exec.cpp:131-142)  */
   SGTK_BF16 = 2  /* operands rounded to BF16, fp32 accumulate (additive)  */
 } sgtk_precision;

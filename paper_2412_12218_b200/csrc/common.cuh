@@ -113,16 +113,47 @@ __device__ __forceinline__ void mma_tf32(float (&c)[4], uint32_t a0, uint32_t a1
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// Operand split per precision: TF32 -> (rne(x), 0); FP32 -> (hi, lo) with
-// x = hi + lo exactly in fp32 (3xTF32 emulation); BF16 handled separately.
+// FP32 precision on TF32 tensor cores ("4-term split"): the data operand d
+// is cut into three TF32-exact parts d = d0 + d1 + d2 (11 + 11 + 2
+// significand bits, by masking, so the tensor core truncates nothing) and the
+// structure operand s (adjacency value, weight) into s = s0 + s1;
+//   s*d ~= s0*d2 + s1*d0 + s0*d1 + s0*d0      (four MMAs, small terms first)
+// drops only s1*d1, s1*d2 (< 2^-21 |s||d|), and is EXACT whenever s is
+// TF32-representable (unit / identity weights: the reference's bit-exact KATs,
+// test_tile_exec.cpp:79-86, test_gnn.cpp:36-42).
+// TF32 precision: both operands RNE-rounded exactly like tf32_round_value.
+__device__ __forceinline__ uint32_t tf32_trunc_bits(float v) {
+  return __float_as_uint(v) & 0xFFFFE000u;
+}
+__device__ __forceinline__ void split2(float v, uint32_t& p0, uint32_t& p1) {
+  p0 = tf32_trunc_bits(v);
+  p1 = __float_as_uint(v - __uint_as_float(p0));
+}
+__device__ __forceinline__ void split3(float v, uint32_t& p0, uint32_t& p1, uint32_t& p2) {
+  p0 = tf32_trunc_bits(v);
+  const float r = v - __uint_as_float(p0);
+  p1 = tf32_trunc_bits(r);
+  p2 = __float_as_uint(r - __uint_as_float(p1));
+}
+
+// Structure operand per precision: TF32 -> (rne, -), FP32 -> split2.
 template <int PREC>
-__device__ __forceinline__ void split_operand(float x, uint32_t& hi, uint32_t& lo) {
+__device__ __forceinline__ void split_s(float x, uint32_t& p0, uint32_t& p1) {
   if constexpr (PREC == SGTK_TF32) {
-    hi = __float_as_uint(tf32_rne(x));
-    lo = 0u;
+    p0 = __float_as_uint(tf32_rne(x));
+    p1 = 0u;
   } else {
-    hi = tf32_rna_bits(x);
-    lo = __float_as_uint(x - __uint_as_float(hi));
+    split2(x, p0, p1);
+  }
+}
+// Data operand per precision: TF32 -> (rne, -, -), FP32 -> split3.
+template <int PREC>
+__device__ __forceinline__ void split_d(float x, uint32_t& p0, uint32_t& p1, uint32_t& p2) {
+  if constexpr (PREC == SGTK_TF32) {
+    p0 = __float_as_uint(tf32_rne(x));
+    p1 = p2 = 0u;
+  } else {
+    split3(x, p0, p1, p2);
   }
 }
 

@@ -8,7 +8,7 @@
 //     accumulator in TMEM — used when the shape/alignment allow it.
 //   * this file: a cp.async double-buffered mma.sync m16n8k8 kernel that
 //     handles every shape/alignment (odd k, odd n, unaligned leading dims).
-// FP32 precision uses the 3xTF32 split (a = hi + lo) on both paths.
+// FP32 precision uses the 4-term TF32 split (common.cuh) on both paths.
 
 #include "graph.cuh"
 
@@ -91,22 +91,23 @@ gemm_mma_kernel(const float* __restrict__ a, uint64_t lda, const float* __restri
     const float* W = Ws[buf];
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 8) {
-      uint32_t ah[4], al[4];
-      split_operand<PREC>(A[g * AS + kk + t], ah[0], al[0]);
-      split_operand<PREC>(A[(g + 8) * AS + kk + t], ah[1], al[1]);
-      split_operand<PREC>(A[g * AS + kk + t + 4], ah[2], al[2]);
-      split_operand<PREC>(A[(g + 8) * AS + kk + t + 4], ah[3], al[3]);
+      uint32_t a0[4], a1[4], a2[4];
+      split_d<PREC>(A[g * AS + kk + t], a0[0], a1[0], a2[0]);
+      split_d<PREC>(A[(g + 8) * AS + kk + t], a0[1], a1[1], a2[1]);
+      split_d<PREC>(A[g * AS + kk + t + 4], a0[2], a1[2], a2[2]);
+      split_d<PREC>(A[(g + 8) * AS + kk + t + 4], a0[3], a1[3], a2[3]);
 #pragma unroll
       for (int j = 0; j < BN / 8; ++j) {
         if (j >= nblk) break;
-        uint32_t bh0, bl0, bh1, bl1;
-        split_operand<PREC>(W[(kk + t) * WS + j * 8 + g], bh0, bl0);
-        split_operand<PREC>(W[(kk + t + 4) * WS + j * 8 + g], bh1, bl1);
+        uint32_t b0, c0, b1, c1;
+        split_s<PREC>(W[(kk + t) * WS + j * 8 + g], b0, c0);
+        split_s<PREC>(W[(kk + t + 4) * WS + j * 8 + g], b1, c1);
         if constexpr (PREC == SGTK_FP32) {
-          mma_tf32(acc[j], al[0], al[1], al[2], al[3], bh0, bh1);
-          mma_tf32(acc[j], ah[0], ah[1], ah[2], ah[3], bl0, bl1);
+          mma_tf32(acc[j], a2[0], a2[1], a2[2], a2[3], b0, b1);
+          mma_tf32(acc[j], a0[0], a0[1], a0[2], a0[3], c0, c1);
+          mma_tf32(acc[j], a1[0], a1[1], a1[2], a1[3], b0, b1);
         }
-        mma_tf32(acc[j], ah[0], ah[1], ah[2], ah[3], bh0, bh1);
+        mma_tf32(acc[j], a0[0], a0[1], a0[2], a0[3], b0, b1);
       }
     }
     __syncthreads();

@@ -4,7 +4,7 @@
 //   out[e] = a_e * <x[row e], y[col e]>, CSR edge order.
 // Per 16-row window the 16-wide condensed tiles (the reference reblocks to 16
 // before calling it, gnn.cpp:101-112) are 16x16 blocks of dot products:
-// two m16n8k8 TF32 MMAs per 8 features (FP32 precision = 3xTF32), with the
+// two m16n8k8 TF32 MMAs per 8 features (FP32 precision: 4-term split), with the
 // window's x rows held in registers as A fragments and the tile's 16 gathered
 // y rows as B fragments.  Only positions that are edges are written: the
 // tile's 16x16 occupancy bitmap plus per-row CSR cursors give each edge's
@@ -32,7 +32,8 @@ __device__ __forceinline__ uint32_t bits16_of(const uint4& lo, const uint4& hi, 
 
 template <int PREC, bool VEC>
 struct Frag {
-  uint32_t hi[4][KS], lo[4][KS];  // [segment: (row a, k=t), (row b, k=t), (row a, t+4), (row b, t+4)]
+  // [segment: (row a, k=t), (row b, k=t), (row a, t+4), (row b, t+4)]; x = p0 + p1 + p2
+  uint32_t p0[4][KS], p1[4][KS], p2[4][KS];
 };
 
 template <int PREC, bool VEC>
@@ -54,7 +55,7 @@ __device__ __forceinline__ void load_a(Frag<PREC, VEC>& A, const float* __restri
     for (int i = 0; i < KS; ++i) {
       float v = s[i];
       if (inva) v = v * (rowa ? *inva : *invb);  // z = h * inv_norm (gnn.cpp:85-87)
-      split_operand<PREC>(v, A.hi[q][i], A.lo[q][i]);
+      split_d<PREC>(v, A.p0[q][i], A.p1[q][i], A.p2[q][i]);
     }
   }
 }
@@ -138,16 +139,17 @@ sddmm_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t n_un
         load_seg<KS, VEC>(s1, yr + fb + (t + 4) * KS, v1);
 #pragma unroll
         for (int i = 0; i < KS; ++i) {
-          uint32_t bh0, bl0, bh1, bl1;
+          uint32_t b0, c0, b1, c1;  // y = b + c (rows k=t and k=t+4)
           const float y0 = inv_norm ? s0[i] * ic[nb] : s0[i];
           const float y1 = inv_norm ? s1[i] * ic[nb] : s1[i];
-          split_operand<PREC>(y0, bh0, bl0);
-          split_operand<PREC>(y1, bh1, bl1);
+          split_s<PREC>(y0, b0, c0);
+          split_s<PREC>(y1, b1, c1);
           if constexpr (PREC == SGTK_FP32) {
-            mma_tf32(acc[nb], A.lo[0][i], A.lo[1][i], A.lo[2][i], A.lo[3][i], bh0, bh1);
-            mma_tf32(acc[nb], A.hi[0][i], A.hi[1][i], A.hi[2][i], A.hi[3][i], bl0, bl1);
+            mma_tf32(acc[nb], A.p2[0][i], A.p2[1][i], A.p2[2][i], A.p2[3][i], b0, b1);
+            mma_tf32(acc[nb], A.p0[0][i], A.p0[1][i], A.p0[2][i], A.p0[3][i], c0, c1);
+            mma_tf32(acc[nb], A.p1[0][i], A.p1[1][i], A.p1[2][i], A.p1[3][i], b0, b1);
           }
-          mma_tf32(acc[nb], A.hi[0][i], A.hi[1][i], A.hi[2][i], A.hi[3][i], bh0, bh1);
+          mma_tf32(acc[nb], A.p0[0][i], A.p0[1][i], A.p0[2][i], A.p0[3][i], b0, b1);
         }
       }
     }

@@ -3,7 +3,7 @@
 // Replaces spmm_hybrid (/root/reference/proj/src/tile_exec.cpp:200-314):
 //   out = A * x, rows of A from the SGT windows.  Per 16-row window, the
 //   8-wide condensed tiles below the plan's cut run on the tensor cores
-//   (mma.sync m16n8k8 TF32, fp32 accumulate; FP32 precision = 3xTF32 split),
+//   (mma.sync m16n8k8 TF32, fp32 accumulate; FP32 precision = 4-term TF32 split),
 //   the remaining edges of each row run edge-by-edge on the CUDA cores
 //   (tile_exec.cpp:291-303) — in the same warp, into the same accumulators.
 //
@@ -106,21 +106,22 @@ spmm_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t n_uni
     const float a2 = a_at<VALS>(vals, bya, t + 4, ca), a3 = a_at<VALS>(vals, byb, t + 4, cb);
     ca += __popc(bya);
     cb += __popc(byb);
-    uint32_t ah[4], al[4];
-    split_operand<PREC>(a0, ah[0], al[0]);
-    split_operand<PREC>(a1, ah[1], al[1]);
-    split_operand<PREC>(a2, ah[2], al[2]);
-    split_operand<PREC>(a3, ah[3], al[3]);
+    uint32_t s0[4], s1[4];
+    split_s<PREC>(a0, s0[0], s1[0]);
+    split_s<PREC>(a1, s0[1], s1[1]);
+    split_s<PREC>(a2, s0[2], s1[2]);
+    split_s<PREC>(a3, s0[3], s1[3]);
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
-      uint32_t bh0, bl0, bh1, bl1;
-      split_operand<PREC>(xb0[j], bh0, bl0);
-      split_operand<PREC>(xb1[j], bh1, bl1);
+      uint32_t p0, p1, p2, q0, q1, q2;  // B rows k=t (p) and k=t+4 (q)
+      split_d<PREC>(xb0[j], p0, p1, p2);
+      split_d<PREC>(xb1[j], q0, q1, q2);
       if constexpr (PREC == SGTK_FP32) {
-        mma_tf32(acc[j], al[0], al[1], al[2], al[3], bh0, bh1);
-        mma_tf32(acc[j], ah[0], ah[1], ah[2], ah[3], bl0, bl1);
+        mma_tf32(acc[j], s0[0], s0[1], s0[2], s0[3], p2, q2);
+        mma_tf32(acc[j], s1[0], s1[1], s1[2], s1[3], p0, q0);
+        mma_tf32(acc[j], s0[0], s0[1], s0[2], s0[3], p1, q1);
       }
-      mma_tf32(acc[j], ah[0], ah[1], ah[2], ah[3], bh0, bh1);
+      mma_tf32(acc[j], s0[0], s0[1], s0[2], s0[3], p0, q0);
     }
   }
 
