@@ -86,13 +86,16 @@ int sgtk_graph_create(const uint64_t* node_pointer, const uint32_t* edge_list,
                       int ptr_kind, void* stream, sgtk_graph** out);
 
 /* Row-slice variant for the multi-GPU row-window partition: `num_rows` local
- * rows (a contiguous range of whole 16-row windows of the global graph) whose
- * column ids index a `num_cols`-row feature matrix.  Same semantics otherwise. */
+ * rows, global rows [row_offset, row_offset + num_rows) (row_offset a multiple
+ * of 16: whole windows, so the slice's transform equals the global transform
+ * restricted to it), whose column ids index a `num_cols`-row feature replica.
+ * Kernels write local rows; feature reads use global ids. */
 int sgtk_graph_create_rows(const uint64_t* node_pointer,
                            const uint32_t* edge_list, const float* values,
                            uint64_t num_rows, uint64_t num_cols,
-                           uint64_t num_edges, uint32_t blk_h, uint32_t blk_w,
-                           int ptr_kind, void* stream, sgtk_graph** out);
+                           uint64_t row_offset, uint64_t num_edges,
+                           uint32_t blk_h, uint32_t blk_w, int ptr_kind,
+                           void* stream, sgtk_graph** out);
 
 /* Build from an already-transformed graph's host fields (load_sgt output or a
  * host TransformedGraph).  Fields are trusted to be consistent with the CSR;

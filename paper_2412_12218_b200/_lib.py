@@ -78,7 +78,8 @@ vp = C.c_void_p
 
 _SIGS = {
     "sgtk_graph_create": [vp, vp, vp, u64, u64, u32, u32, C.c_int, vp, C.POINTER(vp)],
-    "sgtk_graph_create_rows": [vp, vp, vp, u64, u64, u64, u32, u32, C.c_int, vp, C.POINTER(vp)],
+    "sgtk_graph_create_rows": [vp, vp, vp, u64, u64, u64, u64, u32, u32, C.c_int, vp,
+                               C.POINTER(vp)],
     "sgtk_graph_import": [vp, vp, vp, u64, u64, u32, u32, vp, vp, vp, vp, C.POINTER(vp)],
     "sgtk_graph_info": [vp, vp],
     "sgtk_graph_device_ptrs": [vp, vp],

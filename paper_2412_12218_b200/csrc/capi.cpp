@@ -89,11 +89,14 @@ int sgtk_graph_create(const uint64_t* np, const uint32_t* el, const float* vals,
 }
 
 int sgtk_graph_create_rows(const uint64_t* np, const uint32_t* el, const float* vals,
-                           uint64_t n_rows, uint64_t n_cols, uint64_t nnz, uint32_t blk_h,
-                           uint32_t blk_w, int kind, void* stream, sgtk_graph** out) {
+                           uint64_t n_rows, uint64_t n_cols, uint64_t row_offset, uint64_t nnz,
+                           uint32_t blk_h, uint32_t blk_w, int kind, void* stream,
+                           sgtk_graph** out) {
   return guard([&] {
     need(out != nullptr, SGTK_ERR, "null output handle");
-    *out = graph_create(np, el, vals, n_rows, n_cols, nnz, blk_h, blk_w, kind, as_stream(stream));
+    need(row_offset + n_rows <= n_cols, SGTK_ERR_SHAPE, "row slice exceeds the column space");
+    *out = graph_create(np, el, vals, n_rows, n_cols, nnz, blk_h, blk_w, kind, as_stream(stream),
+                        row_offset);
   });
 }
 

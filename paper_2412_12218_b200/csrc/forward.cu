@@ -110,8 +110,8 @@ void gcn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint32_t L,
 }
 
 uint64_t agnn_workspace(const sgtk_graph* g, uint64_t d) {
-  return 2 * align256(g->n_rows * ld4(d) * 4) + align256(g->n_rows * 4) +
-         align256(std::max<uint64_t>(g->nnz, 1) * 4) + align256(16 * 4) + align256(g->internal.W * 4);
+  return 2 * align256(g->n_rows * ld4(d) * 4) + align256(g->n_cols * 4) +
+         align256(std::max<uint64_t>(g->nnz, 1) * 4) + align256(16 * 4);
 }
 
 void agnn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d, uint32_t L,
@@ -125,12 +125,13 @@ void agnn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
   float* buf[2];
   buf[0] = reinterpret_cast<float*>(p); p += align256(N * ldb * 4);
   buf[1] = reinterpret_cast<float*>(p); p += align256(N * ldb * 4);
-  float* inv = reinterpret_cast<float*>(p); p += align256(N * 4);
+  float* inv = reinterpret_cast<float*>(p); p += align256(g->n_cols * 4);
   float* logits = reinterpret_cast<float*>(p); p += align256(std::max<uint64_t>(g->nnz, 1) * 4);
-  uint64_t* zeros = reinterpret_cast<uint64_t*>(p); p += align256(16 * 4);
-  uint32_t* cut16 = reinterpret_cast<uint32_t*>(p);
+  uint64_t* zeros = reinterpret_cast<uint64_t*>(p);
+  if (g->n_rows != g->n_cols && L > 1)
+    raise(SGTK_ERR_SHAPE, "agnn_forward: a row-slice graph runs one layer per call "
+                          "(all-gather the slices between layers)");
   CU(cudaMemsetAsync(zeros, 0, 8, s));
-  (void)cut16;
 
   if (L == 0) {
     CU(cudaMemcpy2DAsync(out, ldo * 4, x, ldx * 4, d * 4, N, cudaMemcpyDeviceToDevice, s));
@@ -141,9 +142,10 @@ void agnn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
     const bool last = l + 1 == L;
     float* dst = last ? out : buf[l & 1];
     const uint64_t ldd = last ? ldo : ldb;
-    l2norm_launch(h, N, d, ldh, nullptr, 0, inv, zeros, s);
+    // first layer of a row-slice graph: the input is the full n_cols-row replica
+    l2norm_launch(h, l == 0 ? g->n_cols : N, d, ldh, nullptr, 0, inv, zeros, s);
     if (mode == 1) {
-      agnn_fused_launch(g, h, ldh, d, inv, betas[l], prec, dst, ldd, s);
+      agnn_fused_launch(g, h, ldh, d, inv, betas[l], prec, cut, dst, ldd, s);
     } else {
       // The reference's SDDMM runs on reblock(t, 16) with make_split_plan(t16, ratio)
       // (gnn.cpp:101-102); the 8-wide cut carried over to 16-wide tiles is

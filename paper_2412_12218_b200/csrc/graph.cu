@@ -513,8 +513,9 @@ void build_e2r(sgtk_graph& g, cudaStream_t s) {
 
 sgtk_graph* graph_create(const uint64_t* np, const uint32_t* el, const float* vals, uint64_t n_rows,
                          uint64_t n_cols, uint64_t nnz, uint32_t blk_h, uint32_t blk_w, int kind,
-                         cudaStream_t s) {
+                         cudaStream_t s, uint64_t row_offset) {
   if (blk_h == 0 || blk_w == 0) raise(SGTK_ERR_GEOMETRY, "tile dimensions must be positive");
+  if (row_offset % 16) raise(SGTK_ERR_SHAPE, "row slice must start on a 16-row window boundary");
   if (n_cols > 0xFFFFFFFFull || nnz > 0xFFFFFFFFull)
     raise(SGTK_ERR_OVERFLOW, "graph exceeds 32-bit node/edge ids");
   auto g = std::make_unique<sgtk_graph>();
@@ -522,6 +523,7 @@ sgtk_graph* graph_create(const uint64_t* np, const uint32_t* el, const float* va
   g->n_rows = n_rows;
   g->n_cols = n_cols;
   g->nnz = nnz;
+  g->row_offset = row_offset;
   g->blk_h = blk_h;
   g->blk_w = blk_w;
   load_csr(*g, np, el, vals, kind, s);

@@ -45,6 +45,7 @@ struct Windows {
 // POD view handed to kernels.
 struct DevGraph {
   uint64_t n_rows, n_cols, nnz, W;
+  uint64_t row_offset;  // global id of local row 0 (row-window partition)
   const uint64_t* np;
   const uint32_t* el;
   const float* vals;
@@ -60,7 +61,7 @@ struct DevGraph {
 }  // namespace sgtkcu
 
 struct sgtk_graph {
-  uint64_t n_rows = 0, n_cols = 0, nnz = 0;
+  uint64_t n_rows = 0, n_cols = 0, nnz = 0, row_offset = 0;
   uint32_t blk_h = 16, blk_w = 8;
   bool has_values = false;
   int device = 0;
@@ -85,6 +86,7 @@ struct sgtk_graph {
     v.n_rows = n_rows;
     v.n_cols = n_cols;
     v.nnz = nnz;
+    v.row_offset = row_offset;
     v.W = internal.W;
     v.np = np->as<uint64_t>();
     v.el = el->as<uint32_t>();

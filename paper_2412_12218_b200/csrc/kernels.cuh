@@ -7,7 +7,7 @@ namespace sgtkcu {
 
 sgtk_graph* graph_create(const uint64_t* np, const uint32_t* el, const float* vals, uint64_t n_rows,
                          uint64_t n_cols, uint64_t nnz, uint32_t blk_h, uint32_t blk_w, int kind,
-                         cudaStream_t s);
+                         cudaStream_t s, uint64_t row_offset = 0);
 sgtk_graph* graph_import(const uint64_t* np, const uint32_t* el, const float* vals,
                          uint64_t n_rows, uint64_t nnz, uint32_t blk_h, uint32_t blk_w,
                          const uint32_t* e2c, const uint64_t* wo, const uint32_t* wuc,
@@ -31,8 +31,8 @@ void gemm_launch(const float* a, uint64_t lda, const float* w, uint64_t m, uint6
 void relu_nonfinite_launch(float* x, uint64_t rows, uint64_t cols, uint64_t ld, int relu,
                            uint32_t* nonfinite, cudaStream_t s);
 void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, uint64_t d,
-                       const float* inv_norm, float beta, int prec, float* out, uint64_t ldo,
-                       cudaStream_t s);
+                       const float* inv_norm, float beta, int prec, const uint32_t* cut_dev,
+                       float* out, uint64_t ldo, cudaStream_t s);
 
 // Host-side split plan (make_split_plan, tile_exec.cpp:150-161).
 std::vector<uint32_t> split_plan_host(const sgtk_graph* g, double ratio);

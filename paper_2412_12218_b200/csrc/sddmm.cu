@@ -91,16 +91,19 @@ sddmm_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t n_un
     ea = lower_bound_u32(G.e2c, ca, ea, u.t1 * 16u);
     eb = lower_bound_u32(G.e2c, cb, eb, u.t1 * 16u);
   }
+  // x rows are global ids (row_offset + local row): a row-slice graph reads
+  // the full feature replica.
+  const uint64_t xa = G.row_offset + ra, xb = G.row_offset + rb;
   float ia = 0.f, ib = 0.f;
   if (inv_norm) {
-    ia = va ? inv_norm[ra] : 0.f;
-    ib = vb ? inv_norm[rb] : 0.f;
+    ia = va ? inv_norm[xa] : 0.f;
+    ib = vb ? inv_norm[xb] : 0.f;
   }
   const float* pia = inv_norm ? &ia : nullptr;
   const float* pib = inv_norm ? &ib : nullptr;
 
   Frag<PREC, VEC> A;
-  if (nch == 1) load_a(A, x, ldx, d, ra, rb, va, vb, 0, t, pia, pib);
+  if (nch == 1) load_a(A, x, ldx, d, xa, xb, va, vb, 0, t, pia, pib);
 
   auto emit = [&](float dot, uint64_t pos) {
     const float a = vals ? __ldg(vals + pos) : 1.0f;
@@ -126,7 +129,7 @@ sddmm_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t n_un
     }
     for (uint32_t ch = 0; ch < nch; ++ch) {
       const uint64_t fb = uint64_t(ch) * DK;
-      if (nch > 1) load_a(A, x, ldx, d, ra, rb, va, vb, fb, t, pia, pib);
+      if (nch > 1) load_a(A, x, ldx, d, xa, xb, va, vb, fb, t, pia, pib);
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb) {
         float s0[KS], s1[KS];
@@ -181,7 +184,7 @@ sddmm_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t n_un
       const bool act = half ? i < nbb : i < na;
       const uint64_t e = (half ? cb : ca) + i;
       const uint32_t col = act ? __ldg(G.el + e) : 0u;
-      const uint64_t r = half ? rb : ra;
+      const uint64_t r = half ? xb : xa;
       float part = 0.0f;
       if (act) {
         for (uint32_t ch = 0; ch < nch; ++ch) {

@@ -74,6 +74,7 @@ class DeviceGraph:
         self.info = GraphInfo(*(int(v) for v in a[:5]), int(a[5]), int(a[6]), bool(a[7]),
                               int(a[8]), int(a[9]), int(a[10]))
         self.num_cols = self.info.num_nodes if num_cols is None else num_cols
+        self.row_offset = 0
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -91,7 +92,7 @@ class DeviceGraph:
     # ---- construction ------------------------------------------------------
     @classmethod
     def from_csr(cls, node_pointer, edge_list, values=None, num_nodes=None, blk_h=16, blk_w=8,
-                 num_cols=None) -> "DeviceGraph":
+                 num_cols=None, row_offset=0) -> "DeviceGraph":
         """sgt_transform on the GPU.  numpy inputs are host pointers, CUDA
         tensors device pointers."""
         dev = isinstance(node_pointer, torch.Tensor)
@@ -113,9 +114,11 @@ class DeviceGraph:
                                           blk_h, blk_w, kind, _stream(), C.byref(h)))
         else:
             check(lib().sgtk_graph_create_rows(_ptr(np_), _ptr(el), _ptr(vals), u64(n),
-                                               u64(num_cols), u64(nnz), blk_h, blk_w, kind,
-                                               _stream(), C.byref(h)))
-        return cls(h, num_cols)
+                                               u64(num_cols), u64(row_offset), u64(nnz), blk_h,
+                                               blk_w, kind, _stream(), C.byref(h)))
+        g = cls(h, num_cols)
+        g.row_offset = row_offset
+        return g
 
     @classmethod
     def import_fields(cls, node_pointer, edge_list, values, blk_h, blk_w, edge_to_column,

@@ -295,17 +295,49 @@ def test_agnn_vs_reference(key):
     assert mre(sg.agnn_forward(t, x, betas, precision="tf32"), G[f"{key}_agnn/agnn_tf1"]) <= 2e-3
     assert mre(sg.agnn_forward(t, x, betas, plan=sg.make_split_plan(t, 0.0)),
                G[f"{key}_agnn/agnn_tf0"]) <= TOL_FP32
+    # fused single-pass mode (online softmax; attention never materialised)
+    for ratio in (1.0, 0.5, 0.0):
+        plan = sg.make_split_plan(t, ratio)
+        assert mre(sg.agnn_forward(t, x, betas, plan=plan, mode=1),
+                   G[f"{key}_agnn/agnn_tf0"]) <= TOL_FP32
+    assert mre(sg.agnn_forward(t, x, betas, precision="tf32", mode=1),
+               G[f"{key}_agnn/agnn_tf1"]) <= 2e-3
 
 
-def test_agnn_kats():
+@pytest.mark.parametrize("name,g", big_graphs())
+@pytest.mark.parametrize("mode", [0, 1])
+def test_agnn_large_windows(name, g, mode):
+    # split windows: the fused kernel merges (m, l, O) states across units
+    c = Csr.of(g.num_nodes, g.node_pointer, g.edge_list)
+    t = sg.sgt_transform(g)
+    x = sg.dense_random(g.num_nodes, 32, 3)
+    want, _ = O.agnn_forward(c, x, [1.0, 0.7])
+    assert mre(sg.agnn_forward(t, x, [1.0, 0.7], mode=mode), want) <= TOL_FP32
+    assert mre(sg.agnn_forward(t, x, [1.0, 0.7], plan=sg.make_split_plan(t, 0.4), mode=mode),
+               want) <= TOL_FP32
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_agnn_kats(mode):
     t = sg.sgt_transform(sgcsr(csr("kat_agnn_zero")))
-    out, z = sg.agnn_forward(t, G["kat_agnn_zero/x"], [1.0], return_zeros=True)
+    out, z = sg.agnn_forward(t, G["kat_agnn_zero/x"], [1.0], return_zeros=True, mode=mode)
     assert z == 2
     np.testing.assert_allclose(out, G["kat_agnn_zero/out"], rtol=1e-6)
     # single self-looped node: identity map (test_gnn.cpp:157-164)
     t = sg.sgt_transform(sg.CsrGraph(1, np.array([0, 1]), np.array([0])))
     x = np.array([[0.5, -1.0, 2.0]], np.float32)
-    np.testing.assert_array_equal(sg.agnn_forward(t, x, [1.0] * 4), x)
+    np.testing.assert_array_equal(sg.agnn_forward(t, x, [1.0] * 4, mode=mode), x)
+    # beta = 0: uniform neighbour mean (test_gnn.cpp:166-178), tolerance 1e-5
+    g = sgcsr(csr("rand2"))
+    t = sg.sgt_transform(g)
+    x = G["rand2/x"]
+    deg = np.diff(g.node_pointer.astype(np.int64))
+    rows = np.repeat(np.arange(g.num_nodes), deg)
+    want = np.zeros_like(x, dtype=np.float64)
+    np.add.at(want, rows, x[g.edge_list] / np.maximum(deg, 1)[rows, None])
+    want = np.zeros_like(want) if False else want
+    h = sg.agnn_forward(t, x, [0.0], mode=mode)
+    assert mre(h, want) <= 1e-5
 
 
 def test_gcn_normalize_values_bit_exact():
