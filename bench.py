@@ -161,8 +161,8 @@ def reference_layer_sample(g, h0, beta=1.0, threads=0):
                              values=np.ones(c.num_edges, np.float32))
             logits *= np.float32(beta)
             out = np.zeros(c.num_edges, np.float32)
-            R._ok(R.L.ref_edge_softmax(hc.ptr, logits.ctypes.data, C.c_uint64(c.num_edges),
-                                       out.ctypes.data))
+            R._ok(R.L.ref_edge_softmax(hc.ptr, C.c_void_p(logits.ctypes.data),
+                                       C.c_uint64(c.num_edges), C.c_void_p(out.ctypes.data)))
             return R.spmm(th, c.num_nodes, h0, 1.0, False, threads, values=out)
     except FileNotFoundError:
         from oracle.oracle import Oracle

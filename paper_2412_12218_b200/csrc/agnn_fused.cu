@@ -8,20 +8,24 @@
 //
 // One warp owns a 16-row window (or a slice of its 16-wide tiles).  Per tile:
 //   S  = Q K^T       16x16, Q = z rows of the window (A fragments, registers),
-//                    K = z rows of the tile's 16 unique columns  (2x4 MMAs at d=32)
-//   mask by the tile's 16x16 occupancy bitmap, online softmax per row
+//                    K = z rows of the tile's 16 unique columns
+//   mask by the tile's 16x16 occupancy bitmap, online softmax per row (exp2)
 //   O += P V         P re-used straight from S's accumulator layout (the PV
 //                    MMA's k index is permuted so no shuffle is needed),
-//                    V = h rows of the tile columns              (2x4 MMAs)
+//                    V = h rows of the tile columns
+// The next tile's 16 column ids, bitmap and gathered rows are prefetched into
+// registers while the current tile computes (two tiles in flight per warp).
 // Logits and attention never touch HBM: per layer the kernel reads the
-// bitmaps, the unique-column ids and gathered feature rows (L2-resident at
-// the configs' sizes) and writes N x d — the "fused" lower bound of
-// SURVEY.md §8(d) instead of the unfused chain's 2x4E round trips.
+// bitmaps, the unique-column ids and gathered feature rows and writes N x d —
+// the "fused" lower bound of SURVEY.md §8(d) instead of the unfused chain's
+// E-sized round trips.
 //
-// Tiles at or past the plan's cut are processed edge-by-edge on CUDA cores
-// (dot -> online softmax -> axpy) into the same running state.  Windows split
-// over several warps merge their (m, l, O) states in unit order.
-// Precision: TF32 = RNE-rounded operands; FP32 = the 4-term split (common.cuh).
+// Precision.  TF32: operands RNE-rounded like tf32_round_value.  FP32:
+//   S uses 3xTF32 (q = qh + ql, k = kh + kl, drops ql*kl ~ 2^-22 relative);
+//   PV uses the exact-on-representable 4-term split (common.cuh) so unit
+//   attention reproduces h bit-exactly (test_gnn.cpp:157-164).
+// Tiles at or past the plan's cut go edge-by-edge on CUDA cores into the same
+// running state; windows split over several warps merge (m, l, O) in order.
 
 #include "graph.cuh"
 
@@ -29,6 +33,13 @@ namespace sgtkcu {
 namespace {
 
 constexpr int kWarps = 4;
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 __device__ __forceinline__ uint32_t bits16(const uint4& lo, const uint4& hi, uint32_t r) {
   const uint4& b = r < 8 ? lo : hi;
@@ -46,29 +57,75 @@ __device__ __forceinline__ float quad_sum(float v) {
   return v + __shfl_xor_sync(0xFFFFFFFFu, v, 2);
 }
 
-template <int NB, bool VEC>
-__device__ __forceinline__ void load_row_seg(float (&dst)[NB], const float* __restrict__ h,
-                                             uint64_t ldh, uint64_t row, uint64_t f, uint64_t d,
-                                             bool ok) {
-  const int64_t rem = int64_t(d) - int64_t(f);
-  const int valid = !ok || rem <= 0 ? 0 : (rem > NB ? NB : int(rem));
-  load_seg<NB, VEC>(dst, h + row * ldh + f, valid);
+// NB contiguous floats of row `row` starting at feature f.  FULL: the segment
+// is known in-bounds and 16-byte aligned (d == 8*NB, ld % 4 == 0).
+template <int NB, bool FULL>
+__device__ __forceinline__ void ld_seg(float (&dst)[NB], const float* __restrict__ h, uint64_t ldh,
+                                       uint64_t row, uint64_t f, uint64_t d) {
+  if constexpr (FULL) {
+    load_seg<NB, true>(dst, h + row * ldh + f, NB);
+  } else {
+    const int64_t rem = int64_t(d) - int64_t(f);
+    load_seg<NB, false>(dst, h + row * ldh + f, rem <= 0 ? 0 : (rem > NB ? NB : int(rem)));
+  }
 }
 
-// Online-softmax running state of one row (replicated across its 4 lanes).
+// Running state of one row (replicated over its 4 lanes), log2 domain.
 struct RowState {
   float m, l;
 };
 
-__device__ __forceinline__ void online_update(RowState& st, float tile_max, float& scale) {
+// New row max -> rescale factor for the old (l, O); returns the max to use.
+__device__ __forceinline__ float online_update(RowState& st, float tile_max, float& scale) {
   const float mn = fmaxf(st.m, tile_max);
-  scale = (st.m == -INFINITY) ? 0.0f : expf(st.m - mn);
-  if (mn == -INFINITY) scale = 1.0f;
+  scale = mn == -INFINITY ? 1.0f : ex2(st.m - mn);  // ex2(-inf) = 0
   st.m = mn;
   st.l *= scale;
+  return mn == -INFINITY ? 0.0f : mn;
 }
 
-template <int NB, int PREC, bool VEC>
+// Per-tile gathered operands (registers).
+template <int NB>
+struct TileRegs {
+  float k0[2][NB], k1[2][NB];  // z rows of cols nb*8+g: features t*NB.., (t+4)*NB..
+  float v[2][2][NB];           // h rows of cols kb*8+2t(+1): features g*NB..
+  float ick[2];                // inv_norm of the K columns
+  uint32_t wa, wb;             // bitmap rows g, g+8
+};
+
+template <int NB, bool FULL>
+__device__ __forceinline__ void fetch_tile(TileRegs<NB>& R, const DevGraph& G,
+                                           const float* __restrict__ h, uint64_t ldh, uint64_t d,
+                                           const float* __restrict__ inv, uint64_t ubase,
+                                           uint32_t ucnt, uint64_t tileg, uint32_t tile,
+                                           uint32_t lane, uint32_t g, uint32_t t) {
+  const uint4 blo = __ldg(G.bm16 + 2 * tileg);
+  const uint4 bhi = __ldg(G.bm16 + 2 * tileg + 1);
+  R.wa = bits16(blo, bhi, g);
+  R.wb = bits16(blo, bhi, g + 8);
+  // lanes 0..15 fetch the tile's column ids (ragged lanes reuse column 0 of
+  // the window: finite data, masked out by the bitmap)
+  const uint32_t c = tile * 16u + (lane & 15u);
+  const uint32_t myid = __ldg(G.wuc + ubase + (c < ucnt ? c : 0u));
+  const float myinv = __ldg(inv + myid);
+  uint32_t ck[2], cv[2][2];
+#pragma unroll
+  for (int nb = 0; nb < 2; ++nb) {
+    ck[nb] = __shfl_sync(0xFFFFFFFFu, myid, nb * 8 + g);
+    R.ick[nb] = __shfl_sync(0xFFFFFFFFu, myinv, nb * 8 + g);
+    cv[nb][0] = __shfl_sync(0xFFFFFFFFu, myid, nb * 8 + 2 * t);
+    cv[nb][1] = __shfl_sync(0xFFFFFFFFu, myid, nb * 8 + 2 * t + 1);
+  }
+#pragma unroll
+  for (int nb = 0; nb < 2; ++nb) {
+    ld_seg<NB, FULL>(R.k0[nb], h, ldh, ck[nb], t * NB, d);
+    ld_seg<NB, FULL>(R.k1[nb], h, ldh, ck[nb], (t + 4) * NB, d);
+    ld_seg<NB, FULL>(R.v[nb][0], h, ldh, cv[nb][0], g * NB, d);
+    ld_seg<NB, FULL>(R.v[nb][1], h, ldh, cv[nb][1], g * NB, d);
+  }
+}
+
+template <int NB, int PREC, bool FULL>
 __global__ void __launch_bounds__(kWarps * 32)
 agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t n_units,
                   const uint32_t* __restrict__ thr, const float* __restrict__ h, uint64_t ldh,
@@ -81,25 +138,25 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
   const uint64_t w = u.window;
   const uint64_t ra = w * 16 + g, rb = ra + 8;
   const bool va = ra < G.n_rows, vb = rb < G.n_rows;
-  const uint64_t xa = G.row_offset + ra, xb = G.row_offset + rb;
+  const uint64_t xa = G.row_offset + (va ? ra : 0), xb = G.row_offset + (vb ? rb : 0);
   const uint64_t ubase = G.wo[w];
   const uint32_t ucnt = uint32_t(G.wo[w + 1] - ubase);
   const uint32_t ntiles = (ucnt + 15u) >> 4;
   const uint64_t tbase = G.toff16[w];
   const uint32_t tc_end = thr ? min(u.t1, max(u.t0, thr[w])) : u.t1;
+  const float scale2 = beta * kLog2e;  // logits kept in the log2 domain
 
-  // ---- Q fragments: z rows (h * inv), features k*NB + s  (s = k-step) ----
+  // ---- Q fragments: z rows, features k*NB + s (s = k-step) ---------------
   const float ia = va ? __ldg(inv + xa) : 0.0f, ib = vb ? __ldg(inv + xb) : 0.0f;
-  uint32_t q0[4][NB], q1[4][NB], q2[4][NB];  // [a0 a1 a2 a3][s], z = q0 + q1 + q2
+  uint32_t qh[4][NB], ql[4][NB];  // [a0 a1 a2 a3][s]
   {
     float s_[NB];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const bool rowa = (q & 1) == 0;
-      load_row_seg<NB, VEC>(s_, h, ldh, rowa ? xa : xb, (q < 2 ? t : t + 4) * NB, d,
-                            rowa ? va : vb);
+      ld_seg<NB, FULL>(s_, h, ldh, rowa ? xa : xb, (q < 2 ? t : t + 4) * NB, d);
 #pragma unroll
-      for (int i = 0; i < NB; ++i) split_d<PREC>(s_[i] * (rowa ? ia : ib), q0[q][i], q1[q][i], q2[q][i]);
+      for (int i = 0; i < NB; ++i) split_s<PREC>(s_[i] * (rowa ? ia : ib), qh[q][i], ql[q][i]);
     }
   }
 
@@ -108,64 +165,53 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
   for (int j = 0; j < NB; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.0f;
   RowState sa{-INFINITY, 0.0f}, sb{-INFINITY, 0.0f};
 
-  uint64_t ca = 0, cb = 0, ea = 0, eb = 0;  // CSR cursors (CUDA-core path only)
-
-  // ---------------- tensor-core path -------------------------------------
+  // ---------------- tensor-core path (software-pipelined) ------------------
+  TileRegs<NB> cur, nxt;
+  if (u.t0 < tc_end)
+    fetch_tile<NB, FULL>(cur, G, h, ldh, d, inv, ubase, ucnt, tbase + u.t0, u.t0, lane, g, t);
   for (uint32_t tile = u.t0; tile < tc_end; ++tile) {
-    const uint4 blo = __ldg(G.bm16 + 2 * (tbase + tile));
-    const uint4 bhi = __ldg(G.bm16 + 2 * (tbase + tile) + 1);
-    const uint32_t wa = bits16(blo, bhi, g), wb = bits16(blo, bhi, g + 8);
-
-    // S = Q K^T: B fragment of n-block nb is tile column nb*8 + g.
+    if (tile + 1 < tc_end)
+      fetch_tile<NB, FULL>(nxt, G, h, ldh, d, inv, ubase, ucnt, tbase + tile + 1, tile + 1, lane,
+                           g, t);
+    // S = Q K^T  (n-block nb: tile columns nb*8 + g)
     float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-    for (int nb = 0; nb < 2; ++nb) {
-      const uint32_t c = tile * 16u + nb * 8u + g;
-      const bool ok = c < ucnt;
-      const uint32_t col = ok ? __ldg(G.wuc + ubase + c) : 0u;
-      const float ic = ok ? __ldg(inv + col) : 0.0f;
-      float k0[NB], k1[NB];
-      load_row_seg<NB, VEC>(k0, h, ldh, col, t * NB, d, ok);
-      load_row_seg<NB, VEC>(k1, h, ldh, col, (t + 4) * NB, d, ok);
+    for (int i = 0; i < NB; ++i) {
 #pragma unroll
-      for (int i = 0; i < NB; ++i) {
+      for (int nb = 0; nb < 2; ++nb) {
         uint32_t b0, c0, b1, c1;
-        split_s<PREC>(k0[i] * ic, b0, c0);
-        split_s<PREC>(k1[i] * ic, b1, c1);
+        split_s<PREC>(cur.k0[nb][i] * cur.ick[nb], b0, c0);
+        split_s<PREC>(cur.k1[nb][i] * cur.ick[nb], b1, c1);
         if constexpr (PREC == SGTK_FP32) {
-          mma_tf32(s[nb], q2[0][i], q2[1][i], q2[2][i], q2[3][i], b0, b1);
-          mma_tf32(s[nb], q0[0][i], q0[1][i], q0[2][i], q0[3][i], c0, c1);
-          mma_tf32(s[nb], q1[0][i], q1[1][i], q1[2][i], q1[3][i], b0, b1);
+          mma_tf32(s[nb], ql[0][i], ql[1][i], ql[2][i], ql[3][i], b0, b1);
+          mma_tf32(s[nb], qh[0][i], qh[1][i], qh[2][i], qh[3][i], c0, c1);
         }
-        mma_tf32(s[nb], q0[0][i], q0[1][i], q0[2][i], q0[3][i], b0, b1);
+        mma_tf32(s[nb], qh[0][i], qh[1][i], qh[2][i], qh[3][i], b0, b1);
       }
     }
-    // logits, mask (C layout: s[nb][q] is row g(+8), column nb*8 + 2t + (q&1))
+    // logits (log2 domain), mask.  s[nb][q]: row g (q<2) / g+8, col nb*8+2t+(q&1)
     float tma = -INFINITY, tmb = -INFINITY;
 #pragma unroll
     for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const uint32_t c = nb * 8u + 2u * t + (q & 1u);
-        const bool edge = ((q < 2 ? wa : wb) >> c) & 1u;
+        const bool edge = ((q < 2 ? cur.wa : cur.wb) >> c) & 1u;
         float v = s[nb][q];
         if constexpr (PREC == SGTK_TF32) v = tf32_rne(v);  // tf32(1) * tf32(dot)
-        v = edge ? v * beta : -INFINITY;
+        v = edge ? v * scale2 : -INFINITY;
         s[nb][q] = v;
         if (q < 2) tma = fmaxf(tma, v); else tmb = fmaxf(tmb, v);
       }
-    tma = quad_max(tma);
-    tmb = quad_max(tmb);
     float sca, scb;
-    online_update(sa, tma, sca);
-    online_update(sb, tmb, scb);
+    const float ma = online_update(sa, quad_max(tma), sca);
+    const float mb = online_update(sb, quad_max(tmb), scb);
     float pa = 0.f, pb = 0.f;
 #pragma unroll
     for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const float m = q < 2 ? sa.m : sb.m;
-        const float p = s[nb][q] == -INFINITY ? 0.0f : expf(s[nb][q] - m);
+        const float p = ex2(s[nb][q] - (q < 2 ? ma : mb));  // masked: ex2(-inf) = 0
         s[nb][q] = p;
         if (q < 2) pa += p; else pb += p;
       }
@@ -185,18 +231,11 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
       split_s<PREC>(s[kb][2], p0[1], p1[1]);  // (g+8, 2t)   -> a1
       split_s<PREC>(s[kb][1], p0[2], p1[2]);  // (g,   2t+1) -> a2
       split_s<PREC>(s[kb][3], p0[3], p1[3]);  // (g+8, 2t+1) -> a3
-      const uint32_t c0 = tile * 16u + kb * 8u + 2u * t, c1 = c0 + 1u;
-      const bool ok0 = c0 < ucnt, ok1 = c1 < ucnt;
-      const uint32_t col0 = ok0 ? __ldg(G.wuc + ubase + c0) : 0u;
-      const uint32_t col1 = ok1 ? __ldg(G.wuc + ubase + c1) : 0u;
-      float v0[NB], v1[NB];
-      load_row_seg<NB, VEC>(v0, h, ldh, col0, g * NB, d, ok0);
-      load_row_seg<NB, VEC>(v1, h, ldh, col1, g * NB, d, ok1);
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
         uint32_t x0, x1, x2, y0, y1, y2;
-        split_d<PREC>(v0[j], x0, x1, x2);
-        split_d<PREC>(v1[j], y0, y1, y2);
+        split_d<PREC>(cur.v[kb][0][j], x0, x1, x2);
+        split_d<PREC>(cur.v[kb][1][j], y0, y1, y2);
         if constexpr (PREC == SGTK_FP32) {
           mma_tf32(o[j], p0[0], p0[1], p0[2], p0[3], x2, y2);
           mma_tf32(o[j], p1[0], p1[1], p1[2], p1[3], x0, y0);
@@ -205,9 +244,11 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
         mma_tf32(o[j], p0[0], p0[1], p0[2], p0[3], x0, y0);
       }
     }
+    cur = nxt;
   }
 
   // ---------------- CUDA-core path: edges of tiles [tc_end, t1) -----------
+  uint64_t ca = 0, cb = 0, ea = 0, eb = 0;
   if (tc_end < u.t1) {
     ca = va ? G.np[ra] : 0; ea = va ? G.np[ra + 1] : 0;
     cb = vb ? G.np[rb] : 0; eb = vb ? G.np[rb + 1] : 0;
@@ -228,18 +269,15 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
         const uint64_t e = (half ? cb : ca) + i;
         const uint32_t col = act ? __ldg(G.el + e) : 0u;
         const float ic = act ? __ldg(inv + col) : 0.0f;
-        // dot(z_row, z_col) over this lane's Q features, reduced over the quad
         float k0[NB], k1[NB];
-        load_row_seg<NB, VEC>(k0, h, ldh, col, t * NB, d, act);
-        load_row_seg<NB, VEC>(k1, h, ldh, col, (t + 4) * NB, d, act);
+        ld_seg<NB, FULL>(k0, h, ldh, col, t * NB, d);
+        ld_seg<NB, FULL>(k1, h, ldh, col, (t + 4) * NB, d);
         float part = 0.0f;
+        const int qa = half ? 1 : 0;
 #pragma unroll
         for (int s_ = 0; s_ < NB; ++s_) {
-          const int qa = half ? 1 : 0;
-          const float z0 = __uint_as_float(q0[qa][s_]) + __uint_as_float(q1[qa][s_]) +
-                           __uint_as_float(q2[qa][s_]);
-          const float z1 = __uint_as_float(q0[qa + 2][s_]) + __uint_as_float(q1[qa + 2][s_]) +
-                           __uint_as_float(q2[qa + 2][s_]);
+          const float z0 = __uint_as_float(qh[qa][s_]) + __uint_as_float(ql[qa][s_]);
+          const float z1 = __uint_as_float(qh[qa + 2][s_]) + __uint_as_float(ql[qa + 2][s_]);
           float y0 = k0[s_] * ic, y1 = k1[s_] * ic;
           if constexpr (PREC == SGTK_TF32) { y0 = tf32_rne(y0); y1 = tf32_rne(y1); }
           part = fmaf(z0, y0, part);
@@ -247,16 +285,14 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
         }
         float logit = quad_sum(part);
         if constexpr (PREC == SGTK_TF32) logit = tf32_rne(logit);
-        logit = act ? logit * beta : -INFINITY;
+        logit = act ? logit * scale2 : -INFINITY;
         RowState& st = half ? sb : sa;
         float sc;
-        online_update(st, logit, sc);
-        const float p = act ? expf(logit - st.m) : 0.0f;
+        const float m = online_update(st, logit, sc);
+        const float p = ex2(logit - m);
         st.l += p;
         float vs[2 * NB];
-        const int64_t rem = int64_t(d) - int64_t(2u * t * NB);
-        const int valid = !act || rem <= 0 ? 0 : (rem > 2 * NB ? 2 * NB : int(rem));
-        load_seg<2 * NB, VEC>(vs, h + uint64_t(col) * ldh + 2u * t * NB, valid);
+        ld_seg<2 * NB, FULL>(vs, h, ldh, col, 2u * t * NB, d);
 #pragma unroll
         for (int j = 0; j < NB; ++j) {
           float x0 = vs[j], x1 = vs[NB + j];
@@ -280,10 +316,10 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
       va_[j] = o[j][0] * la; va_[NB + j] = o[j][1] * la;
       vb_[j] = o[j][2] * lb; vb_[NB + j] = o[j][3] * lb;
     }
-    if (va) store_seg<2 * NB, VEC>(out + ra * ldo + sf, va_, svalid);
-    if (vb) store_seg<2 * NB, VEC>(out + rb * ldo + sf, vb_, svalid);
+    if (va) store_seg<2 * NB, FULL>(out + ra * ldo + sf, va_, svalid);
+    if (vb) store_seg<2 * NB, FULL>(out + rb * ldo + sf, vb_, svalid);
   } else {
-    // partial state: O[16][8*NB], then m[16], l[16]
+    // partial state: O[16][8*NB], then m[16] (log2 domain), l[16]
     float* P = partial + uint64_t(u.slot) * pstride;
     float va_[2 * NB], vb_[2 * NB];
 #pragma unroll
@@ -320,7 +356,7 @@ __global__ void agnn_merge_kernel(const ReduceItem* __restrict__ items, uint64_t
       const float* P = partial + uint64_t(it.slot0 + k) * pstride;
       const float m = P[16 * 8 * NB + rr];
       if (m == -INFINITY) continue;
-      const float sc = expf(m - M);
+      const float sc = exp2f(m - M);
       L += P[16 * 8 * NB + 16 + rr] * sc;
       O += P[rr * 8 * NB + f] * sc;
     }
@@ -328,7 +364,7 @@ __global__ void agnn_merge_kernel(const ReduceItem* __restrict__ items, uint64_t
   }
 }
 
-template <int NB, int PREC, bool VEC>
+template <int NB, int PREC, bool FULL>
 void launch(const sgtk_graph* g, const uint32_t* thr, const float* h, uint64_t ldh, uint64_t d,
             const float* inv, float beta, float* out, uint64_t ldo, cudaStream_t s) {
   const auto& P = g->plan16;
@@ -336,7 +372,7 @@ void launch(const sgtk_graph* g, const uint32_t* thr, const float* h, uint64_t l
   float* partial = nullptr;
   if (P.n_slots)
     CU(cudaMallocAsync(reinterpret_cast<void**>(&partial), uint64_t(P.n_slots) * pstride * 4, s));
-  agnn_fused_kernel<NB, PREC, VEC><<<(P.n_units + kWarps - 1) / kWarps, kWarps * 32, 0, s>>>(
+  agnn_fused_kernel<NB, PREC, FULL><<<(P.n_units + kWarps - 1) / kWarps, kWarps * 32, 0, s>>>(
       g->view(), P.units->as<WorkUnit>(), P.n_units, thr, h, ldh, d, inv, beta, out, ldo, partial,
       pstride);
   CU_LAUNCH("agnn_fused_kernel");
@@ -349,14 +385,14 @@ void launch(const sgtk_graph* g, const uint32_t* thr, const float* h, uint64_t l
 }
 
 template <int NB>
-void dispatch(int prec, bool vec, const sgtk_graph* g, const uint32_t* thr, const float* h,
+void dispatch(int prec, bool full, const sgtk_graph* g, const uint32_t* thr, const float* h,
               uint64_t ldh, uint64_t d, const float* inv, float beta, float* out, uint64_t ldo,
               cudaStream_t s) {
   if (prec == SGTK_FP32) {
-    if (vec) launch<NB, SGTK_FP32, true>(g, thr, h, ldh, d, inv, beta, out, ldo, s);
+    if (full) launch<NB, SGTK_FP32, true>(g, thr, h, ldh, d, inv, beta, out, ldo, s);
     else launch<NB, SGTK_FP32, false>(g, thr, h, ldh, d, inv, beta, out, ldo, s);
   } else {
-    if (vec) launch<NB, SGTK_TF32, true>(g, thr, h, ldh, d, inv, beta, out, ldo, s);
+    if (full) launch<NB, SGTK_TF32, true>(g, thr, h, ldh, d, inv, beta, out, ldo, s);
     else launch<NB, SGTK_TF32, false>(g, thr, h, ldh, d, inv, beta, out, ldo, s);
   }
 }
@@ -373,11 +409,12 @@ void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, uint64
   DevBuf cut_keep;
   const uint32_t* thr = internal_cut(g, cut_dev, 16, s, cut_keep);
   const int nb = d <= 16 ? 2 : d <= 32 ? 4 : 8;
-  const bool vec = ldh % 4 == 0 && ldo % 4 == 0 && reinterpret_cast<uintptr_t>(h) % 16 == 0 &&
-                   reinterpret_cast<uintptr_t>(out) % 16 == 0;
-  if (nb == 2) dispatch<2>(prec, vec, g, thr, h, ldh, d, inv, beta, out, ldo, s);
-  else if (nb == 4) dispatch<4>(prec, vec, g, thr, h, ldh, d, inv, beta, out, ldo, s);
-  else dispatch<8>(prec, vec, g, thr, h, ldh, d, inv, beta, out, ldo, s);
+  const bool full = uint64_t(8 * nb) == d && ldh % 4 == 0 && ldo % 4 == 0 &&
+                    reinterpret_cast<uintptr_t>(h) % 16 == 0 &&
+                    reinterpret_cast<uintptr_t>(out) % 16 == 0;
+  if (nb == 2) dispatch<2>(prec, full, g, thr, h, ldh, d, inv, beta, out, ldo, s);
+  else if (nb == 4) dispatch<4>(prec, full, g, thr, h, ldh, d, inv, beta, out, ldo, s);
+  else dispatch<8>(prec, full, g, thr, h, ldh, d, inv, beta, out, ldo, s);
 }
 
 }  // namespace sgtkcu
