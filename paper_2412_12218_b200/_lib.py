@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsgtk_b200.so")
+LIB_PATH = os.environ.get("SGTK_LIB", os.path.join(HERE, "libsgtk_b200.so"))
 
 # sgtk_status -> exception (mirrors the reference pybind mapping,
 # /root/reference/proj/src/python/bindings.cpp:88-100).

@@ -89,48 +89,55 @@ template <int NB>
 struct TileRegs {
   float k0[2][NB], k1[2][NB];  // z rows of cols nb*8+g: features t*NB.., (t+4)*NB..
   float v[2][2][NB];           // h rows of cols kb*8+2t(+1): features g*NB..
-  float ick[2];                // inv_norm of the K columns
   uint32_t wa, wb;             // bitmap rows g, g+8
 };
 
+// Column ids straight from window_unique_cols (no shuffles on the address
+// chain); ragged lanes of the last tile reuse the window's last column
+// (finite data, masked out by the bitmap).  K rows come from z (the
+// normalised rows, materialised by the row-norm kernel as the reference does,
+// gnn.cpp:109), V rows from h.
 template <int NB, bool FULL>
 __device__ __forceinline__ void fetch_tile(TileRegs<NB>& R, const DevGraph& G,
-                                           const float* __restrict__ h, uint64_t ldh, uint64_t d,
-                                           const float* __restrict__ inv, uint64_t ubase,
-                                           uint32_t ucnt, uint64_t tileg, uint32_t tile,
-                                           uint32_t lane, uint32_t g, uint32_t t) {
+                                           const float* __restrict__ h,
+                                           const float* __restrict__ z, uint64_t ldh,
+                                           uint64_t ldz, uint64_t d,
+                                           uint64_t ubase, uint32_t ucnt, uint64_t tileg,
+                                           uint32_t tile, uint32_t g, uint32_t t) {
   const uint4 blo = __ldg(G.bm16 + 2 * tileg);
   const uint4 bhi = __ldg(G.bm16 + 2 * tileg + 1);
   R.wa = bits16(blo, bhi, g);
   R.wb = bits16(blo, bhi, g + 8);
-  // lanes 0..15 fetch the tile's column ids (ragged lanes reuse column 0 of
-  // the window: finite data, masked out by the bitmap)
-  const uint32_t c = tile * 16u + (lane & 15u);
-  const uint32_t myid = __ldg(G.wuc + ubase + (c < ucnt ? c : 0u));
-  const float myinv = __ldg(inv + myid);
+  const uint32_t last = ucnt - 1u;
+  const uint32_t* ids = G.wuc + ubase;
   uint32_t ck[2], cv[2][2];
 #pragma unroll
   for (int nb = 0; nb < 2; ++nb) {
-    ck[nb] = __shfl_sync(0xFFFFFFFFu, myid, nb * 8 + g);
-    R.ick[nb] = __shfl_sync(0xFFFFFFFFu, myinv, nb * 8 + g);
-    cv[nb][0] = __shfl_sync(0xFFFFFFFFu, myid, nb * 8 + 2 * t);
-    cv[nb][1] = __shfl_sync(0xFFFFFFFFu, myid, nb * 8 + 2 * t + 1);
+    const uint32_t c0 = tile * 16u + nb * 8u;
+    ck[nb] = __ldg(ids + min(c0 + g, last));
+    cv[nb][0] = __ldg(ids + min(c0 + 2u * t, last));
+    cv[nb][1] = __ldg(ids + min(c0 + 2u * t + 1u, last));
   }
 #pragma unroll
   for (int nb = 0; nb < 2; ++nb) {
-    ld_seg<NB, FULL>(R.k0[nb], h, ldh, ck[nb], t * NB, d);
-    ld_seg<NB, FULL>(R.k1[nb], h, ldh, ck[nb], (t + 4) * NB, d);
+    ld_seg<NB, FULL>(R.k0[nb], z, ldz, ck[nb], t * NB, d);
+    ld_seg<NB, FULL>(R.k1[nb], z, ldz, ck[nb], (t + 4) * NB, d);
     ld_seg<NB, FULL>(R.v[nb][0], h, ldh, cv[nb][0], g * NB, d);
     ld_seg<NB, FULL>(R.v[nb][1], h, ldh, cv[nb][1], g * NB, d);
   }
 }
 
+#ifndef SGTK_AGNN_MINB
+#define SGTK_AGNN_MINB 1
+#endif
+
 template <int NB, int PREC, bool FULL>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, SGTK_AGNN_MINB)
 agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t n_units,
-                  const uint32_t* __restrict__ thr, const float* __restrict__ h, uint64_t ldh,
-                  uint64_t d, const float* __restrict__ inv, float beta, float* __restrict__ out,
-                  uint64_t ldo, float* __restrict__ partial, uint64_t pstride) {
+                  const uint32_t* __restrict__ thr, const float* __restrict__ h,
+                  const float* __restrict__ z, uint64_t ldh, uint64_t ldz, uint64_t d, float beta,
+                  float* __restrict__ out, uint64_t ldo, float* __restrict__ partial,
+                  uint64_t pstride) {
   const uint32_t wid = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (wid >= n_units) return;
   const WorkUnit u = units[wid];
@@ -147,16 +154,16 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
   const float scale2 = beta * kLog2e;  // logits kept in the log2 domain
 
   // ---- Q fragments: z rows, features k*NB + s (s = k-step) ---------------
-  const float ia = va ? __ldg(inv + xa) : 0.0f, ib = vb ? __ldg(inv + xb) : 0.0f;
   uint32_t qh[4][NB], ql[4][NB];  // [a0 a1 a2 a3][s]
   {
     float s_[NB];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const bool rowa = (q & 1) == 0;
-      ld_seg<NB, FULL>(s_, h, ldh, rowa ? xa : xb, (q < 2 ? t : t + 4) * NB, d);
+      ld_seg<NB, FULL>(s_, z, ldz, rowa ? xa : xb, (q < 2 ? t : t + 4) * NB, d);
+      const bool ok = rowa ? va : vb;
 #pragma unroll
-      for (int i = 0; i < NB; ++i) split_s<PREC>(s_[i] * (rowa ? ia : ib), qh[q][i], ql[q][i]);
+      for (int i = 0; i < NB; ++i) split_s<PREC>(ok ? s_[i] : 0.0f, qh[q][i], ql[q][i]);
     }
   }
 
@@ -166,13 +173,7 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
   RowState sa{-INFINITY, 0.0f}, sb{-INFINITY, 0.0f};
 
   // ---------------- tensor-core path (software-pipelined) ------------------
-  TileRegs<NB> cur, nxt;
-  if (u.t0 < tc_end)
-    fetch_tile<NB, FULL>(cur, G, h, ldh, d, inv, ubase, ucnt, tbase + u.t0, u.t0, lane, g, t);
-  for (uint32_t tile = u.t0; tile < tc_end; ++tile) {
-    if (tile + 1 < tc_end)
-      fetch_tile<NB, FULL>(nxt, G, h, ldh, d, inv, ubase, ucnt, tbase + tile + 1, tile + 1, lane,
-                           g, t);
+  auto process = [&](const TileRegs<NB>& cur) {
     // S = Q K^T  (n-block nb: tile columns nb*8 + g)
     float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
@@ -180,8 +181,8 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb) {
         uint32_t b0, c0, b1, c1;
-        split_s<PREC>(cur.k0[nb][i] * cur.ick[nb], b0, c0);
-        split_s<PREC>(cur.k1[nb][i] * cur.ick[nb], b1, c1);
+        split_s<PREC>(cur.k0[nb][i], b0, c0);
+        split_s<PREC>(cur.k1[nb][i], b1, c1);
         if constexpr (PREC == SGTK_FP32) {
           mma_tf32(s[nb], ql[0][i], ql[1][i], ql[2][i], ql[3][i], b0, b1);
           mma_tf32(s[nb], qh[0][i], qh[1][i], qh[2][i], qh[3][i], c0, c1);
@@ -198,7 +199,7 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
         const uint32_t c = nb * 8u + 2u * t + (q & 1u);
         const bool edge = ((q < 2 ? cur.wa : cur.wb) >> c) & 1u;
         float v = s[nb][q];
-        if constexpr (PREC == SGTK_TF32) v = tf32_rne(v);  // tf32(1) * tf32(dot)
+        if constexpr (PREC == SGTK_TF32) v = __uint_as_float(tf32_op(v));  // tf32(1)*tf32(dot)
         v = edge ? v * scale2 : -INFINITY;
         s[nb][q] = v;
         if (q < 2) tma = fmaxf(tma, v); else tmb = fmaxf(tmb, v);
@@ -217,10 +218,14 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
       }
     sa.l += quad_sum(pa);
     sb.l += quad_sum(pb);
+    // the row maxima settle after a few tiles: skip the rescale when no row
+    // of the window changed its max (warp-uniform vote)
+    if (!__all_sync(0xFFFFFFFFu, sca == 1.0f && scb == 1.0f)) {
 #pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      o[j][0] *= sca; o[j][1] *= sca;
-      o[j][2] *= scb; o[j][3] *= scb;
+      for (int j = 0; j < NB; ++j) {
+        o[j][0] *= sca; o[j][1] *= sca;
+        o[j][2] *= scb; o[j][3] *= scb;
+      }
     }
     // O += P V.  k-step kb covers tile columns kb*8 + {2t, 2t+1} for A's
     // k = {t, t+4}: exactly the columns this lane's S accumulator holds.
@@ -244,6 +249,16 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
         mma_tf32(o[j], p0[0], p0[1], p0[2], p0[3], x0, y0);
       }
     }
+  };
+
+  // the next tile's ids/bitmap/rows are in flight while the current computes
+  TileRegs<NB> cur, nxt;
+  if (u.t0 < tc_end)
+    fetch_tile<NB, FULL>(cur, G, h, z, ldh, ldz, d, ubase, ucnt, tbase + u.t0, u.t0, g, t);
+  for (uint32_t tile = u.t0; tile < tc_end; ++tile) {
+    if (tile + 1 < tc_end)
+      fetch_tile<NB, FULL>(nxt, G, h, z, ldh, ldz, d, ubase, ucnt, tbase + tile + 1, tile + 1, g, t);
+    process(cur);
     cur = nxt;
   }
 
@@ -268,17 +283,16 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
         const bool act = half ? i < nbb : i < na;
         const uint64_t e = (half ? cb : ca) + i;
         const uint32_t col = act ? __ldg(G.el + e) : 0u;
-        const float ic = act ? __ldg(inv + col) : 0.0f;
         float k0[NB], k1[NB];
-        ld_seg<NB, FULL>(k0, h, ldh, col, t * NB, d);
-        ld_seg<NB, FULL>(k1, h, ldh, col, (t + 4) * NB, d);
+        ld_seg<NB, FULL>(k0, z, ldz, col, t * NB, d);
+        ld_seg<NB, FULL>(k1, z, ldz, col, (t + 4) * NB, d);
         float part = 0.0f;
         const int qa = half ? 1 : 0;
 #pragma unroll
         for (int s_ = 0; s_ < NB; ++s_) {
           const float z0 = __uint_as_float(qh[qa][s_]) + __uint_as_float(ql[qa][s_]);
           const float z1 = __uint_as_float(qh[qa + 2][s_]) + __uint_as_float(ql[qa + 2][s_]);
-          float y0 = k0[s_] * ic, y1 = k1[s_] * ic;
+          float y0 = k0[s_], y1 = k1[s_];
           if constexpr (PREC == SGTK_TF32) { y0 = tf32_rne(y0); y1 = tf32_rne(y1); }
           part = fmaf(z0, y0, part);
           part = fmaf(z1, y1, part);
@@ -365,16 +379,16 @@ __global__ void agnn_merge_kernel(const ReduceItem* __restrict__ items, uint64_t
 }
 
 template <int NB, int PREC, bool FULL>
-void launch(const sgtk_graph* g, const uint32_t* thr, const float* h, uint64_t ldh, uint64_t d,
-            const float* inv, float beta, float* out, uint64_t ldo, cudaStream_t s) {
+void launch(const sgtk_graph* g, const uint32_t* thr, const float* h, uint64_t ldh, const float* z,
+            uint64_t ldz, uint64_t d, float beta, float* out, uint64_t ldo, cudaStream_t s) {
   const auto& P = g->plan16;
   const uint64_t pstride = 16 * 8 * NB + 32;
   float* partial = nullptr;
   if (P.n_slots)
     CU(cudaMallocAsync(reinterpret_cast<void**>(&partial), uint64_t(P.n_slots) * pstride * 4, s));
   agnn_fused_kernel<NB, PREC, FULL><<<(P.n_units + kWarps - 1) / kWarps, kWarps * 32, 0, s>>>(
-      g->view(), P.units->as<WorkUnit>(), P.n_units, thr, h, ldh, d, inv, beta, out, ldo, partial,
-      pstride);
+      g->view(), P.units->as<WorkUnit>(), P.n_units, thr, h, z, ldh, ldz, d, beta, out, ldo,
+      partial, pstride);
   CU_LAUNCH("agnn_fused_kernel");
   if (P.n_reduce) {
     agnn_merge_kernel<NB><<<P.n_reduce, 256, 0, s>>>(P.reduce->as<ReduceItem>(), g->n_rows,
@@ -386,21 +400,21 @@ void launch(const sgtk_graph* g, const uint32_t* thr, const float* h, uint64_t l
 
 template <int NB>
 void dispatch(int prec, bool full, const sgtk_graph* g, const uint32_t* thr, const float* h,
-              uint64_t ldh, uint64_t d, const float* inv, float beta, float* out, uint64_t ldo,
-              cudaStream_t s) {
+              uint64_t ldh, const float* z, uint64_t ldz, uint64_t d, float beta, float* out,
+              uint64_t ldo, cudaStream_t s) {
   if (prec == SGTK_FP32) {
-    if (full) launch<NB, SGTK_FP32, true>(g, thr, h, ldh, d, inv, beta, out, ldo, s);
-    else launch<NB, SGTK_FP32, false>(g, thr, h, ldh, d, inv, beta, out, ldo, s);
+    if (full) launch<NB, SGTK_FP32, true>(g, thr, h, ldh, z, ldz, d, beta, out, ldo, s);
+    else launch<NB, SGTK_FP32, false>(g, thr, h, ldh, z, ldz, d, beta, out, ldo, s);
   } else {
-    if (full) launch<NB, SGTK_TF32, true>(g, thr, h, ldh, d, inv, beta, out, ldo, s);
-    else launch<NB, SGTK_TF32, false>(g, thr, h, ldh, d, inv, beta, out, ldo, s);
+    if (full) launch<NB, SGTK_TF32, true>(g, thr, h, ldh, z, ldz, d, beta, out, ldo, s);
+    else launch<NB, SGTK_TF32, false>(g, thr, h, ldh, z, ldz, d, beta, out, ldo, s);
   }
 }
 
 }  // namespace
 
-void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, uint64_t d,
-                       const float* inv, float beta, int prec, const uint32_t* cut_dev,
+void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, const float* z,
+                       uint64_t ldz, uint64_t d, float beta, int prec, const uint32_t* cut_dev,
                        float* out, uint64_t ldo, cudaStream_t s) {
   if (prec != SGTK_FP32 && prec != SGTK_TF32)
     raise(SGTK_ERR_RANGE, "agnn_forward: precision must be FP32 or TF32");
@@ -409,12 +423,13 @@ void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, uint64
   DevBuf cut_keep;
   const uint32_t* thr = internal_cut(g, cut_dev, 16, s, cut_keep);
   const int nb = d <= 16 ? 2 : d <= 32 ? 4 : 8;
-  const bool full = uint64_t(8 * nb) == d && ldh % 4 == 0 && ldo % 4 == 0 &&
+  const bool full = uint64_t(8 * nb) == d && ldh % 4 == 0 && ldz % 4 == 0 && ldo % 4 == 0 &&
                     reinterpret_cast<uintptr_t>(h) % 16 == 0 &&
+                    reinterpret_cast<uintptr_t>(z) % 16 == 0 &&
                     reinterpret_cast<uintptr_t>(out) % 16 == 0;
-  if (nb == 2) dispatch<2>(prec, full, g, thr, h, ldh, d, inv, beta, out, ldo, s);
-  else if (nb == 4) dispatch<4>(prec, full, g, thr, h, ldh, d, inv, beta, out, ldo, s);
-  else dispatch<8>(prec, full, g, thr, h, ldh, d, inv, beta, out, ldo, s);
+  if (nb == 2) dispatch<2>(prec, full, g, thr, h, ldh, z, ldz, d, beta, out, ldo, s);
+  else if (nb == 4) dispatch<4>(prec, full, g, thr, h, ldh, z, ldz, d, beta, out, ldo, s);
+  else dispatch<8>(prec, full, g, thr, h, ldh, z, ldz, d, beta, out, ldo, s);
 }
 
 }  // namespace sgtkcu

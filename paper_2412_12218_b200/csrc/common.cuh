@@ -138,11 +138,20 @@ __device__ __forceinline__ void split3(float v, uint32_t& p0, uint32_t& p1, uint
   p2 = __float_as_uint(r - __uint_as_float(p1));
 }
 
+// MMA operand rounding in TF32 mode: RNE like tf32_round_value for every
+// finite value (one F2FP); +-inf saturates instead of passing through, which
+// only matters for non-finite inputs (documented in DESIGN.md).
+__device__ __forceinline__ uint32_t tf32_op(float v) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return r;
+}
+
 // Structure operand per precision: TF32 -> (rne, -), FP32 -> split2.
 template <int PREC>
 __device__ __forceinline__ void split_s(float x, uint32_t& p0, uint32_t& p1) {
   if constexpr (PREC == SGTK_TF32) {
-    p0 = __float_as_uint(tf32_rne(x));
+    p0 = tf32_op(x);
     p1 = 0u;
   } else {
     split2(x, p0, p1);
@@ -152,7 +161,7 @@ __device__ __forceinline__ void split_s(float x, uint32_t& p0, uint32_t& p1) {
 template <int PREC>
 __device__ __forceinline__ void split_d(float x, uint32_t& p0, uint32_t& p1, uint32_t& p2) {
   if constexpr (PREC == SGTK_TF32) {
-    p0 = __float_as_uint(tf32_rne(x));
+    p0 = tf32_op(x);
     p1 = p2 = 0u;
   } else {
     split3(x, p0, p1, p2);

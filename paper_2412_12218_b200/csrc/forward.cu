@@ -111,6 +111,7 @@ void gcn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint32_t L,
 
 uint64_t agnn_workspace(const sgtk_graph* g, uint64_t d) {
   return 2 * align256(g->n_rows * ld4(d) * 4) + align256(g->n_cols * 4) +
+         align256(g->n_cols * ld4(d) * 4) +
          align256(std::max<uint64_t>(g->nnz, 1) * 4) + align256(16 * 4);
 }
 
@@ -127,6 +128,7 @@ void agnn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
   buf[1] = reinterpret_cast<float*>(p); p += align256(N * ldb * 4);
   float* inv = reinterpret_cast<float*>(p); p += align256(g->n_cols * 4);
   float* logits = reinterpret_cast<float*>(p); p += align256(std::max<uint64_t>(g->nnz, 1) * 4);
+  float* zbuf = reinterpret_cast<float*>(p); p += align256(g->n_cols * ld4(d) * 4);
   uint64_t* zeros = reinterpret_cast<uint64_t*>(p);
   if (g->n_rows != g->n_cols && L > 1)
     raise(SGTK_ERR_SHAPE, "agnn_forward: a row-slice graph runs one layer per call "
@@ -143,10 +145,12 @@ void agnn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
     float* dst = last ? out : buf[l & 1];
     const uint64_t ldd = last ? ldo : ldb;
     // first layer of a row-slice graph: the input is the full n_cols-row replica
-    l2norm_launch(h, l == 0 ? g->n_cols : N, d, ldh, nullptr, 0, inv, zeros, s);
     if (mode == 1) {
-      agnn_fused_launch(g, h, ldh, d, inv, betas[l], prec, cut, dst, ldd, s);
+      // z = h * inv_norm materialised (as the reference does, gnn.cpp:109)
+      l2norm_launch(h, l == 0 ? g->n_cols : N, d, ldh, zbuf, ldb, inv, zeros, s);
+      agnn_fused_launch(g, h, ldh, zbuf, ldb, d, betas[l], prec, cut, dst, ldd, s);
     } else {
+      l2norm_launch(h, l == 0 ? g->n_cols : N, d, ldh, nullptr, 0, inv, zeros, s);
       // The reference's SDDMM runs on reblock(t, 16) with make_split_plan(t16, ratio)
       // (gnn.cpp:101-102); the 8-wide cut carried over to 16-wide tiles is
       // the same ratio up to floor rounding.
