@@ -177,6 +177,11 @@ int sgtk_sddmm(const sgtk_graph* g, const float* x_dev, uint64_t ldx,
 int sgtk_edge_softmax(const sgtk_graph* g, const float* logits_dev,
                       float* out_dev, void* stream);
 
+/* edge_softmax on a bare device CSR (no transform needed): node_pointer_dev
+ * u64[n+1]; gnn.cpp:54-72 takes a CsrGraph, not a TransformedGraph. */
+int sgtk_csr_softmax(const uint64_t* node_pointer_dev, uint64_t num_nodes,
+                     const float* logits_dev, float* out_dev, void* stream);
+
 /* l2_normalize_rows (gnn.hpp:45-46, gnn.cpp:74-91).  z_dev may be NULL (only
  * inv_norm_dev f32[rows] = float(1/sqrt(sum h^2)), 0 for zero rows, is written);
  * zero_rows_dev (u64, accumulated, may be NULL) counts all-zero rows. */
@@ -232,6 +237,25 @@ int sgtk_gcn_normalize_values(const uint64_t* node_pointer_dev,
                               const uint32_t* edge_list_dev,
                               uint64_t num_nodes, float* vals_dev,
                               void* stream);
+
+/* normalize_graph (graph_io.hpp:33, graph_io.cpp:195-259) on the GPU:
+ * dedupe (values summed in input order), symmetrize (missing reverse edges
+ * take the forward value), add_self_loops (missing (i,i), value 1.0), result
+ * sorted-unique CSR; bit-exact with the reference.  `values` may be NULL.
+ * Synchronous; the result is an opaque device CSR. */
+typedef struct sgtk_csr sgtk_csr;
+int sgtk_normalize_graph(const uint64_t* node_pointer, const uint32_t* edge_list,
+                         const float* values, uint64_t num_nodes, uint64_t num_edges,
+                         int symmetrize, int add_self_loops, int dedupe,
+                         int ptr_kind, void* stream, sgtk_csr** out);
+/* {num_nodes, num_edges, has_values} */
+int sgtk_csr_info(const sgtk_csr* c, uint64_t info[3]);
+/* host copies (vals ignored when the graph is unweighted; any may be NULL) */
+int sgtk_csr_download(const sgtk_csr* c, uint64_t* node_pointer,
+                      uint32_t* edge_list, float* values);
+/* device views: [0] node_pointer [1] edge_list [2] values|NULL */
+int sgtk_csr_device_ptrs(const sgtk_csr* c, const void* ptrs[3]);
+void sgtk_csr_destroy(sgtk_csr* c);
 
 /* tf32_round_value (tile_exec.hpp:64, tile_exec.cpp:131-142), device,
  * elementwise, in-place allowed. */

@@ -236,6 +236,11 @@ int sgtk_edge_softmax(const sgtk_graph* g, const float* logits, float* out, void
   });
 }
 
+int sgtk_csr_softmax(const uint64_t* np, uint64_t n, const float* logits, float* out,
+                     void* stream) {
+  return guard([&] { csr_softmax_launch(np, n, logits, out, as_stream(stream)); });
+}
+
 int sgtk_l2_normalize_rows(const float* h, uint64_t rows, uint64_t cols, uint64_t ldh, float* z,
                            uint64_t ldz, float* inv, uint64_t* zeros, void* stream) {
   return guard([&] { l2norm_launch(h, rows, cols, ldh, z, ldz, inv, zeros, as_stream(stream)); });
@@ -284,6 +289,51 @@ int sgtk_agnn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_
 int sgtk_gcn_normalize_values(const uint64_t* np, const uint32_t* el, uint64_t n, float* vals,
                               void* stream) {
   return guard([&] { gcn_normalize_launch(np, el, n, vals, as_stream(stream)); });
+}
+
+int sgtk_normalize_graph(const uint64_t* np, const uint32_t* el, const float* vals, uint64_t n,
+                         uint64_t nnz, int symmetrize, int loops, int dedupe, int kind,
+                         void* stream, sgtk_csr** out) {
+  return guard([&] {
+    need(out != nullptr && np != nullptr, SGTK_ERR, "null argument");
+    *out = normalize_graph(np, el, vals, n, nnz, symmetrize, loops, dedupe, kind,
+                           as_stream(stream));
+  });
+}
+
+int sgtk_csr_info(const sgtk_csr* c, uint64_t info[3]) {
+  return guard([&] {
+    need(c != nullptr, SGTK_ERR, "null csr handle");
+    info[0] = c->n;
+    info[1] = c->nnz;
+    info[2] = c->has_values ? 1 : 0;
+  });
+}
+
+int sgtk_csr_download(const sgtk_csr* c, uint64_t* np, uint32_t* el, float* vals) {
+  return guard([&] {
+    need(c != nullptr, SGTK_ERR, "null csr handle");
+    if (np) CU(cudaMemcpy(np, c->np.p, (c->n + 1) * 8, cudaMemcpyDeviceToHost));
+    if (el && c->nnz) CU(cudaMemcpy(el, c->el.p, c->nnz * 4, cudaMemcpyDeviceToHost));
+    if (vals && c->has_values && c->nnz)
+      CU(cudaMemcpy(vals, c->vals.p, c->nnz * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int sgtk_csr_device_ptrs(const sgtk_csr* c, const void* ptrs[3]) {
+  return guard([&] {
+    need(c != nullptr, SGTK_ERR, "null csr handle");
+    ptrs[0] = c->np.p;
+    ptrs[1] = c->el.p;
+    ptrs[2] = c->has_values ? c->vals.p : nullptr;
+  });
+}
+
+void sgtk_csr_destroy(sgtk_csr* c) {
+  if (c) {
+    cudaDeviceSynchronize();
+    delete c;
+  }
 }
 
 int sgtk_tf32_round(const float* in, float* out, uint64_t n, void* stream) {

@@ -1,2 +1,568 @@
-// C++ drop-in (sgtk:: namespace) — see include/sgtk/api.hpp
+// C++ drop-in (include/sgtk/api.hpp): the reference's public C++ interface
+// over the C ABI.  Host-side argument checks throw the reference's exception
+// types (/root/reference/proj/include/sgtk/errors.hpp:10-51) before any launch;
+// every kernel runs on the GPU through include/sgtk_cuda.h.  Scalar helpers
+// (validate_csr, csr_from_triples, make_split_plan, block_stats, reblock's
+// O(windows) arithmetic, tf32_round_value on one float, file I/O) stay on the
+// host like the reference's.
 
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <bit>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+
+#include "sgtk/api.hpp"
+#include "sgtk_cuda.h"
+
+#define SGTK_EXPORT __attribute__((visibility("default")))
+
+namespace sgtk {
+namespace {
+
+[[noreturn]] void throw_status(int rc) {
+  const std::string m = sgtk_last_error();
+  switch (rc) {
+    case SGTK_ERR_IO: throw IoError(m);
+    case SGTK_ERR_PARSE: throw ParseError(m, 0);
+    case SGTK_ERR_OVERFLOW: throw OverflowError(m);
+    case SGTK_ERR_DEGREE: throw DegreeError(m);
+    case SGTK_ERR_GEOMETRY: throw GeometryError(m);
+    case SGTK_ERR_INDEX: throw IndexError(m);
+    case SGTK_ERR_RANGE: throw RangeError(m);
+    case SGTK_ERR_SHAPE: throw ShapeError(m);
+    case SGTK_ERR_NONFINITE: throw NonFiniteError(m);
+    default: throw Error(m);
+  }
+}
+inline void ck(int rc) {
+  if (rc) throw_status(rc);
+}
+inline void cuck(cudaError_t e) {
+  if (e != cudaSuccess) throw Error(std::string("CUDA: ") + cudaGetErrorString(e));
+}
+
+// RAII device array
+template <class T>
+struct Dev {
+  T* p = nullptr;
+  size_t n = 0;
+  explicit Dev(size_t count) : n(count) {
+    if (count) cuck(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+  }
+  Dev(const T* host, size_t count) : Dev(count) {
+    if (count) cuck(cudaMemcpy(p, host, count * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  Dev(const Dev&) = delete;
+  Dev& operator=(const Dev&) = delete;
+  ~Dev() {
+    if (p) cudaFree(p);
+  }
+  void get(T* host) const {
+    if (n) cuck(cudaMemcpy(host, p, n * sizeof(T), cudaMemcpyDeviceToHost));
+  }
+};
+
+// Device graph cached on a TransformedGraph (its `device` member), tagged
+// with a fingerprint of the host fields it was built from.
+struct DeviceCache {
+  std::shared_ptr<sgtk_graph> g;
+  const void* el_data;
+  size_t nnz;
+  uint64_t block_counter;
+  uint32_t blk_w;
+};
+
+std::shared_ptr<sgtk_graph> own(sgtk_graph* g) {
+  return std::shared_ptr<sgtk_graph>(g, [](sgtk_graph* p) { sgtk_graph_destroy(p); });
+}
+
+sgtk_graph* device_of(const TransformedGraph& t) {
+  if (t.device) {
+    auto* c = static_cast<DeviceCache*>(t.device.get());
+    if (c->el_data == t.csr.edge_list.data() && c->nnz == t.csr.num_edges() &&
+        c->block_counter == t.block_counter && c->blk_w == t.geometry.blk_w)
+      return c->g.get();
+  }
+  sgtk_graph* h = nullptr;
+  const auto& g = t.csr;
+  ck(sgtk_graph_import(g.node_pointer.data(), g.edge_list.data(),
+                       g.has_values() ? g.values.data() : nullptr, g.num_nodes, g.num_edges(),
+                       t.geometry.blk_h, t.geometry.blk_w, t.edge_to_column.data(),
+                       t.window_offsets.data(), t.window_unique_cols.data(), nullptr, &h));
+  auto cache = std::make_shared<DeviceCache>(
+      DeviceCache{own(h), g.edge_list.data(), g.num_edges(), t.block_counter, t.geometry.blk_w});
+  t.device = cache;
+  return h;
+}
+
+void attach(TransformedGraph& t, std::shared_ptr<sgtk_graph> g) {
+  t.device = std::make_shared<DeviceCache>(DeviceCache{std::move(g), t.csr.edge_list.data(),
+                                                       t.csr.num_edges(), t.block_counter,
+                                                       t.geometry.blk_w});
+}
+
+// tile_exec.cpp:35-42
+void check_plan(const TransformedGraph& t, const HybridSplitPlan& plan) {
+  if (plan.per_window_tile_cut.size() != t.num_windows())
+    throw ShapeError("split plan window count does not match transform");
+  for (size_t w = 0; w < t.num_windows(); ++w)
+    if (plan.per_window_tile_cut[w] > t.block_partition[w])
+      throw ShapeError("split plan cut exceeds tiles in window");
+}
+
+// nullptr when every tile is on the tensor-core path (ratio 1 plan)
+std::unique_ptr<Dev<uint32_t>> upload_cut(const TransformedGraph& t, const HybridSplitPlan& plan) {
+  if (plan.per_window_tile_cut == t.block_partition) return nullptr;
+  return std::make_unique<Dev<uint32_t>>(plan.per_window_tile_cut.data(),
+                                         plan.per_window_tile_cut.size());
+}
+
+int prec_of(Precision p) { return p == Precision::Tf32 ? SGTK_TF32 : SGTK_FP32; }
+
+}  // namespace
+
+// ---------------------------------------------------------------- csr_graph
+SGTK_EXPORT void validate_csr(const CsrGraph& g, bool require_sorted_unique) {
+  if (g.node_pointer.size() != g.num_nodes + 1)
+    throw Error("csr: node_pointer length must be num_nodes + 1");
+  if (g.node_pointer.front() != 0) throw Error("csr: node_pointer[0] != 0");
+  if (g.node_pointer.back() != g.num_edges())
+    throw Error("csr: node_pointer end does not match edge count");
+  for (size_t i = 0; i < g.num_nodes; ++i)
+    if (g.node_pointer[i] > g.node_pointer[i + 1]) throw Error("csr: node_pointer not non-decreasing");
+  for (NodeId c : g.edge_list)
+    if (size_t(c) >= g.num_nodes) throw Error("csr: column id out of range");
+  if (require_sorted_unique)
+    for (size_t r = 0; r < g.num_nodes; ++r)
+      for (auto e = g.row_begin(r) + 1; e < g.row_end(r); ++e)
+        if (g.edge_list[e - 1] >= g.edge_list[e])
+          throw Error("csr: columns not strictly ascending within a row");
+  if (!g.values.empty()) {
+    if (g.values.size() != g.num_edges()) throw Error("csr: values length does not match edge count");
+    for (float v : g.values)
+      if (!std::isfinite(v)) throw Error("csr: non-finite edge value");
+  }
+}
+
+SGTK_EXPORT CsrGraph csr_from_triples(size_t num_nodes, std::vector<Triple> triples,
+                                      bool with_values) {
+  std::stable_sort(triples.begin(), triples.end(), [](const Triple& a, const Triple& b) {
+    return a.row != b.row ? a.row < b.row : a.col < b.col;
+  });
+  CsrGraph g;
+  g.num_nodes = num_nodes;
+  g.node_pointer.assign(num_nodes + 1, 0);
+  for (const Triple& t : triples) {
+    ++g.node_pointer[t.row + 1];
+    g.edge_list.push_back(t.col);
+    if (with_values) g.values.push_back(t.value);
+  }
+  for (size_t i = 0; i < num_nodes; ++i) g.node_pointer[i + 1] += g.node_pointer[i];
+  return g;
+}
+
+// ------------------------------------------------------------ sgt_transform
+SGTK_EXPORT TransformedGraph sgt_transform(const CsrGraph& g, TileGeometry geom, int) {
+  if (geom.blk_h == 0 || geom.blk_w == 0) throw GeometryError("tile dimensions must be positive");
+  if (g.node_pointer.size() != g.num_nodes + 1)
+    throw Error("csr: node_pointer length must be num_nodes + 1");
+  if (g.has_values() && g.values.size() != g.num_edges())
+    throw Error("csr: values length does not match edge count");
+  sgtk_graph* h = nullptr;
+  ck(sgtk_graph_create(g.node_pointer.data(), g.edge_list.data(),
+                       g.has_values() ? g.values.data() : nullptr, g.num_nodes, g.num_edges(),
+                       geom.blk_h, geom.blk_w, SGTK_PTR_HOST, nullptr, &h));
+  auto dg = own(h);
+  uint64_t info[11];
+  ck(sgtk_graph_info(h, info));
+  TransformedGraph t;
+  t.csr = g;
+  t.geometry = geom;
+  t.edge_to_row.resize(info[1]);
+  t.edge_to_column.resize(info[1]);
+  t.block_partition.resize(info[2]);
+  t.window_offsets.resize(info[2] + 1);
+  t.window_unique_cols.resize(info[3]);
+  t.block_counter = info[4];
+  ck(sgtk_graph_download(h, t.edge_to_row.data(), t.edge_to_column.data(), t.block_partition.data(),
+                         t.window_offsets.data(), t.window_unique_cols.data()));
+  attach(t, std::move(dg));
+  return t;
+}
+
+SGTK_EXPORT TransformedGraph reblock(const TransformedGraph& t, uint32_t new_blk_w) {
+  if (new_blk_w == 0) throw GeometryError("tile width must be positive");
+  TransformedGraph out = t;
+  out.device.reset();
+  out.geometry.blk_w = new_blk_w;
+  out.block_counter = 0;
+  for (size_t w = 0; w < t.num_windows(); ++w) {
+    const uint64_t u = t.window_offsets[w + 1] - t.window_offsets[w];
+    out.block_partition[w] = uint32_t((u + new_blk_w - 1) / new_blk_w);
+    out.block_counter += out.block_partition[w];
+  }
+  if (t.device) {  // share the resident arrays (edge maps are unchanged)
+    sgtk_graph* h = nullptr;
+    ck(sgtk_graph_reblock(device_of(t), new_blk_w, nullptr, &h));
+    attach(out, own(h));
+  }
+  return out;
+}
+
+SGTK_EXPORT BlockStats block_stats(const TransformedGraph& t) {
+  BlockStats s;
+  s.block_counter = t.block_counter;
+  s.capacity = t.block_counter * t.geometry.blk_h * t.geometry.blk_w;
+  s.nnz = t.csr.num_edges();
+  s.mean_tile_density = s.capacity ? double(s.nnz) / double(s.capacity) : 0.0;
+  return s;
+}
+
+// ---------------------------------------------------------------- tile_exec
+SGTK_EXPORT HybridSplitPlan make_split_plan(const TransformedGraph& t, double ratio) {
+  if (!(ratio >= 0.0 && ratio <= 1.0)) throw RangeError("split ratio must be within [0, 1]");
+  HybridSplitPlan p;
+  p.ratio = ratio;
+  p.per_window_tile_cut.resize(t.num_windows());
+  for (size_t w = 0; w < t.num_windows(); ++w)
+    p.per_window_tile_cut[w] = uint32_t(std::floor(ratio * double(t.block_partition[w])));
+  return p;
+}
+
+SGTK_EXPORT GatheredTile gather_tile(const TransformedGraph& t, size_t window, size_t tile) {
+  if (window >= t.num_windows()) throw IndexError("gather_tile: window out of range");
+  if (tile >= t.block_partition[window]) throw IndexError("gather_tile: tile out of range");
+  GatheredTile out{DenseMatrix(t.geometry.blk_h, t.geometry.blk_w),
+                   std::vector<NodeId>(t.geometry.blk_w)};
+  ck(sgtk_gather_tile(device_of(t), window, tile, out.a_tile.data.data(), out.x_index.data()));
+  return out;
+}
+
+SGTK_EXPORT DenseMatrix spmm_hybrid(const TransformedGraph& t, const DenseMatrix& x,
+                                    const HybridSplitPlan& plan, Precision prec, int,
+                                    std::span<const float> edge_values) {
+  const CsrGraph& g = t.csr;
+  if (x.rows != g.num_nodes) throw ShapeError("spmm_hybrid: x.rows != num_nodes");
+  check_plan(t, plan);
+  if (!edge_values.empty() && edge_values.size() != g.num_edges())
+    throw ShapeError("edge value override length does not match edge count");
+  DenseMatrix out(g.num_nodes, x.cols);
+  if (!g.num_nodes || !x.cols) return out;
+  sgtk_graph* dg = device_of(t);
+  Dev<float> xd(x.data.data(), x.data.size()), od(out.data.size());
+  auto cut = upload_cut(t, plan);
+  std::unique_ptr<Dev<float>> ev;
+  if (!edge_values.empty()) ev = std::make_unique<Dev<float>>(edge_values.data(), edge_values.size());
+  Dev<uint32_t> flag(1);
+  cuck(cudaMemset(flag.p, 0, 4));
+  ck(sgtk_spmm(dg, xd.p, x.cols, x.cols, cut ? cut->p : nullptr, ev ? ev->p : nullptr,
+               prec_of(prec), od.p, x.cols, flag.p, nullptr));
+  uint32_t bad = 0;
+  flag.get(&bad);
+  if (bad) throw NonFiniteError("spmm_hybrid: output contains NaN or Inf");
+  od.get(out.data.data());
+  return out;
+}
+
+SGTK_EXPORT EdgeValList sddmm_hybrid(const TransformedGraph& t, const DenseMatrix& x,
+                                     const DenseMatrix& y, const HybridSplitPlan& plan,
+                                     Precision prec, int, std::span<const float> edge_values) {
+  const CsrGraph& g = t.csr;
+  if (x.rows != g.num_nodes || y.rows != g.num_nodes)
+    throw ShapeError("sddmm_hybrid: feature rows != num_nodes");
+  if (x.cols != y.cols) throw ShapeError("sddmm_hybrid: x.cols != y.cols");
+  check_plan(t, plan);
+  if (!edge_values.empty() && edge_values.size() != g.num_edges())
+    throw ShapeError("edge value override length does not match edge count");
+  EdgeValList out(g.num_edges(), 0.0f);
+  if (!g.num_edges()) return out;
+  sgtk_graph* dg = device_of(t);
+  Dev<float> xd(x.data.data(), x.data.size()), yd(y.data.data(), y.data.size()), od(out.size());
+  auto cut = upload_cut(t, plan);
+  std::unique_ptr<Dev<float>> ev;
+  if (!edge_values.empty()) ev = std::make_unique<Dev<float>>(edge_values.data(), edge_values.size());
+  ck(sgtk_sddmm(dg, xd.p, x.cols, yd.p, y.cols, x.cols, cut ? cut->p : nullptr,
+                ev ? ev->p : nullptr, prec_of(prec), 1.0f, od.p, nullptr));
+  od.get(out.data());
+  return out;
+}
+
+// tile_exec.cpp:131-142 on one host float (the scalar helper)
+SGTK_EXPORT float tf32_round_value(float v) {
+  uint32_t u = std::bit_cast<uint32_t>(v);
+  if ((u & 0x7F800000u) == 0x7F800000u) return v;
+  u = (u + 0x0FFFu + ((u >> 13) & 1u)) & 0xFFFFE000u;
+  if ((u & 0x7F800000u) == 0x7F800000u) u = (u & 0x80000000u) | 0x7F7FE000u;
+  return std::bit_cast<float>(u);
+}
+
+SGTK_EXPORT DenseMatrix tf32_round(const DenseMatrix& m) {
+  DenseMatrix out(m.rows, m.cols);
+  if (m.data.empty()) return out;
+  Dev<float> d(m.data.data(), m.data.size());
+  ck(sgtk_tf32_round(d.p, d.p, m.data.size(), nullptr));
+  d.get(out.data.data());
+  return out;
+}
+
+// ---------------------------------------------------------------------- gnn
+SGTK_EXPORT DenseMatrix gcn_forward(const TransformedGraph& t, const DenseMatrix& x,
+                                    const std::vector<GcnLayerParams>& layers,
+                                    const HybridSplitPlan& plan, Precision prec, int) {
+  if (x.rows != t.csr.num_nodes) throw ShapeError("gcn_forward: x.rows != num_nodes");
+  std::vector<uint64_t> dims{x.cols};
+  std::vector<float> w;
+  std::vector<int> relu;
+  for (const auto& l : layers) {
+    if (l.weight.rows != dims.back()) throw ShapeError("gcn_forward: weight shape does not chain");
+    dims.push_back(l.weight.cols);
+    w.insert(w.end(), l.weight.data.begin(), l.weight.data.end());
+    relu.push_back(l.apply_relu ? 1 : 0);
+  }
+  check_plan(t, plan);
+  if (layers.empty()) {
+    if (!x.all_finite()) throw NonFiniteError("gcn_forward: output contains NaN or Inf");
+    return x;
+  }
+  DenseMatrix out(x.rows, dims.back());
+  if (!x.rows) return out;
+  sgtk_graph* dg = device_of(t);
+  const uint64_t wsb = sgtk_gcn_workspace(dg, uint32_t(layers.size()), dims.data());
+  Dev<char> ws(wsb);
+  Dev<float> xd(x.data.data(), x.data.size()), wd(w.data(), w.size()), od(out.data.size());
+  auto cut = upload_cut(t, plan);
+  ck(sgtk_gcn_forward(dg, xd.p, x.cols, uint32_t(layers.size()), dims.data(), wd.p, relu.data(),
+                      cut ? cut->p : nullptr, prec_of(prec), 2, ws.p, wsb, od.p, out.cols, nullptr));
+  od.get(out.data.data());
+  return out;
+}
+
+SGTK_EXPORT EdgeValList edge_softmax(const CsrGraph& g, const EdgeValList& logits) {
+  if (logits.size() != g.num_edges()) throw ShapeError("edge_softmax: logits length != num_edges");
+  EdgeValList out(logits.size(), 0.0f);
+  if (logits.empty()) return out;
+  Dev<uint64_t> np(g.node_pointer.data(), g.node_pointer.size());
+  Dev<float> ld(logits.data(), logits.size()), od(out.size());
+  cuck(cudaMemset(od.p, 0, out.size() * 4));
+  ck(sgtk_csr_softmax(np.p, g.num_nodes, ld.p, od.p, nullptr));
+  od.get(out.data());
+  return out;
+}
+
+SGTK_EXPORT DenseMatrix l2_normalize_rows(const DenseMatrix& m, size_t* zero_rows) {
+  DenseMatrix out(m.rows, m.cols);
+  uint64_t z = 0;
+  if (m.rows) {
+    Dev<float> md(m.data.data(), m.data.size()), od(std::max<size_t>(m.data.size(), 1));
+    Dev<float> inv(m.rows);
+    Dev<uint64_t> zd(1);
+    cuck(cudaMemset(zd.p, 0, 8));
+    ck(sgtk_l2_normalize_rows(md.p, m.rows, m.cols, m.cols, od.p, m.cols, inv.p, zd.p, nullptr));
+    if (!m.data.empty()) cuck(cudaMemcpy(out.data.data(), od.p, m.data.size() * 4, cudaMemcpyDeviceToHost));
+    zd.get(&z);
+  }
+  if (zero_rows) *zero_rows = z;
+  return out;
+}
+
+SGTK_EXPORT DenseMatrix agnn_forward(const TransformedGraph& t, const DenseMatrix& x,
+                                     const std::vector<AgnnLayerParams>& layers,
+                                     const HybridSplitPlan& plan, Precision prec, int,
+                                     size_t* zero_norm_rows) {
+  if (x.rows != t.csr.num_nodes) throw ShapeError("agnn_forward: x.rows != num_nodes");
+  check_plan(t, plan);
+  DenseMatrix out(x.rows, x.cols);
+  uint64_t zeros = 0;
+  if (x.rows && x.cols) {
+    sgtk_graph* dg = device_of(t);
+    std::vector<float> betas;
+    for (const auto& l : layers) betas.push_back(l.beta);
+    const uint64_t wsb = sgtk_agnn_workspace(dg, x.cols);
+    Dev<char> ws(wsb);
+    Dev<float> xd(x.data.data(), x.data.size()), od(out.data.size());
+    auto cut = upload_cut(t, plan);
+    const int mode = x.cols <= 64 ? 1 : 0;  // fused single pass when it fits
+    ck(sgtk_agnn_forward(dg, xd.p, x.cols, x.cols, uint32_t(layers.size()), betas.data(),
+                         cut ? cut->p : nullptr, prec_of(prec), mode, ws.p, wsb, od.p, x.cols,
+                         &zeros, nullptr));
+    od.get(out.data.data());
+  } else {
+    out = x;
+  }
+  if (zero_norm_rows) *zero_norm_rows = zeros;
+  return out;
+}
+
+SGTK_EXPORT std::vector<GcnLayerParams> random_gcn_layers(size_t in_dim, size_t hidden_dim,
+                                                          size_t out_dim, size_t num_layers,
+                                                          uint64_t seed) {
+  std::vector<GcnLayerParams> layers;
+  size_t d = in_dim;
+  for (size_t l = 0; l < num_layers; ++l) {
+    const bool last = l + 1 == num_layers;
+    const size_t o = last ? out_dim : hidden_dim;
+    layers.push_back({DenseMatrix::random(d, o, seed + l, -0.1f, 0.1f), !last});
+    d = o;
+  }
+  return layers;
+}
+
+// Weight files (gnn.hpp:56-59): raw f32 + one-line JSON sidecar
+// {"rows": R, "cols": C, "apply_relu": bool}.
+SGTK_EXPORT GcnLayerParams load_gcn_layer(const std::string& path) {
+  std::ifstream side(path + ".json");
+  if (!side) throw IoError("cannot open '" + path + ".json'");
+  std::stringstream ss;
+  ss << side.rdbuf();
+  const std::string js = ss.str();
+  auto field = [&](const char* key) -> std::string {
+    const std::string k = std::string("\"") + key + "\"";
+    const size_t p = js.find(k);
+    if (p == std::string::npos) return {};
+    size_t c = js.find(':', p + k.size());
+    if (c == std::string::npos) throw IoError("bad weight sidecar");
+    size_t b = js.find_first_not_of(" \t", c + 1), e = js.find_first_of(",}", b);
+    return js.substr(b, e - b);
+  };
+  const std::string r = field("rows"), c = field("cols"), relu = field("apply_relu");
+  if (r.empty() || c.empty()) throw IoError("bad weight sidecar: missing rows/cols");
+  GcnLayerParams layer{DenseMatrix(std::stoull(r), std::stoull(c)),
+                       relu.empty() ? true : relu.rfind("true", 0) == 0};
+  std::ifstream bin(path, std::ios::binary);
+  if (!bin) throw IoError("cannot open '" + path + "'");
+  bin.read(reinterpret_cast<char*>(layer.weight.data.data()),
+           std::streamsize(layer.weight.data.size() * sizeof(float)));
+  if (!bin || bin.get() != std::ifstream::traits_type::eof())
+    throw IoError("weight file size does not match sidecar shape");
+  return layer;
+}
+
+SGTK_EXPORT void save_gcn_layer(const GcnLayerParams& layer, const std::string& path) {
+  std::ofstream bin(path, std::ios::binary);
+  if (!bin) throw IoError("cannot write '" + path + "'");
+  bin.write(reinterpret_cast<const char*>(layer.weight.data.data()),
+            std::streamsize(layer.weight.data.size() * sizeof(float)));
+  if (!bin) throw IoError("write failed for '" + path + "'");
+  std::ofstream side(path + ".json");
+  side << "{\"rows\":" << layer.weight.rows << ",\"cols\":" << layer.weight.cols
+       << ",\"apply_relu\":" << (layer.apply_relu ? "true" : "false") << "}\n";
+  if (!side) throw IoError("write failed for '" + path + ".json'");
+}
+
+// ----------------------------------------------------------------- graph_io
+SGTK_EXPORT CsrGraph normalize_graph(const CsrGraph& g, NormalizeOpts opts) {
+  validate_csr(g, /*require_sorted_unique=*/false);
+  sgtk_csr* c = nullptr;
+  ck(sgtk_normalize_graph(g.node_pointer.data(), g.edge_list.data(),
+                          g.has_values() ? g.values.data() : nullptr, g.num_nodes, g.num_edges(),
+                          opts.symmetrize, opts.add_self_loops, opts.dedupe, SGTK_PTR_HOST, nullptr,
+                          &c));
+  std::unique_ptr<sgtk_csr, void (*)(sgtk_csr*)> hold(c, sgtk_csr_destroy);
+  uint64_t info[3];
+  ck(sgtk_csr_info(c, info));
+  CsrGraph out;
+  out.num_nodes = info[0];
+  out.node_pointer.resize(info[0] + 1);
+  out.edge_list.resize(info[1]);
+  if (info[2]) out.values.resize(info[1]);
+  ck(sgtk_csr_download(c, out.node_pointer.data(), out.edge_list.data(),
+                       info[2] ? out.values.data() : nullptr));
+  return out;
+}
+
+SGTK_EXPORT CsrGraph gcn_normalize_values(const CsrGraph& g) {
+  validate_csr(g);
+  CsrGraph out = g;
+  out.values.assign(g.num_edges(), 0.0f);
+  if (!g.num_nodes) return out;
+  Dev<uint64_t> np(g.node_pointer.data(), g.node_pointer.size());
+  Dev<uint32_t> el(g.edge_list.data(), g.edge_list.size());
+  Dev<float> v(std::max<size_t>(g.num_edges(), 1));
+  ck(sgtk_gcn_normalize_values(np.p, el.p, g.num_nodes, v.p, nullptr));
+  if (g.num_edges()) cuck(cudaMemcpy(out.values.data(), v.p, g.num_edges() * 4, cudaMemcpyDeviceToHost));
+  return out;
+}
+
+// ----------------------------------------------------------------- sgt_file
+// "SGT1" container, byte-compatible with sgt_file.cpp:47-107.
+namespace {
+template <class T>
+void wpod(std::ostream& os, T v) {
+  os.write(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+template <class T>
+void warr(std::ostream& os, const std::vector<T>& v) {
+  os.write(reinterpret_cast<const char*>(v.data()), std::streamsize(v.size() * sizeof(T)));
+}
+template <class T>
+T rpod(std::istream& is) {
+  T v{};
+  is.read(reinterpret_cast<char*>(&v), sizeof(T));
+  if (!is) throw IoError("SGT1: truncated header");
+  return v;
+}
+template <class T>
+void rarr(std::istream& is, std::vector<T>& v, uint64_t n) {
+  if (n > (uint64_t(1) << 40) / sizeof(T)) throw IoError("SGT1: truncated payload");
+  v.resize(n);
+  is.read(reinterpret_cast<char*>(v.data()), std::streamsize(n * sizeof(T)));
+  if (!is) throw IoError("SGT1: truncated payload");
+}
+}  // namespace
+
+SGTK_EXPORT void save_sgt(const TransformedGraph& t, const std::string& path) {
+  std::ofstream os(path, std::ios::binary);
+  if (!os) throw IoError("cannot write '" + path + "'");
+  os.write("SGT1", 4);
+  wpod<uint32_t>(os, t.geometry.blk_h);
+  wpod<uint32_t>(os, t.geometry.blk_w);
+  wpod<uint8_t>(os, t.csr.has_values() ? 1 : 0);
+  wpod<uint64_t>(os, t.csr.num_nodes);
+  wpod<uint64_t>(os, t.csr.num_edges());
+  wpod<uint64_t>(os, t.num_windows());
+  wpod<uint64_t>(os, t.block_counter);
+  warr(os, t.csr.node_pointer);
+  warr(os, t.csr.edge_list);
+  if (t.csr.has_values()) warr(os, t.csr.values);
+  warr(os, t.edge_to_row);
+  warr(os, t.edge_to_column);
+  warr(os, t.block_partition);
+  warr(os, t.window_offsets);
+  warr(os, t.window_unique_cols);
+  if (!os) throw IoError("write failed for '" + path + "'");
+}
+
+SGTK_EXPORT TransformedGraph load_sgt(const std::string& path) {
+  std::ifstream is(path, std::ios::binary);
+  if (!is) throw IoError("cannot open '" + path + "'");
+  char magic[4];
+  is.read(magic, 4);
+  if (!is || std::memcmp(magic, "SGT1", 4) != 0) throw IoError("SGT1: bad magic in '" + path + "'");
+  TransformedGraph t;
+  t.geometry.blk_h = rpod<uint32_t>(is);
+  t.geometry.blk_w = rpod<uint32_t>(is);
+  const uint8_t flags = rpod<uint8_t>(is);
+  const uint64_t n = rpod<uint64_t>(is), E = rpod<uint64_t>(is), W = rpod<uint64_t>(is);
+  t.block_counter = rpod<uint64_t>(is);
+  if (t.geometry.blk_h == 0 || t.geometry.blk_w == 0) throw IoError("SGT1: zero tile geometry");
+  t.csr.num_nodes = n;
+  rarr(is, t.csr.node_pointer, n + 1);
+  rarr(is, t.csr.edge_list, E);
+  if (flags & 1) rarr(is, t.csr.values, E);
+  rarr(is, t.edge_to_row, E);
+  rarr(is, t.edge_to_column, E);
+  rarr(is, t.block_partition, W);
+  rarr(is, t.window_offsets, W + 1);
+  if (t.window_offsets.front() != 0) throw IoError("SGT1: corrupt window offsets");
+  rarr(is, t.window_unique_cols, t.window_offsets.back());
+  if (is.get() != std::ifstream::traits_type::eof())
+    throw IoError("SGT1: trailing bytes in '" + path + "'");
+  validate_csr(t.csr);
+  if (t.csr.node_pointer.back() != E) throw IoError("SGT1: inconsistent edge count");
+  return t;
+}
+
+}  // namespace sgtk

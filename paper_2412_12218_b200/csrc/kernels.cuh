@@ -21,6 +21,8 @@ void sddmm_launch(const sgtk_graph* g, const float* x, uint64_t ldx, const float
                   uint64_t d, const uint32_t* cut16_dev, const float* ev, bool unit_values,
                   int prec, const float* inv_norm, float scale, float* out, cudaStream_t s);
 void edge_softmax_launch(const sgtk_graph* g, const float* logits, float* out, cudaStream_t s);
+void csr_softmax_launch(const uint64_t* np, uint64_t n, const float* logits, float* out,
+                        cudaStream_t s);
 void l2norm_launch(const float* h, uint64_t rows, uint64_t cols, uint64_t ldh, float* z,
                    uint64_t ldz, float* inv, uint64_t* zeros, cudaStream_t s);
 void gcn_normalize_launch(const uint64_t* np, const uint32_t* el, uint64_t n, float* vals,
@@ -37,4 +39,17 @@ void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, const 
 // Host-side split plan (make_split_plan, tile_exec.cpp:150-161).
 std::vector<uint32_t> split_plan_host(const sgtk_graph* g, double ratio);
 
+}  // namespace sgtkcu
+
+// Device CSR produced by normalize_graph (normalize.cu).
+struct sgtk_csr {
+  uint64_t n = 0, nnz = 0;
+  bool has_values = false;
+  sgtkcu::DevBuf np, el, vals;
+};
+
+namespace sgtkcu {
+sgtk_csr* normalize_graph(const uint64_t* np, const uint32_t* el, const float* vals, uint64_t n,
+                          uint64_t E, int symmetrize, int loops, int dedupe, int kind,
+                          cudaStream_t s);
 }  // namespace sgtkcu

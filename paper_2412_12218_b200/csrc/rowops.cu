@@ -116,11 +116,16 @@ inline unsigned blocks_for(uint64_t threads, unsigned bs = 256) {
 
 }  // namespace
 
+void csr_softmax_launch(const uint64_t* np, uint64_t n, const float* logits, float* out,
+                        cudaStream_t s) {
+  if (!n) return;
+  edge_softmax_kernel<<<blocks_for(n * 32), 256, 0, s>>>(np, n, logits, out);
+  CU_LAUNCH("edge_softmax_kernel");
+}
+
 void edge_softmax_launch(const sgtk_graph* g, const float* logits, float* out, cudaStream_t s) {
   if (!g->n_rows || !g->nnz) return;
-  edge_softmax_kernel<<<blocks_for(g->n_rows * 32), 256, 0, s>>>(g->np->as<uint64_t>(), g->n_rows,
-                                                                logits, out);
-  CU_LAUNCH("edge_softmax_kernel");
+  csr_softmax_launch(g->np->as<uint64_t>(), g->n_rows, logits, out, s);
 }
 
 void l2norm_launch(const float* h, uint64_t rows, uint64_t cols, uint64_t ldh, float* z,

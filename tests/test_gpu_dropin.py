@@ -1,0 +1,29 @@
+"""The C++ drop-in (include/sgtk/*.hpp over libsgtk_b200.so) through a test
+program written against the reference's public API (tests/cpp/test_dropin.cpp)."""
+
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CPP = os.path.join(ROOT, "tests", "cpp")
+
+
+def build():
+    subprocess.run(["make", "-C", CPP], check=True, capture_output=True)
+    return os.path.join(CPP, "test_dropin")
+
+
+def test_dropin_compiles_against_reference_api():
+    # CPU-only: the headers + library link (no kernel runs)
+    assert os.path.exists(build())
+
+
+@pytest.mark.gpu
+def test_dropin_cpp_suite():
+    exe = build()
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout[-3000:])
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "checks passed" in r.stdout
