@@ -280,7 +280,10 @@ def run_b200(args, wl):
     x_host = sg.dense_random(N, wl["d_in"], 8)
     w_in = torch.from_numpy(sg.dense_random(wl["d_in"], wl["hidden"], 1, -0.1, 0.1)).to(dev)
     w_out = torch.from_numpy(sg.dense_random(wl["hidden"], wl["d_out"], 2, -0.1, 0.1)).to(dev)
-    x = torch.from_numpy(x_host).to(dev)
+    # features resident with a 16-byte-multiple row pitch (TMA-eligible rows)
+    ldx = (wl["d_in"] + 3) // 4 * 4
+    x = torch.zeros((N, ldx), dtype=torch.float32, device=dev)[:, :wl["d_in"]]
+    x.copy_(torch.from_numpy(x_host))
     L = wl["layers"]
     d = wl["hidden"]
     betas = np.ones(L, np.float32)
@@ -383,9 +386,11 @@ def run_b200(args, wl):
     # ---------------- dominant-kernel roofline (CUDA events on our stream) ----
     roof = None
     kern = {}
+    extra = {}
     if world == 1:
         kern, roof = kernel_breakdown(args, wl, dg, g, h0 if wl["kind"] == "agnn" else xs, D, prec,
-                                      mode, flush, stream, layers if wl["kind"] == "gcn" else None)
+                                      mode, flush, stream, layers if wl["kind"] == "gcn" else None,
+                                      extra, (x, w_in) if wl["kind"] == "agnn" else None)
 
     # ---------------- e2e through the host-buffer C ABI ----------------------
     e2e = None
@@ -428,6 +433,11 @@ def run_b200(args, wl):
             "gpu_launches": launches_per_step * args.steps,
             "model_forward_ms": round(model_ms, 4), "kernels_ms": kern,
         }
+        if "roofline_gemm" in extra:
+            rg = extra["roofline_gemm"]
+            rg["peak"] = pk["hbm_gbs"]
+            rg["frac"] = round(rg["achieved"] / pk["hbm_gbs"], 4)
+            line["roofline_gemm"] = rg
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -438,7 +448,8 @@ def dg_has_splits(dg, tile_w):
     return dg.info.work_units8 > dg.info.num_windows if tile_w == 8 else False
 
 
-def kernel_breakdown(args, wl, dg, g, h, D, prec, mode, flush, stream, gcn_layers):
+def kernel_breakdown(args, wl, dg, g, h, D, prec, mode, flush, stream, gcn_layers, extra,
+                     proj=None):
     """Per-kernel CUDA-event times for one layer and the dominant kernel's roofline."""
     import torch
 
@@ -491,6 +502,17 @@ def kernel_breakdown(args, wl, dg, g, h, D, prec, mode, flush, stream, gcn_layer
         res["spmm"] = ev_time(lambda: dg.spmm(h, edge_values=logits, precision=prec, out=out))
         res["agnn_layer_fused(l2norm+fused)"] = ev_time(fused_one)
         res["agnn_fused_kernel"] = res["agnn_layer_fused(l2norm+fused)"] - res["l2norm"]
+        if proj is not None:
+            px, pw = proj
+            res["in_proj_gemm"] = ev_time(lambda: D.gemm(px, pw, relu=True, precision=prec))
+            K, M = px.shape[1], pw.shape[1]
+            Bg = 4 * N * K + 4 * K * M + 4 * N * M
+            extra["roofline_gemm"] = {
+                "bound": "hbm", "kernel": "gemm_tc05 (in-proj %dx%d)" % (K, M),
+                "achieved": round(Bg / (res["in_proj_gemm"] * 1e-3) / 1e9, 1), "unit": "GB/s",
+                "algorithmic_bytes": int(Bg), "formula": "s*N*K + 4*K*M + 4*N*M (SURVEY §8d B_gemm)",
+                "tflops": round(2 * N * K * M / (res["in_proj_gemm"] * 1e-3) / 1e12, 2),
+                "kernel_ms": round(res["in_proj_gemm"], 4)}
         s_ = 4
         B_fused = 8 * (N + 1) + 4 * E + 4 * N + 2 * s_ * N * d
         B_spmm = 8 * (N + 1) + 4 * E + 4 * E + s_ * N * d + 4 * N * d

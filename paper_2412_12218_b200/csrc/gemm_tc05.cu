@@ -340,14 +340,18 @@ bool gemm_tc05_launch(const float* a, uint64_t lda, const float* w, uint64_t m, 
   while (tmem_cols < n_pad) tmem_cols <<= 1;
   const uint32_t num_kc = uint32_t(k_pad / kBK);
   dim3 grid(unsigned((m + kBM - 1) / kBM));
+  // the opt-in smem ceiling is set once per kernel (host overhead, not per call)
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
+    cudaFuncSetAttribute(gemm_tc05_kernel<SGTK_FP32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    cudaFuncSetAttribute(gemm_tc05_kernel<SGTK_TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+  });
   if (prec == SGTK_FP32) {
-    CU(cudaFuncSetAttribute(gemm_tc05_kernel<SGTK_FP32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(smem)));
     gemm_tc05_kernel<SGTK_FP32><<<grid, kThreads, smem, s>>>(ma, mw, m, uint32_t(n), n_pad, num_kc,
                                                              relu, out, ldo, stages, tmem_cols);
   } else {
-    CU(cudaFuncSetAttribute(gemm_tc05_kernel<SGTK_TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(smem)));
     gemm_tc05_kernel<SGTK_TF32><<<grid, kThreads, smem, s>>>(ma, mw, m, uint32_t(n), n_pad, num_kc,
                                                              relu, out, ldo, stages, tmem_cols);
   }
