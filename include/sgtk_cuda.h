@@ -177,6 +177,11 @@ int sgtk_sddmm(const sgtk_graph* g, const float* x_dev, uint64_t ldx,
 int sgtk_edge_softmax(const sgtk_graph* g, const float* logits_dev,
                       float* out_dev, void* stream);
 
+/* In-place ReLU of a row-major device matrix (GCN activation, gnn.cpp:45-47;
+ * used by the multi-GPU A (h W) layer order after the aggregation). */
+int sgtk_relu_inplace(float* x_dev, uint64_t rows, uint64_t cols, uint64_t ld,
+                      void* stream);
+
 /* edge_softmax on a bare device CSR (no transform needed): node_pointer_dev
  * u64[n+1]; gnn.cpp:54-72 takes a CsrGraph, not a TransformedGraph. */
 int sgtk_csr_softmax(const uint64_t* node_pointer_dev, uint64_t num_nodes,

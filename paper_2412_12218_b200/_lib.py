@@ -98,6 +98,13 @@ _SIGS = {
                           vp],
     "sgtk_gcn_normalize_values": [vp, vp, u64, vp, vp],
     "sgtk_tf32_round": [vp, vp, u64, vp],
+    "sgtk_relu_inplace": [vp, u64, u64, u64, vp],
+    "sgtk_csr_softmax": [vp, u64, vp, vp, vp],
+    "sgtk_normalize_graph": [vp, vp, vp, u64, u64, C.c_int, C.c_int, C.c_int, C.c_int, vp,
+                             C.POINTER(vp)],
+    "sgtk_csr_info": [vp, vp],
+    "sgtk_csr_download": [vp, vp, vp, vp],
+    "sgtk_csr_device_ptrs": [vp, vp],
     "sgtk_gcn_forward_host": [vp, vp, u32, vp, vp, vp, C.c_double, C.c_int, vp, vp],
     "sgtk_agnn_forward_host": [vp, vp, u64, u32, vp, C.c_double, C.c_int, C.c_int, vp, vp, vp],
     "sgtk_spmm_host": [vp, vp, u64, C.c_double, C.c_int, vp, vp, vp],
@@ -127,6 +134,8 @@ def lib() -> C.CDLL:
         L.sgtk_graph_destroy.restype = None
         L.sgtk_synth_destroy.argtypes = [vp]
         L.sgtk_synth_destroy.restype = None
+        L.sgtk_csr_destroy.argtypes = [vp]
+        L.sgtk_csr_destroy.restype = None
         L.sgtk_gcn_workspace.argtypes = [vp, u32, vp]
         L.sgtk_gcn_workspace.restype = u64
         L.sgtk_agnn_workspace.argtypes = [vp, u64]
@@ -146,5 +155,6 @@ def check(rc: int) -> None:
 def exported_symbols() -> list[str]:
     """Names declared in include/sgtk_cuda.h (for the CPU load/export test)."""
     return sorted(set(_SIGS) | {"sgtk_last_error", "sgtk_version", "sgtk_graph_destroy",
+                                "sgtk_csr_destroy",
                                 "sgtk_gcn_workspace", "sgtk_agnn_workspace", "sgtk_synth_destroy",
                                 "sgtk_dense_random"})

@@ -236,6 +236,10 @@ int sgtk_edge_softmax(const sgtk_graph* g, const float* logits, float* out, void
   });
 }
 
+int sgtk_relu_inplace(float* x, uint64_t rows, uint64_t cols, uint64_t ld, void* stream) {
+  return guard([&] { relu_nonfinite_launch(x, rows, cols, ld, 1, nullptr, as_stream(stream)); });
+}
+
 int sgtk_csr_softmax(const uint64_t* np, uint64_t n, const float* logits, float* out,
                      void* stream) {
   return guard([&] { csr_softmax_launch(np, n, logits, out, as_stream(stream)); });

@@ -396,14 +396,16 @@ Windows build_windows(const sgtk_graph& g, uint32_t bh, cudaStream_t s) {
   return win;
 }
 
-// Work units: split windows with more than max_tiles tiles so no warp-task is
-// far larger than the average; split windows reduce their partials in order.
-UnitPlan build_units(const std::vector<uint32_t>& ucount, uint32_t tile_w, uint64_t total_tiles,
+// Work units: split windows with more than max_tiles tiles (4096 unique
+// columns) so no warp-task is far larger than the average; split windows
+// reduce their partials in unit order.  The split depends on the window alone
+// (never on graph-wide totals), so a window's summation order -- hence its
+// output bits -- is the same whether it is transformed in the full graph or
+// in one GPU's row slice: results are bit-identical for any GPU count.
+UnitPlan build_units(const std::vector<uint32_t>& ucount, uint32_t tile_w, uint64_t,
                      cudaStream_t s) {
   UnitPlan p;
-  const uint64_t target_units = 148ull * 48;  // ~3 warp-tasks per resident warp slot
-  uint64_t mt = (total_tiles + target_units - 1) / std::max<uint64_t>(target_units, 1);
-  mt = std::min<uint64_t>(std::max<uint64_t>(mt, 64), 1u << 16);
+  const uint64_t mt = 4096 / tile_w;
   p.max_tiles = uint32_t(mt);
   std::vector<WorkUnit> units;
   std::vector<ReduceItem> red;

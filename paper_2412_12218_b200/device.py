@@ -290,6 +290,14 @@ def gemm(a: torch.Tensor, w: torch.Tensor, relu=False, precision="fp32") -> torc
     return out
 
 
+def relu_(x: torch.Tensor) -> torch.Tensor:
+    """In-place ReLU on the GPU (the GCN layer activation, gnn.cpp:45-47)."""
+    _f32_2d(x, "x")
+    check(lib().sgtk_relu_inplace(_ptr(x), u64(x.shape[0]), u64(x.shape[1]), u64(x.stride(0)),
+                                  _stream()))
+    return x
+
+
 def gcn_normalize_values(node_pointer: torch.Tensor, edge_list: torch.Tensor) -> torch.Tensor:
     n = node_pointer.numel() - 1
     vals = torch.empty(edge_list.numel(), dtype=torch.float32, device=edge_list.device)
