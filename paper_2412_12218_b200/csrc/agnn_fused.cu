@@ -218,17 +218,15 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
       }
     sa.l += quad_sum(pa);
     sb.l += quad_sum(pb);
-    // the row maxima settle after a few tiles: skip the rescale when no row
-    // of the window changed its max (warp-uniform vote)
-    if (!__all_sync(0xFFFFFFFFu, sca == 1.0f && scb == 1.0f)) {
+    // O = O * scale + P V.  The tile's P V is a fresh tensor-core partial
+    // folded into the IEEE fp32 running sum by one FFMA per element (the
+    // online-softmax rescale rides along for free): tensor-core accumulation
+    // does not round to nearest, so O never sits on a long MMA chain.
+    // k-step kb covers tile columns kb*8 + {2t, 2t+1} for A's k = {t, t+4}:
+    // exactly the columns this lane's S accumulator holds.
+    float po[NB][4];
 #pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        o[j][0] *= sca; o[j][1] *= sca;
-        o[j][2] *= scb; o[j][3] *= scb;
-      }
-    }
-    // O += P V.  k-step kb covers tile columns kb*8 + {2t, 2t+1} for A's
-    // k = {t, t+4}: exactly the columns this lane's S accumulator holds.
+    for (int j = 0; j < NB; ++j) po[j][0] = po[j][1] = po[j][2] = po[j][3] = 0.0f;
 #pragma unroll
     for (int kb = 0; kb < 2; ++kb) {
       uint32_t p0[4], p1[4];
@@ -242,12 +240,19 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
         split_d<PREC>(cur.v[kb][0][j], x0, x1, x2);
         split_d<PREC>(cur.v[kb][1][j], y0, y1, y2);
         if constexpr (PREC == SGTK_FP32) {
-          mma_tf32(o[j], p0[0], p0[1], p0[2], p0[3], x2, y2);
-          mma_tf32(o[j], p1[0], p1[1], p1[2], p1[3], x0, y0);
-          mma_tf32(o[j], p0[0], p0[1], p0[2], p0[3], x1, y1);
+          mma_tf32(po[j], p0[0], p0[1], p0[2], p0[3], x2, y2);
+          mma_tf32(po[j], p1[0], p1[1], p1[2], p1[3], x0, y0);
+          mma_tf32(po[j], p0[0], p0[1], p0[2], p0[3], x1, y1);
         }
-        mma_tf32(o[j], p0[0], p0[1], p0[2], p0[3], x0, y0);
+        mma_tf32(po[j], p0[0], p0[1], p0[2], p0[3], x0, y0);
       }
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      o[j][0] = fmaf(o[j][0], sca, po[j][0]);
+      o[j][1] = fmaf(o[j][1], sca, po[j][1]);
+      o[j][2] = fmaf(o[j][2], scb, po[j][2]);
+      o[j][3] = fmaf(o[j][3], scb, po[j][3]);
     }
   };
 

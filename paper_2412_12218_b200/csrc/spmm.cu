@@ -75,15 +75,33 @@ spmm_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t n_uni
     eb = lower_bound_u32(G.e2c, cb, eb, u.t1 * 8u);
   }
 
-  float acc[NB][4];
+  // acc: round-to-nearest fp32 running sums; part: the tensor-core partial of
+  // the current group of kFold tiles.  Tensor-core fp32 accumulation does not
+  // round to nearest, so a chain of ~10^3 MMAs on one accumulator (hub
+  // windows) drifts; folding every kFold tiles keeps each chain short and the
+  // long sum in IEEE FADDs (error ~ the sequential reference's).
+  constexpr uint32_t kFold = 4;
+  float acc[NB][4], part[NB][4];
 #pragma unroll
-  for (int j = 0; j < NB; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0f;
+  for (int j = 0; j < NB; ++j) {
+    acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0f;
+    part[j][0] = part[j][1] = part[j][2] = part[j][3] = 0.0f;
+  }
 
   const int64_t bv = int64_t(d) - int64_t(fbase + g * NB);
   const int bvalid = bv < 0 ? 0 : (bv > NB ? NB : int(bv));
 
   // ---------------- tensor-core path: tiles [t0, tc_end) -----------------
   for (uint32_t tile = u.t0; tile < tc_end; ++tile) {
+    if ((tile - u.t0) % kFold == 0 && tile != u.t0) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc[j][q] += part[j][q];
+          part[j][q] = 0.0f;
+        }
+    }
     const uint4 bm = __ldg(G.bm8 + tbase + tile);
     const uint32_t bya = byte_of(bm, g), byb = byte_of(bm, g + 8);
     const uint32_t ct = tile * 8u + t, ct4 = ct + 4u;
@@ -117,13 +135,17 @@ spmm_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t n_uni
       split_d<PREC>(xb0[j], p0, p1, p2);
       split_d<PREC>(xb1[j], q0, q1, q2);
       if constexpr (PREC == SGTK_FP32) {
-        mma_tf32(acc[j], s0[0], s0[1], s0[2], s0[3], p2, q2);
-        mma_tf32(acc[j], s1[0], s1[1], s1[2], s1[3], p0, q0);
-        mma_tf32(acc[j], s0[0], s0[1], s0[2], s0[3], p1, q1);
+        mma_tf32(part[j], s0[0], s0[1], s0[2], s0[3], p2, q2);
+        mma_tf32(part[j], s1[0], s1[1], s1[2], s1[3], p0, q0);
+        mma_tf32(part[j], s0[0], s0[1], s0[2], s0[3], p1, q1);
       }
-      mma_tf32(acc[j], s0[0], s0[1], s0[2], s0[3], p0, q0);
+      mma_tf32(part[j], s0[0], s0[1], s0[2], s0[3], p0, q0);
     }
   }
+#pragma unroll
+  for (int j = 0; j < NB; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[j][q] += part[j][q];
 
   // ---------------- CUDA-core path: remaining edges of the unit ----------
   const uint64_t sf = fbase + 2u * t * NB;  // this lane's output feature segment

@@ -250,7 +250,7 @@ class DeviceGraph:
 
     def agnn_forward(self, x, betas, cut=None, precision="fp32", mode=0, return_zeros=False):
         _f32_2d(x, "x")
-        if x.shape[0] != self.info.num_nodes:
+        if x.shape[0] != self.num_cols:  # == num_nodes unless a row slice (full replica in)
             raise ShapeError("agnn_forward: x.rows != num_nodes")
         d = x.shape[1]
         b = np.ascontiguousarray(betas, np.float32)

@@ -199,13 +199,24 @@ def test_spmm_widths(d):
 
 @pytest.mark.parametrize("name,g", big_graphs())
 def test_spmm_large_windows_split_units(name, g):
+    # Hub rows (degree up to ~8k) make fp32 summation order visible: the
+    # sequential oracle itself is ~3e-6 off the exact (float64) result.  Bar:
+    # the reference's own tolerance vs the oracle (1e-4, test_tile_exec.cpp:97-112)
+    # and no more than twice the oracle's own rounding error vs exact.
     c = Csr.of(g.num_nodes, g.node_pointer, g.edge_list)
     t = sg.sgt_transform(g)
+    deg = np.diff(g.node_pointer.astype(np.int64))
+    rows = np.repeat(np.arange(g.num_nodes), deg)
     for d in (16, 64):
         x = sg.dense_random(g.num_nodes, d, 5)
         want = O.spmm(c, x)
-        assert mre(sg.spmm_hybrid(t, x), want) <= TOL_FP32
-        assert mre(sg.spmm_hybrid(t, x, sg.make_split_plan(t, 0.25)), want) <= TOL_FP32
+        exact = np.zeros((g.num_nodes, d))
+        np.add.at(exact, rows, x[g.edge_list].astype(np.float64))
+        ref_err = mre(want, exact)
+        for plan in (None, sg.make_split_plan(t, 0.25)):
+            got = sg.spmm_hybrid(t, x, plan)
+            assert mre(got, want) <= 1e-4
+            assert mre(got, exact) <= 2 * ref_err + 1e-6
 
 
 def test_spmm_deterministic():
