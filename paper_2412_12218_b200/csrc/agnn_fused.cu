@@ -27,6 +27,8 @@
 // Tiles at or past the plan's cut go edge-by-edge on CUDA cores into the same
 // running state; windows split over several warps merge (m, l, O) in order.
 
+#include <cstdlib>
+
 #include "graph.cuh"
 
 namespace sgtkcu {
@@ -383,6 +385,263 @@ __global__ void agnn_merge_kernel(const ReduceItem* __restrict__ items, uint64_t
   }
 }
 
+// ===========================================================================
+// v3 (d == 32, every tile on the tensor cores): shared-memory staging.
+// Each warp keeps a kStages ring of tile slots filled with cp.async (L2 ->
+// smem, no registers): the tile's 16 gathered h rows (2 KB, XOR-swizzled per
+// 16-byte chunk), their 16 inv_norm values and the 32-byte bitmap.  Only h is
+// gathered: S = (z_row . h_col) * inv_col, so K and V share one copy (half the
+// L2 traffic of gathering z and h).  Feature map for the S MMA: k-column k
+// of k-step i is feature 8(k mod 4) + 4(k div 4) + i, i.e. lane t reads the
+// 16-byte chunks 2t and 2t+1 of a row; with the XOR swizzle (chunk ^ row%8)
+// every fragment read (K: row g; V: rows 2t, 2t+1) is bank-conflict free.
+// ===========================================================================
+constexpr int kStages = 4;
+
+struct V3Slot {
+  float rows[16][32];
+  float inv[16];
+  uint32_t bm[8];
+};
+
+__device__ __forceinline__ void cp_async16_cg(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4_ca(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int PREC>
+__global__ void __launch_bounds__(kWarps * 32, 4)
+agnn_fused_v3_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t n_units,
+                     const float* __restrict__ h, uint64_t ldh, const float* __restrict__ inv,
+                     float beta, float* __restrict__ out, uint64_t ldo,
+                     float* __restrict__ partial, uint64_t pstride) {
+  constexpr int NB = 4;
+  extern __shared__ __align__(16) uint8_t smem_v3[];
+  const uint32_t wib = threadIdx.x >> 5;
+  const uint32_t wid = blockIdx.x * kWarps + wib;
+  if (wid >= n_units) return;
+  V3Slot* ring = reinterpret_cast<V3Slot*>(smem_v3) + wib * kStages;
+  const WorkUnit u = units[wid];
+  const uint32_t lane = lane_id(), g = lane >> 2, t = lane & 3u;
+  const uint64_t w = u.window;
+  const uint64_t ra = w * 16 + g, rb = ra + 8;
+  const bool va = ra < G.n_rows, vb = rb < G.n_rows;
+  const uint64_t xa = G.row_offset + (va ? ra : 0), xb = G.row_offset + (vb ? rb : 0);
+  const uint64_t ubase = G.wo[w];
+  const uint32_t ucnt = uint32_t(G.wo[w + 1] - ubase);
+  const uint64_t tbase = G.toff16[w];
+  const float scale2 = beta * kLog2e;
+
+  // ---- Q: z rows g, g+8; k-col t <-> chunk 2t, k-col t+4 <-> chunk 2t+1 ----
+  uint32_t qh[4][NB], ql[4][NB];
+  {
+    const float ia = va ? __ldg(inv + xa) : 0.0f, ib = vb ? __ldg(inv + xb) : 0.0f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool rowa = (q & 1) == 0;
+      const float4 v = __ldg(reinterpret_cast<const float4*>(h + (rowa ? xa : xb) * ldh) +
+                             (2 * t + (q >> 1)));
+      const float sc = rowa ? ia : ib;
+      split_s<PREC>(v.x * sc, qh[q][0], ql[q][0]);
+      split_s<PREC>(v.y * sc, qh[q][1], ql[q][1]);
+      split_s<PREC>(v.z * sc, qh[q][2], ql[q][2]);
+      split_s<PREC>(v.w * sc, qh[q][3], ql[q][3]);
+    }
+  }
+
+  // ---- producer: fill one slot with tile `tile` (all 32 lanes) -------------
+  const uint32_t* ids = G.wuc + ubase;
+  const uint32_t last = ucnt ? ucnt - 1u : 0u;
+  auto produce = [&](uint32_t tile, V3Slot& sl) {
+    const uint32_t c = lane & 7u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t r = (lane >> 3) + 4u * k;
+      const uint32_t id = __ldg(ids + min(tile * 16u + r, last));
+      cp_async16_cg(&sl.rows[r][(c ^ (r & 7u)) * 4u], h + uint64_t(id) * ldh + c * 4u);
+    }
+    if (lane < 16) {
+      const uint32_t id = __ldg(ids + min(tile * 16u + lane, last));
+      cp_async4_ca(&sl.inv[lane], inv + id);
+    } else if (lane < 18) {
+      cp_async16_cg(&sl.bm[(lane - 16) * 4], G.bm16 + 2 * (tbase + tile) + (lane - 16));
+    }
+  };
+
+  float o[NB][4];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.0f;
+  RowState sa{-INFINITY, 0.0f}, sb{-INFINITY, 0.0f};
+
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (u.t0 + s < u.t1) produce(u.t0 + s, ring[s]);
+    cp_commit();
+  }
+  for (uint32_t tile = u.t0; tile < u.t1; ++tile) {
+    const uint32_t it = tile - u.t0;
+    if (tile + kStages - 1 < u.t1) produce(tile + kStages - 1, ring[(it + kStages - 1) % kStages]);
+    cp_commit();
+    cp_wait<kStages - 1>();
+    __syncwarp();
+    const V3Slot& sl = ring[it % kStages];
+
+    const uint4 blo = *reinterpret_cast<const uint4*>(&sl.bm[0]);
+    const uint4 bhi = *reinterpret_cast<const uint4*>(&sl.bm[4]);
+    const uint32_t wa = bits16(blo, bhi, g), wb = bits16(blo, bhi, g + 8);
+
+    // S = Q H^T (columns scaled by inv afterwards)
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      const uint32_t r = nb * 8u + g;
+      const float4 k0 = *reinterpret_cast<const float4*>(&sl.rows[r][((2u * t) ^ g) * 4u]);
+      const float4 k1 = *reinterpret_cast<const float4*>(&sl.rows[r][((2u * t + 1u) ^ g) * 4u]);
+      const float kk0[4] = {k0.x, k0.y, k0.z, k0.w}, kk1[4] = {k1.x, k1.y, k1.z, k1.w};
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        uint32_t b0, c0, b1, c1;
+        split_s<PREC>(kk0[i], b0, c0);
+        split_s<PREC>(kk1[i], b1, c1);
+        if constexpr (PREC == SGTK_FP32) {
+          mma_tf32(s[nb], ql[0][i], ql[1][i], ql[2][i], ql[3][i], b0, b1);
+          mma_tf32(s[nb], qh[0][i], qh[1][i], qh[2][i], qh[3][i], c0, c1);
+        }
+        mma_tf32(s[nb], qh[0][i], qh[1][i], qh[2][i], qh[3][i], b0, b1);
+      }
+    }
+    // logits: * inv[col] (z_col = h_col * inv_col), tf32 rounding, * beta, mask
+    float tma = -INFINITY, tmb = -INFINITY;
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      const float2 ic = *reinterpret_cast<const float2*>(&sl.inv[nb * 8 + 2 * t]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t c = nb * 8u + 2u * t + (q & 1u);
+        const bool edge = ((q < 2 ? wa : wb) >> c) & 1u;
+        float v = s[nb][q] * ((q & 1) ? ic.y : ic.x);
+        if constexpr (PREC == SGTK_TF32) v = __uint_as_float(tf32_op(v));
+        v = edge ? v * scale2 : -INFINITY;
+        s[nb][q] = v;
+        if (q < 2) tma = fmaxf(tma, v); else tmb = fmaxf(tmb, v);
+      }
+    }
+    float sca, scb;
+    const float ma = online_update(sa, quad_max(tma), sca);
+    const float mb = online_update(sb, quad_max(tmb), scb);
+    float pa = 0.f, pb = 0.f;
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float p = ex2(s[nb][q] - (q < 2 ? ma : mb));
+        s[nb][q] = p;
+        if (q < 2) pa += p; else pb += p;
+      }
+    sa.l += quad_sum(pa);
+    sb.l += quad_sum(pb);
+    // O = O * scale + P V  (V rows kb*8 + 2t, +1; feature chunk g)
+    float po[NB][4];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) po[j][0] = po[j][1] = po[j][2] = po[j][3] = 0.0f;
+#pragma unroll
+    for (int kb = 0; kb < 2; ++kb) {
+      uint32_t p0[4], p1[4];
+      split_s<PREC>(s[kb][0], p0[0], p1[0]);
+      split_s<PREC>(s[kb][2], p0[1], p1[1]);
+      split_s<PREC>(s[kb][1], p0[2], p1[2]);
+      split_s<PREC>(s[kb][3], p0[3], p1[3]);
+      const uint32_t r0 = kb * 8u + 2u * t, r1 = r0 + 1u;
+      const float4 v0 = *reinterpret_cast<const float4*>(&sl.rows[r0][(g ^ (r0 & 7u)) * 4u]);
+      const float4 v1 = *reinterpret_cast<const float4*>(&sl.rows[r1][(g ^ (r1 & 7u)) * 4u]);
+      const float vv0[4] = {v0.x, v0.y, v0.z, v0.w}, vv1[4] = {v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        uint32_t x0, x1, x2, y0, y1, y2;
+        split_d<PREC>(vv0[j], x0, x1, x2);
+        split_d<PREC>(vv1[j], y0, y1, y2);
+        if constexpr (PREC == SGTK_FP32) {
+          mma_tf32(po[j], p0[0], p0[1], p0[2], p0[3], x2, y2);
+          mma_tf32(po[j], p1[0], p1[1], p1[2], p1[3], x0, y0);
+          mma_tf32(po[j], p0[0], p0[1], p0[2], p0[3], x1, y1);
+        }
+        mma_tf32(po[j], p0[0], p0[1], p0[2], p0[3], x0, y0);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      o[j][0] = fmaf(o[j][0], sca, po[j][0]);
+      o[j][1] = fmaf(o[j][1], sca, po[j][1]);
+      o[j][2] = fmaf(o[j][2], scb, po[j][2]);
+      o[j][3] = fmaf(o[j][3], scb, po[j][3]);
+    }
+    __syncwarp();  // every lane is done with this slot before it is refilled
+  }
+  cp_wait<0>();
+
+  // ---- epilogue (same layout as v2, NB = 4) --------------------------------
+  const uint64_t sf = 2u * t * NB;
+  float va_[2 * NB], vb_[2 * NB];
+  if (u.slot == kNoSlot) {
+    const float la = sa.l > 0.0f ? 1.0f / sa.l : 0.0f, lb = sb.l > 0.0f ? 1.0f / sb.l : 0.0f;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      va_[j] = o[j][0] * la; va_[NB + j] = o[j][1] * la;
+      vb_[j] = o[j][2] * lb; vb_[NB + j] = o[j][3] * lb;
+    }
+    if (va) store_seg<2 * NB, true>(out + ra * ldo + sf, va_, 2 * NB);
+    if (vb) store_seg<2 * NB, true>(out + rb * ldo + sf, vb_, 2 * NB);
+  } else {
+    float* P = partial + uint64_t(u.slot) * pstride;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      va_[j] = o[j][0]; va_[NB + j] = o[j][1];
+      vb_[j] = o[j][2]; vb_[NB + j] = o[j][3];
+    }
+    store_seg<2 * NB, true>(P + g * 8 * NB + sf, va_, 2 * NB);
+    store_seg<2 * NB, true>(P + (g + 8) * 8 * NB + sf, vb_, 2 * NB);
+    if (t == 0) {
+      P[16 * 8 * NB + g] = sa.m;
+      P[16 * 8 * NB + g + 8] = sb.m;
+      P[16 * 8 * NB + 16 + g] = sa.l;
+      P[16 * 8 * NB + 16 + g + 8] = sb.l;
+    }
+  }
+}
+
+template <int PREC>
+void launch_v3(const sgtk_graph* g, const float* h, uint64_t ldh, const float* inv, float beta,
+               float* out, uint64_t ldo, cudaStream_t s) {
+  const auto& P = g->plan16;
+  const uint64_t pstride = 16 * 8 * 4 + 32;
+  float* partial = nullptr;
+  if (P.n_slots)
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&partial), uint64_t(P.n_slots) * pstride * 4, s));
+  const size_t smem = size_t(kWarps) * kStages * sizeof(V3Slot);
+  agnn_fused_v3_kernel<PREC><<<(P.n_units + kWarps - 1) / kWarps, kWarps * 32, smem, s>>>(
+      g->view(), P.units->as<WorkUnit>(), P.n_units, h, ldh, inv, beta, out, ldo, partial, pstride);
+  CU_LAUNCH("agnn_fused_v3_kernel");
+  if (P.n_reduce) {
+    agnn_merge_kernel<4><<<P.n_reduce, 256, 0, s>>>(P.reduce->as<ReduceItem>(), g->n_rows, partial,
+                                                    pstride, 32, out, ldo);
+    CU_LAUNCH("agnn_merge_kernel");
+  }
+  if (partial) CU(cudaFreeAsync(partial, s));
+}
+
 template <int NB, int PREC, bool FULL>
 void launch(const sgtk_graph* g, const uint32_t* thr, const float* h, uint64_t ldh, const float* z,
             uint64_t ldz, uint64_t d, float beta, float* out, uint64_t ldo, cudaStream_t s) {
@@ -419,14 +678,21 @@ void dispatch(int prec, bool full, const sgtk_graph* g, const uint32_t* thr, con
 }  // namespace
 
 void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, const float* z,
-                       uint64_t ldz, uint64_t d, float beta, int prec, const uint32_t* cut_dev,
-                       float* out, uint64_t ldo, cudaStream_t s) {
+                       uint64_t ldz, const float* inv, uint64_t d, float beta, int prec,
+                       const uint32_t* cut_dev, float* out, uint64_t ldo, cudaStream_t s) {
   if (prec != SGTK_FP32 && prec != SGTK_TF32)
     raise(SGTK_ERR_RANGE, "agnn_forward: precision must be FP32 or TF32");
   if (d > 64) raise(SGTK_ERR_SHAPE, "agnn_forward: fused mode supports d <= 64 (use mode 0)");
   if (g->n_rows == 0 || d == 0) return;
   DevBuf cut_keep;
   const uint32_t* thr = internal_cut(g, cut_dev, 16, s, cut_keep);
+  // d == 32 with every tile on the tensor cores: the smem-staged v3 kernel
+  if (d == 32 && !thr && !getenv("SGTK_AGNN_V2") && ldh % 4 == 0 && ldo % 4 == 0 &&
+      reinterpret_cast<uintptr_t>(h) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0) {
+    if (prec == SGTK_FP32) launch_v3<SGTK_FP32>(g, h, ldh, inv, beta, out, ldo, s);
+    else launch_v3<SGTK_TF32>(g, h, ldh, inv, beta, out, ldo, s);
+    return;
+  }
   const int nb = d <= 16 ? 2 : d <= 32 ? 4 : 8;
   const bool full = uint64_t(8 * nb) == d && ldh % 4 == 0 && ldz % 4 == 0 && ldo % 4 == 0 &&
                     reinterpret_cast<uintptr_t>(h) % 16 == 0 &&

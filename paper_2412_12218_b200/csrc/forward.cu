@@ -148,7 +148,7 @@ void agnn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
     if (mode == 1) {
       // z = h * inv_norm materialised (as the reference does, gnn.cpp:109)
       l2norm_launch(h, l == 0 ? g->n_cols : N, d, ldh, zbuf, ldb, inv, zeros, s);
-      agnn_fused_launch(g, h, ldh, zbuf, ldb, d, betas[l], prec, cut, dst, ldd, s);
+      agnn_fused_launch(g, h, ldh, zbuf, ldb, inv, d, betas[l], prec, cut, dst, ldd, s);
     } else {
       l2norm_launch(h, l == 0 ? g->n_cols : N, d, ldh, nullptr, 0, inv, zeros, s);
       // The reference's SDDMM runs on reblock(t, 16) with make_split_plan(t16, ratio)

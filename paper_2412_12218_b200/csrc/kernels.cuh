@@ -33,8 +33,8 @@ void gemm_launch(const float* a, uint64_t lda, const float* w, uint64_t m, uint6
 void relu_nonfinite_launch(float* x, uint64_t rows, uint64_t cols, uint64_t ld, int relu,
                            uint32_t* nonfinite, cudaStream_t s);
 void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, const float* z,
-                       uint64_t ldz, uint64_t d, float beta, int prec, const uint32_t* cut_dev,
-                       float* out, uint64_t ldo, cudaStream_t s);
+                       uint64_t ldz, const float* inv, uint64_t d, float beta, int prec,
+                       const uint32_t* cut_dev, float* out, uint64_t ldo, cudaStream_t s);
 
 // Host-side split plan (make_split_plan, tile_exec.cpp:150-161).
 std::vector<uint32_t> split_plan_host(const sgtk_graph* g, double ratio);
