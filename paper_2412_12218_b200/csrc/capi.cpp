@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -31,9 +32,30 @@ namespace {
 
 thread_local std::string g_err;
 
+// Stream-ordered scratch (cudaMallocAsync) comes from the device's default
+// pool; its default release threshold (0) hands memory back to the driver at
+// every synchronisation, turning each call's scratch into a fresh cudaMalloc.
+// Keep it cached instead (once per device).
+void prepare_device() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int d : done)
+    if (d == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~uint64_t(0);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.push_back(dev);
+}
+
 template <class F>
 int guard(F&& f) {
   try {
+    prepare_device();
     f();
     return SGTK_OK;
   } catch (const Status& e) {
