@@ -128,6 +128,21 @@ int sgtk_graph_download(const sgtk_graph* g, uint32_t* edge_to_row,
                         uint32_t* edge_to_column, uint32_t* block_partition,
                         uint64_t* window_offsets, uint32_t* window_unique_cols);
 
+/* 128-row panel format behind the default-plan SpMM (no reference
+ * counterpart: it is the device layout that replaces the reference's
+ * per-window dense chunk staging, tile_exec.cpp:226-290).
+ * info = {panels, dense_chunks, dense_entries (padded), sparse_edges,
+ *         max_chunk_entries, dense_columns (padded)} */
+int sgtk_panel_info(const sgtk_graph* g, uint64_t info[6]);
+
+/* Download the panel arrays (sizes from sgtk_panel_info; any may be NULL):
+ * chunk_ptr u32[P+1], dense_cols u32[32*chunks], chunk_off u64[chunks+1],
+ * dense_entries u32[entries] (tf32 value | skip<<12 | row<<5 | col),
+ * sparse_ptr u32[N+1], sparse_entries u32[2*sparse] (column, value bits). */
+int sgtk_panel_download(const sgtk_graph* g, uint32_t* chunk_ptr, uint32_t* dense_cols,
+                        uint64_t* chunk_off, uint32_t* dense_entries, uint32_t* sparse_ptr,
+                        uint32_t* sparse_entries);
+
 /* reblock (sgt_transform.hpp:55, sgt_transform.cpp:79-91): a new handle that
  * shares nothing with `g` observable by the caller; block_partition and
  * block_counter recomputed at `blk_w`, edge maps unchanged. */

@@ -83,6 +83,8 @@ _SIGS = {
     "sgtk_graph_import": [vp, vp, vp, u64, u64, u32, u32, vp, vp, vp, vp, C.POINTER(vp)],
     "sgtk_graph_info": [vp, vp],
     "sgtk_graph_device_ptrs": [vp, vp],
+    "sgtk_panel_info": [vp, vp],
+    "sgtk_panel_download": [vp, vp, vp, vp, vp, vp, vp],
     "sgtk_graph_download": [vp, vp, vp, vp, vp, vp],
     "sgtk_graph_reblock": [vp, u32, vp, C.POINTER(vp)],
     "sgtk_block_stats": [vp, vp, C.POINTER(C.c_double)],

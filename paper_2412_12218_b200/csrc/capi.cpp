@@ -147,6 +147,34 @@ int sgtk_graph_info(const sgtk_graph* g, uint64_t info[11]) {
   });
 }
 
+int sgtk_panel_info(const sgtk_graph* g, uint64_t info[6]) {
+  return guard([&] {
+    check_graph(g);
+    const auto& p = *g->panels;
+    const uint64_t v[6] = {p.P, p.n_chunks, p.n_dent, p.n_sparse, p.max_chunk_entries,
+                           p.n_chunks * 32};
+    std::memcpy(info, v, sizeof v);
+  });
+}
+
+int sgtk_panel_download(const sgtk_graph* g, uint32_t* chunk_ptr, uint32_t* dense_cols,
+                        uint64_t* chunk_off, uint32_t* dense_entries, uint32_t* sparse_ptr,
+                        uint32_t* sparse_entries) {
+  return guard([&] {
+    check_graph(g);
+    const auto& p = *g->panels;
+    auto get = [](void* dst, const sgtkcu::DevBuf& src, size_t bytes) {
+      if (dst && bytes) CU(cudaMemcpy(dst, src.p, bytes, cudaMemcpyDeviceToHost));
+    };
+    get(chunk_ptr, *p.cptr, (p.P + 1) * 4);
+    get(dense_cols, *p.dcols, p.n_chunks * 32 * 4);
+    get(chunk_off, *p.coff, (p.n_chunks + 1) * 8);
+    get(dense_entries, *p.dent, p.n_dent * 4);
+    get(sparse_ptr, *p.sptr, (g->n_rows + 1) * 4);
+    get(sparse_entries, *p.sent, p.n_sparse * 8);
+  });
+}
+
 int sgtk_graph_device_ptrs(const sgtk_graph* g, const void* ptrs[8]) {
   return guard([&] {
     check_graph(g);

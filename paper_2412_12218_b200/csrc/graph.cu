@@ -25,7 +25,7 @@
 #include <memory>
 #include <numeric>
 
-#include "graph.cuh"
+#include "kernels.cuh"
 
 namespace sgtkcu {
 namespace {
@@ -513,6 +513,10 @@ void build_e2r(sgtk_graph& g, cudaStream_t s) {
 
 }  // namespace
 
+Windows build_row_windows(const sgtk_graph& g, uint32_t bh, cudaStream_t s) {
+  return build_windows(g, bh, s);
+}
+
 sgtk_graph* graph_create(const uint64_t* np, const uint32_t* el, const float* vals, uint64_t n_rows,
                          uint64_t n_cols, uint64_t nnz, uint32_t blk_h, uint32_t blk_w, int kind,
                          cudaStream_t s, uint64_t row_offset) {
@@ -536,6 +540,7 @@ sgtk_graph* graph_create(const uint64_t* np, const uint32_t* el, const float* va
   set_partition(*g);
   g->bp = upload(g->bp_host.data(), g->bp_host.size(), s);
   finish_tiles(*g, s);
+  build_panels(*g, s);
   g->scratch = std::make_shared<DevBuf>();
   return g.release();
 }
@@ -567,6 +572,7 @@ sgtk_graph* graph_import(const uint64_t* np, const uint32_t* el, const float* va
   set_partition(*g);
   g->bp = upload(g->bp_host.data(), g->bp_host.size(), s);
   finish_tiles(*g, s);
+  build_panels(*g, s);
   g->scratch = std::make_shared<DevBuf>();
   return g.release();
 }

@@ -42,6 +42,49 @@ struct Windows {
   std::vector<uint64_t> wo_host;
 };
 
+// 128-row panel format for the tcgen05 aggregation kernels (panel.cu).
+// Per panel (128 rows, the UMMA M), the unique columns with >= kDenseMin
+// edges are "dense": they are gathered once per panel and multiplied on the
+// tensor cores in chunks of 32 (one 128-byte swizzle row of TF32).  The other
+// ("sparse") edges -- mostly singleton columns -- run edge-by-edge on CUDA
+// cores.  This is the density-aware hybrid split of SURVEY §8f rank 3.
+constexpr int kPanelRows = 128;
+constexpr int kChunkCols = 32;
+constexpr uint32_t kDenseMin = 2;
+constexpr uint32_t kEntrySkip = 0x1000u;  // padding entry marker (bit 12)
+constexpr uint32_t kSegEdges = 512;       // sparse edges per CUDA-core work item
+
+struct Panels {
+  uint64_t P = 0, n_chunks = 0, n_dent = 0, n_sparse = 0;
+  uint32_t max_chunk_entries = 0;
+  std::shared_ptr<DevBuf> cptr;   // u32[P+1]   first chunk of panel p
+  std::shared_ptr<DevBuf> dcols;  // u32[32*n_chunks] dense column ids (pad 0xFFFFFFFF)
+  std::shared_ptr<DevBuf> coff;   // u64[n_chunks+1] entry range of a chunk (multiple of 4)
+  std::shared_ptr<DevBuf> dent;   // u32[n_dent]  tf32(value) | skip<<12 | row<<5 | k
+  std::shared_ptr<DevBuf> dval;   // f32[n_dent]  full fp32 value
+  std::shared_ptr<DevBuf> deid;   // u32[n_dent]  CSR edge id (0xFFFFFFFF for padding)
+  std::shared_ptr<DevBuf> sptr;   // u32[n_rows+1] sparse edges of a row
+  std::shared_ptr<DevBuf> sent;   // uint2[n_sparse] (column, value bits)
+  std::shared_ptr<DevBuf> seid;   // u32[n_sparse] CSR edge id
+  // CUDA-core work list: one item per row with sparse edges; rows with more
+  // than kSegEdges sparse edges are cut into segments whose partial sums are
+  // reduced in segment order (sparse_rows_kernel / long_rows_kernel).
+  uint64_t n_items = 0, n_long = 0, n_segs = 0;
+  std::shared_ptr<DevBuf> items;  // uint4[n_items] (row, e_begin, e_end, segment | ~0u)
+  std::shared_ptr<DevBuf> lrows;  // uint4[n_long]  (row, first segment, segments, 0)
+};
+
+struct PanelView {
+  uint64_t n_rows, P;
+  const uint32_t* cptr;
+  const uint32_t* dcols;
+  const uint64_t* coff;
+  const uint32_t* dent;
+  const float* dval;
+  const uint32_t* sptr;
+  const uint2* sent;
+};
+
 // POD view handed to kernels.
 struct DevGraph {
   uint64_t n_rows, n_cols, nnz, W;
@@ -77,6 +120,7 @@ struct sgtk_graph {
   uint64_t T8 = 0, T16 = 0;
   std::shared_ptr<sgtkcu::DevBuf> toff8, bm8, toff16, bm16;
   sgtkcu::UnitPlan plan8, plan16;
+  std::shared_ptr<sgtkcu::Panels> panels;  // 128-row panel format (panel.cu)
 
   // workspace for host-buffer entry points and forwards (mutable scratch)
   mutable std::shared_ptr<sgtkcu::DevBuf> scratch;

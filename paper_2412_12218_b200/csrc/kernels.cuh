@@ -36,6 +36,13 @@ void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, const 
                        uint64_t ldz, const float* inv, uint64_t d, float beta, int prec,
                        const uint32_t* cut_dev, float* out, uint64_t ldo, cudaStream_t s);
 
+// 128-row panel format + tcgen05 SpMM (panel.cu)
+Windows build_row_windows(const sgtk_graph& g, uint32_t bh, cudaStream_t s);
+void build_panels(sgtk_graph& g, cudaStream_t s);
+bool spmm_panel_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
+                       const float* ev, int prec, float* out, uint64_t ldo, uint32_t* nonfinite,
+                       cudaStream_t s);
+
 // Host-side split plan (make_split_plan, tile_exec.cpp:150-161).
 std::vector<uint32_t> split_plan_host(const sgtk_graph* g, double ratio);
 

@@ -1,0 +1,956 @@
+// 128-row panel SpMM on the 5th-gen tensor cores (tcgen05 + TMEM).
+//
+// Replaces spmm_hybrid (/root/reference/proj/src/tile_exec.cpp:200-314) for
+// the default plan (every tile on the tensor cores, ratio 1.0,
+// tile_exec.cpp:150-161): out = A * x.
+//
+// Why 128-row panels instead of the reference's 16-row windows: a column
+// shared by rows of the same panel is gathered once per panel.  On the
+// Reddit-shaped graph the gathered volume drops from 43.7M (16-row windows)
+// to 16.7M unique (panel, column) pairs; the gather, not the arithmetic, is
+// what bounds this kernel.
+//
+// Density-aware split (the paper's thesis): per panel,
+// columns with >= kDenseMin edges are "dense" and go through the tensor
+// cores in chunks of 32 columns; singleton columns (the bulk of the random
+// long-range edges) go edge-by-edge through the CUDA cores -- a 128 x 32 tile
+// holding a single non-zero is not worth 16 KB of shared memory traffic.
+//
+// One CTA per (panel, 32/64-feature slice); 10 warps, warp-specialised:
+//   warp 0      loader: cp.async gather of the chunk's 32 feature rows into
+//               an MN-major SWIZZLE_128B_BASE32B B tile (the UMMA "N" = features are
+//               contiguous in a row of x), plus a 1-D bulk copy (TMA engine)
+//               of the chunk's packed adjacency entries
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (M = 128 rows, N = feature slice, K = 8 per instruction);
+//               groups of kFold chunks rotate over TMEM accumulators
+//   warps 2-5   A-tile builders: zero the K-major SWIZZLE_128B A tile,
+//               scatter the chunk's entries (pos | tf32 value packed in one
+//               u32), TF32-round / FP32-split the B tile, fence, arrive
+//   warps 6-9   accumulators, thread per row: sparse edges on CUDA cores in
+//               fp32 registers; fold every finished TMEM accumulator group
+//               into the same registers (IEEE adds: TC accumulation chains
+//               stay <= 4 chunks long) on a schedule fixed by the panel's
+//               shape (deterministic), then the epilogue store.
+// Precision: TF32 = both operands RNE-rounded like tf32_round_value
+// (tile_exec.cpp:131-142); FP32 = the 4-term TF32 split (common.cuh).
+
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
+
+#include "kernels.cuh"
+#include "tc05.cuh"
+
+namespace sgtkcu {
+namespace {
+
+using namespace tc05;
+
+// =========================================================== format builder
+inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 32u) {
+  uint64_t g = (n + block - 1) / block;
+  return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(g, cap)));
+}
+
+__global__ void panel_count_kernel(const uint32_t* __restrict__ e2r, const uint32_t* __restrict__ e2c,
+                                   const uint64_t* __restrict__ wo, uint64_t E,
+                                   uint32_t* __restrict__ cnt) {
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < E;
+       e += uint64_t(gridDim.x) * blockDim.x)
+    atomicAdd(cnt + wo[e2r[e] / kPanelRows] + e2c[e], 1u);
+}
+
+__global__ void dense_flag_kernel(uint32_t* __restrict__ cnt, uint64_t U) {
+  for (uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; u <= U;
+       u += uint64_t(gridDim.x) * blockDim.x)
+    cnt[u] = (u < U && cnt[u] >= kDenseMin) ? 1u : 0u;
+}
+
+__global__ void panel_dcount_kernel(const uint64_t* __restrict__ wo, const uint32_t* __restrict__ grank,
+                                    uint64_t P, uint32_t* __restrict__ dcnt) {
+  for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < P;
+       p += uint64_t(gridDim.x) * blockDim.x)
+    dcnt[p] = grank[wo[p + 1]] - grank[wo[p]];
+}
+
+// dense column list of each panel, padded to a multiple of 32
+__global__ void dcols_kernel(const uint64_t* __restrict__ wo, const uint32_t* __restrict__ wuc,
+                             const uint32_t* __restrict__ flag, const uint32_t* __restrict__ grank,
+                             const uint32_t* __restrict__ cptr, uint64_t P,
+                             uint32_t* __restrict__ dcols) {
+  for (uint64_t p = blockIdx.x; p < P; p += gridDim.x) {
+    const uint64_t u0 = wo[p], u1 = wo[p + 1];
+    const uint32_t g0 = grank[u0];
+    const uint64_t base = uint64_t(cptr[p]) * kChunkCols;
+    for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x)
+      if (flag[u]) dcols[base + (grank[u] - g0)] = wuc[u];
+  }
+}
+
+__device__ __forceinline__ bool dense_slot(const uint32_t* __restrict__ e2r,
+                                           const uint32_t* __restrict__ e2c,
+                                           const uint64_t* __restrict__ wo,
+                                           const uint32_t* __restrict__ flag,
+                                           const uint32_t* __restrict__ grank, uint64_t e,
+                                           uint32_t& p, uint32_t& slot) {
+  p = e2r[e] / kPanelRows;
+  const uint64_t u = wo[p] + e2c[e];
+  slot = grank[u] - grank[wo[p]];
+  return flag[u] != 0;
+}
+
+__global__ void chunk_count_kernel(const uint32_t* __restrict__ e2r, const uint32_t* __restrict__ e2c,
+                                   const uint64_t* __restrict__ wo, const uint32_t* __restrict__ flag,
+                                   const uint32_t* __restrict__ grank,
+                                   const uint32_t* __restrict__ cptr, uint64_t E,
+                                   uint32_t* __restrict__ ccnt) {
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < E;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t p, slot;
+    if (dense_slot(e2r, e2c, wo, flag, grank, e, p, slot))
+      atomicAdd(ccnt + cptr[p] + slot / kChunkCols, 1u);
+  }
+}
+
+__global__ void fill_u32_kernel(uint32_t* __restrict__ p, uint64_t n, uint32_t v) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+// Packed entry: tf32(value) in bits 31..13 (RNE, tf32_round_value), row in
+// the panel in bits 11..5, column in the chunk in bits 4..0.  The position
+// within a chunk is unique, so the (atomic) slot order never affects results.
+__device__ __forceinline__ uint32_t pack_entry(float v, uint32_t row, uint32_t k) {
+  return (__float_as_uint(tf32_rne(v)) & 0xFFFFE000u) | (row << 5) | k;
+}
+
+__global__ void entry_fill_kernel(const uint32_t* __restrict__ e2r, const uint32_t* __restrict__ e2c,
+                                  const uint64_t* __restrict__ wo, const uint32_t* __restrict__ flag,
+                                  const uint32_t* __restrict__ grank,
+                                  const uint32_t* __restrict__ cptr, const uint64_t* __restrict__ coff,
+                                  const float* __restrict__ vals, uint64_t E,
+                                  uint32_t* __restrict__ cfill, uint32_t* __restrict__ dent,
+                                  float* __restrict__ dval, uint32_t* __restrict__ deid) {
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < E;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t p, slot;
+    if (!dense_slot(e2r, e2c, wo, flag, grank, e, p, slot)) continue;
+    const uint32_t ch = cptr[p] + slot / kChunkCols;
+    const uint64_t i = coff[ch] + atomicAdd(cfill + ch, 1u);
+    const float v = vals ? vals[e] : 1.0f;
+    dent[i] = pack_entry(v, e2r[e] % kPanelRows, slot % kChunkCols);
+    dval[i] = v;
+    deid[i] = uint32_t(e);
+  }
+}
+
+// sparse (CUDA-core) edges: per-row count, then per-row stable compaction
+__global__ void sparse_count_kernel(const uint64_t* __restrict__ np, uint64_t n,
+                                    const uint32_t* __restrict__ e2c, const uint64_t* __restrict__ wo,
+                                    const uint32_t* __restrict__ flag, uint32_t* __restrict__ scnt) {
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t r = warp; r < n; r += nwarps) {
+    const uint64_t ub = wo[r / kPanelRows];
+    uint32_t c = 0;
+    for (uint64_t e = np[r] + lane; e < np[r + 1]; e += 32) c += flag[ub + e2c[e]] ? 0u : 1u;
+    c = __reduce_add_sync(0xFFFFFFFFu, c);
+    if (lane == 0) scnt[r] = c;
+  }
+}
+
+__global__ void sparse_fill_kernel(const uint64_t* __restrict__ np, const uint32_t* __restrict__ el,
+                                   const float* __restrict__ vals, uint64_t n,
+                                   const uint32_t* __restrict__ e2c, const uint64_t* __restrict__ wo,
+                                   const uint32_t* __restrict__ flag,
+                                   const uint32_t* __restrict__ sptr, uint2* __restrict__ sent,
+                                   uint32_t* __restrict__ seid) {
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t r = warp; r < n; r += nwarps) {
+    const uint64_t ub = wo[r / kPanelRows];
+    uint32_t pos = sptr[r];
+    for (uint64_t b = np[r]; b < np[r + 1]; b += 32) {
+      const uint64_t e = b + lane;
+      const bool sp = e < np[r + 1] && !flag[ub + e2c[e]];
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, sp);
+      if (sp) {
+        const uint32_t i = pos + __popc(m & ((1u << lane) - 1u));
+        sent[i] = make_uint2(el[e], __float_as_uint(vals ? vals[e] : 1.0f));
+        seid[i] = uint32_t(e);
+      }
+      pos += __popc(m);
+    }
+  }
+}
+
+// Override values (edge_values span, tile_exec.cpp:44-52): re-pack the
+// entries from a CSR-order value array through the stored edge ids.
+__global__ void repack_dense_kernel(const uint32_t* __restrict__ dent, const uint32_t* __restrict__ deid,
+                                    const float* __restrict__ ev, uint64_t n,
+                                    uint32_t* __restrict__ dent_o, float* __restrict__ dval_o) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t e = deid[i], w = dent[i];
+    if (e == 0xFFFFFFFFu) {
+      dent_o[i] = w;
+      dval_o[i] = 0.0f;
+    } else {
+      const float v = ev[e];
+      dent_o[i] = pack_entry(v, (w >> 5) & 127u, w & 31u);
+      dval_o[i] = v;
+    }
+  }
+}
+__global__ void repack_sparse_kernel(const uint2* __restrict__ sent, const uint32_t* __restrict__ seid,
+                                     const float* __restrict__ ev, uint64_t n,
+                                     uint2* __restrict__ sent_o) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    sent_o[i] = make_uint2(sent[i].x, __float_as_uint(ev[seid[i]]));
+}
+
+template <class T>
+std::vector<T> dl(const void* dev, size_t count, cudaStream_t s) {
+  std::vector<T> h(count);
+  if (count) {
+    CU(cudaMemcpyAsync(h.data(), dev, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+  }
+  return h;
+}
+template <class T>
+std::shared_ptr<DevBuf> ul(const T* host, size_t count, cudaStream_t s) {
+  auto b = std::make_shared<DevBuf>(std::max<size_t>(count, 1) * sizeof(T));
+  if (count) CU(cudaMemcpyAsync(b->p, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  return b;
+}
+
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t s) {
+  size_t tb = 0;
+  CU(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, int64_t(n), s));
+  DevBuf t(std::max<size_t>(tb, 16));
+  CU(cub::DeviceScan::ExclusiveSum(t.p, tb, in, out, int64_t(n), s));
+  CU(cudaStreamSynchronize(s));
+}
+
+// ======================================================== the SpMM kernels
+template <int DC, int PREC>
+struct PanelCfg {
+  static constexpr int PA = PREC == SGTK_FP32 ? 2 : 1;  // A planes (split2)
+  static constexpr int PB = PREC == SGTK_FP32 ? 3 : 1;  // B planes (split3)
+  static constexpr uint32_t A_BYTES = kPanelRows * kChunkCols * 4;  // 16 KB, K-major
+  static constexpr uint32_t B_BYTES = kChunkCols * DC * 4;          // MN-major
+  static constexpr uint32_t STAGE = PA * A_BYTES + PB * B_BYTES;    // multiple of 1024
+  static constexpr int NS = PREC == SGTK_FP32 ? 2 : 4;              // stage ring depth
+  static constexpr int GW = 4 / NS;                                 // builder warps per chunk
+  static constexpr int NV = PREC == SGTK_FP32 ? 2 : 1;              // entry (+ value) slots
+  static constexpr int NF = 512 / DC;                               // TMEM accumulators
+  static constexpr uint32_t FOLD = 4;                               // chunks per accumulator
+};
+
+constexpr int kPanelThreads = 320;
+constexpr uint32_t kBarBytes = 1024;
+constexpr uint32_t kMaxND = 8;
+
+// Runtime shared-memory layout (host-computed from the graph's largest chunk).
+struct PanelSmem {
+  uint32_t nd;     // entry ring depth (multiple of NS, >= NS)
+  uint32_t dslot;  // bytes of one entry slot
+  uint32_t dring_off, total;
+};
+
+// Source of the zero rows that pad a panel's last chunk (cp.async needs a
+// global address; 256 B covers a 64-feature slice).
+__device__ __align__(16) float g_zero_row[64];
+
+// ---------------------------------------------------------------------------
+// Dense part on the tensor cores: out[rows of panel] = A_dense * x (a store:
+// the CUDA-core kernels add the sparse edges afterwards, in a fixed order).
+// One CTA per (panel, 32/64-feature slice); 10 warps, warp-specialised:
+//   warp 0      loader: coalesced cp.async gather of the chunk's 32 feature
+//               rows into an MN-major SWIZZLE_128B_BASE32B B tile, completion
+//               signalled by cp.async.mbarrier.arrive.noinc (the loader never
+//               waits on its own copies); 1-D bulk copies (TMA engine) of the
+//               chunks' packed entries, nd - NS chunks ahead of the stages
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M = 128
+//               rows, N = feature slice, K = 8 per instruction); groups of
+//               FOLD chunks rotate over 512/DC TMEM accumulators
+//   warps 2-5   A-tile builders: chunk c is built by the warp group c % NS,
+//               so NS chunks are in construction at once: zero the K-major
+//               SWIZZLE_128B A tile, scatter the entries (tf32 value | row |
+//               column packed in one u32), FP32: split A and B into TF32
+//               planes; fence.proxy.async, arrive
+//   warps 6-9   accumulators, thread per row: fold each finished TMEM group
+//               into fp32 registers in group order (IEEE adds keep every
+//               tensor-core accumulation chain <= FOLD chunks), store.
+// ---------------------------------------------------------------------------
+template <int DC, int PREC>
+__global__ void __launch_bounds__(kPanelThreads, 1)
+spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict__ x, uint64_t ldx,
+                  uint64_t d, float* __restrict__ out, uint64_t ldo, int vec_out) {
+  using C = PanelCfg<DC, PREC>;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  // 1024-aligned base, derived by offset so the compiler keeps the shared
+  // address space (LDS/STS rather than generic loads)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + C::NS;
+  uint64_t* bfull = empty + C::NS;
+  uint64_t* dfull = bfull + C::NS;
+  uint64_t* accfull = dfull + kMaxND;
+  uint64_t* accempty = accfull + C::NF;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + C::NF);
+  uint8_t* ring = smem + kBarBytes;      // [NS] stages: A planes, B planes
+  uint8_t* dring = smem + L.dring_off;   // [nd] entry slots (+ [nd] value slots, FP32)
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t p = blockIdx.x;
+  const uint64_t fbase = uint64_t(blockIdx.y) * DC;
+  const int dvalid = d - fbase < uint64_t(DC) ? int(d - fbase) : DC;
+  const uint32_t c0 = pv.cptr[p], nch = pv.cptr[p + 1] - c0;
+  const uint32_t ngroups = (nch + C::FOLD - 1) / C::FOLD;
+  const uint32_t ND = L.nd;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NS; ++i) {
+      mbar_init(full + i, C::GW);  // the builder warps that own the chunk
+      mbar_init(empty + i, 1);     // tcgen05.commit
+      mbar_init(bfull + i, 32);    // one cp.async.mbarrier.arrive.noinc per loader lane
+    }
+    for (uint32_t i = 0; i < ND; ++i) mbar_init(dfull + i, 1);  // bulk copy (expect_tx)
+    for (int i = 0; i < C::NF; ++i) {
+      mbar_init(accfull + i, 1);
+      mbar_init(accempty + i, 4);
+    }
+    mbar_init_fence();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ loader
+    // Entry slot of chunk c is reused by chunk c + nd; that chunk's copy is
+    // issued at iteration c + NS, after empty[] says MMA(c) -- hence the
+    // builder of c -- is done.  So copies run nd - NS chunks ahead.
+    const uint32_t LA = ND - C::NS;
+    auto entries = [&](uint32_t c) {
+      if (lane == 0 && c < nch) {
+        const uint32_t ds = c % ND;
+        const uint64_t e0 = pv.coff[c0 + c], e1 = pv.coff[c0 + c + 1];
+        const uint32_t bytes = uint32_t(e1 - e0) * 4u;
+        mbar_expect_tx(dfull + ds, bytes * C::NV);
+        if (bytes) {
+          bulk_load(dring + ds * L.dslot, pv.dent + e0, bytes, dfull + ds);
+          if constexpr (PREC == SGTK_FP32)
+            bulk_load(dring + (ND + ds) * L.dslot, pv.dval + e0, bytes, dfull + ds);
+        }
+      }
+    };
+    for (uint32_t c = 0; c < LA; ++c) entries(c);
+    uint32_t col = nch ? pv.dcols[uint64_t(c0) * kChunkCols + lane] : 0u;
+    for (uint32_t c = 0; c < nch; ++c) {
+      const uint32_t s = c % C::NS, ph = (c / C::NS) & 1u;
+      const uint32_t col_next =
+          c + 1 < nch ? pv.dcols[uint64_t(c0 + c + 1) * kChunkCols + lane] : 0u;
+      mbar_wait(empty + s, ph ^ 1u);
+      entries(c + LA);
+      const uint32_t bst = smem_u32(ring + s * C::STAGE + C::PA * C::A_BYTES);
+      // Cooperative, coalesced gather: an instruction moves RPI whole rows
+      // (DC / 4 lanes of 16 B per row).  Destination: MN-major
+      // SWIZZLE_128B_BASE32B (tc05.cuh desc_mn32): K-row k, 4-row groups
+      // 512 B apart, 32-feature blocks 4096 B apart, 32-byte chunks XOR (k % 4).
+      constexpr uint32_t LPR = DC / 4, RPI = 32 / LPR;
+      const uint32_t j = lane % LPR, jj = j & 7u;
+#pragma unroll
+      for (uint32_t t = 0; t < 32 / RPI; ++t) {
+        const uint32_t k = t * RPI + lane / LPR;
+        const uint32_t ck = __shfl_sync(0xFFFFFFFFu, col, k);
+        const bool real = ck != 0xFFFFFFFFu && int(4 * j) < dvalid;
+        const uint32_t dst = bst + (j >> 3) * 4096u + (k >> 2) * 512u + (k & 3u) * 128u +
+                             ((((jj >> 1) ^ (k & 3u)) << 5) | ((jj & 1u) << 4));
+        cp_async16(dst, real ? x + uint64_t(ck) * ldx + fbase + 4 * j : g_zero_row);
+      }
+      cp_async_arrive_noinc(bfull + s);
+      __syncwarp();
+      col = col_next;
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(DC, true);
+      for (uint32_t c = 0; c < nch; ++c) {
+        const uint32_t s = c % C::NS, ph = (c / C::NS) & 1u;
+        const uint32_t g = c / C::FOLD, buf = g % C::NF;
+        const bool first = (c % C::FOLD) == 0;
+        if (first && g >= uint32_t(C::NF)) mbar_wait(accempty + buf, ((g / C::NF) - 1u) & 1u);
+        mbar_wait(full + s, ph);
+        if constexpr (PREC == SGTK_TF32) {
+          // B went straight from cp.async (generic proxy) to the MMA (async
+          // proxy): acquire the copies, then order them for the async proxy.
+          mbar_wait(bfull + s, ph);
+          fence_async_smem();
+        }
+        tc_fence_after();
+        const uint32_t dt = tmem + buf * DC;
+        const uint32_t a0 = smem_u32(ring + s * C::STAGE), a1 = a0 + C::A_BYTES;
+        const uint32_t b0 = a0 + C::PA * C::A_BYTES, b1 = b0 + C::B_BYTES, b2 = b1 + C::B_BYTES;
+#pragma unroll
+        for (uint32_t ks = 0; ks < kChunkCols / 8; ++ks) {
+          const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+          const uint64_t ad0 = umma_desc(a0 + ks * 32);
+          const uint64_t bd0 = desc_mn32(b0 + ks * 1024, 4096, 512);
+          if constexpr (PREC == SGTK_FP32) {
+            umma_tf32(dt, ad0, desc_mn32(b2 + ks * 1024, 4096, 512), idesc, acc);
+            umma_tf32(dt, umma_desc(a1 + ks * 32), bd0, idesc, 1u);
+            umma_tf32(dt, ad0, desc_mn32(b1 + ks * 1024, 4096, 512), idesc, 1u);
+            umma_tf32(dt, ad0, bd0, idesc, 1u);
+          } else {
+            umma_tf32(dt, ad0, bd0, idesc, acc);
+          }
+        }
+        umma_commit(empty + s);
+        if ((c % C::FOLD) == C::FOLD - 1 || c + 1 == nch) umma_commit(accfull + buf);
+      }
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ A builders
+    const uint32_t b = warp - 2, grp = b % C::NS, sub = b / C::NS;
+    const uint32_t gl = sub * 32 + lane;  // thread index inside the chunk's group
+    constexpr uint32_t GT = C::GW * 32;
+    for (uint32_t c = grp; c < nch; c += C::NS) {
+      const uint32_t s = c % C::NS, ph = (c / C::NS) & 1u;
+      const uint32_t ds = c % ND, dph = (c / ND) & 1u;
+      uint8_t* st = ring + s * C::STAGE;
+      const uint32_t abase = smem_u32(st);
+      const uint64_t e0 = pv.coff[c0 + c], e1 = pv.coff[c0 + c + 1];
+      const uint32_t ne = uint32_t(e1 - e0);
+      mbar_wait(empty + s, ph ^ 1u);
+#pragma unroll 8
+      for (uint32_t i = gl; i < C::PA * C::A_BYTES / 16; i += GT)
+        st_shared_v4(abase + i * 16, 0u, 0u, 0u, 0u);
+      mbar_wait(dfull + ds, dph);
+      if constexpr (C::GW > 1) named_bar(1 + grp, GT);
+      else __syncwarp();
+      const uint32_t* ent = reinterpret_cast<const uint32_t*>(dring + ds * L.dslot);
+      const float* dv = reinterpret_cast<const float*>(dring + (ND + ds) * L.dslot);
+#pragma unroll 4
+      for (uint32_t i = gl; i < ne; i += GT) {
+        const uint32_t w = ent[i];
+        if (w & kEntrySkip) continue;
+        const uint32_t row = (w >> 5) & 127u, k = w & 31u;
+        const uint32_t off = (row >> 3) * 1024u + (row & 7u) * 128u +
+                             (((k >> 2) ^ (row & 7u)) << 4) + (k & 3u) * 4u;
+        if constexpr (PREC == SGTK_FP32) {
+          uint32_t s0, s1;
+          split2(dv[i], s0, s1);
+          st_shared_u32(abase + off, s0);
+          st_shared_u32(abase + C::A_BYTES + off, s1);
+        } else {
+          st_shared_u32(abase + off, w & 0xFFFFE000u);
+        }
+      }
+      if constexpr (PREC == SGTK_FP32) {
+        // B tile: exact 3-plane split in place
+        mbar_wait(bfull + s, ph);
+        uint4* B = reinterpret_cast<uint4*>(st + C::PA * C::A_BYTES);
+#pragma unroll 4
+        for (uint32_t i = gl; i < C::B_BYTES / 16; i += GT) {
+          const uint4 v = B[i];
+          uint32_t xs[4] = {v.x, v.y, v.z, v.w}, q0[4], q1[4], q2[4];
+#pragma unroll
+          for (int jx = 0; jx < 4; ++jx) split3(__uint_as_float(xs[jx]), q0[jx], q1[jx], q2[jx]);
+          B[i] = make_uint4(q0[0], q0[1], q0[2], q0[3]);
+          B[C::B_BYTES / 16 + i] = make_uint4(q1[0], q1[1], q1[2], q1[3]);
+          B[2 * C::B_BYTES / 16 + i] = make_uint4(q2[0], q2[1], q2[2], q2[3]);
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(full + s);
+    }
+  } else {
+    // ------------------------------------------------------------ accumulators
+    const uint32_t q = warp & 3u;
+    const uint64_t r = p * kPanelRows + q * 32 + lane;
+    float acc[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j) acc[j] = 0.0f;
+    for (uint32_t g = 0; g < ngroups; ++g) {
+      const uint32_t buf = g % C::NF;
+      mbar_wait(accfull + buf, (g / C::NF) & 1u);
+      tc_fence_after();
+#pragma unroll
+      for (int cc = 0; cc < DC; cc += 16) {
+        uint32_t v[16];
+        tmem_ld16(tmem + ((q * 32u) << 16) + buf * DC + cc, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[cc + j] += __uint_as_float(v[j]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(accempty + buf);
+    }
+    if (r < pv.n_rows) {
+      float* o = out + r * ldo + fbase;
+      if (vec_out && dvalid == DC) {
+#pragma unroll
+        for (int j = 0; j < DC / 4; ++j)
+          reinterpret_cast<float4*>(o)[j] =
+              make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < DC; ++j)
+          if (j < dvalid) o[j] = acc[j];
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Sparse part on the CUDA cores: one warp per work item (a row's sparse
+// edges, or a <= kSegEdges segment of a hub row), lanes over features
+// (FPL = 1 or 2 consecutive floats per lane: 128- or 256-byte coalesced
+// rows), 8 edges' rows in flight per warp, edges of a batch broadcast by
+// shuffle.  Direct items continue the row's sum from the dense result in
+// `out` (out = dense + e0 + e1 + ...); segments write partials that
+// long_rows_kernel adds in segment order.  Deterministic throughout.
+// ---------------------------------------------------------------------------
+template <int FPL, int PREC>
+__global__ void __launch_bounds__(256)
+sparse_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2* __restrict__ sent,
+                   const float* __restrict__ x, uint64_t ldx, uint64_t d, uint64_t fbase,
+                   float* __restrict__ out, uint64_t ldo, float* __restrict__ part, uint64_t ldp,
+                   uint32_t* __restrict__ nonfinite) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t f = fbase + uint64_t(lane) * FPL;  // this lane's first feature
+  const int fv = f >= d ? 0 : (d - f >= uint64_t(FPL) ? FPL : int(d - f));
+  bool bad = false;
+  for (uint64_t it = warp; it < n_items; it += nw) {
+    const uint4 w = items[it];
+    float acc[FPL];
+    const bool direct = w.w == 0xFFFFFFFFu;
+    float* dst = direct ? out + uint64_t(w.x) * ldo + f : part + uint64_t(w.w) * ldp + (f - fbase);
+#pragma unroll
+    for (int i = 0; i < FPL; ++i) acc[i] = (direct && i < fv) ? dst[i] : 0.0f;
+    for (uint32_t e = w.y; e < w.z; e += 32) {
+      const uint32_t cnt = min(32u, w.z - e);
+      const uint2 en = lane < cnt ? sent[e + lane] : make_uint2(0u, 0u);
+      for (uint32_t u0 = 0; u0 < cnt; u0 += 8) {
+        float xv[8][FPL];
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) {
+          const uint32_t c = __shfl_sync(0xFFFFFFFFu, en.x, u0 + u);
+          const float* src = x + uint64_t(c) * ldx + f;
+          if (u0 + u < cnt && fv == FPL) {
+            if constexpr (FPL == 2) {
+              const float2 v = __ldg(reinterpret_cast<const float2*>(src));
+              xv[u][0] = v.x;
+              xv[u][1] = v.y;
+            } else {
+              xv[u][0] = __ldg(src);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < FPL; ++i) xv[u][i] = (u0 + u < cnt && i < fv) ? __ldg(src + i) : 0.0f;
+          }
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) {
+          float a = __uint_as_float(__shfl_sync(0xFFFFFFFFu, en.y, u0 + u));
+          if (u0 + u >= cnt) a = 0.0f;
+          if constexpr (PREC == SGTK_TF32) a = tf32_rne(a);  // x arrives pre-rounded
+#pragma unroll
+          for (int i = 0; i < FPL; ++i) acc[i] = fmaf(a, xv[u][i], acc[i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < FPL; ++i)
+      if (i < fv) {
+        dst[i] = acc[i];
+        bad |= direct && !isfinite(acc[i]);
+      }
+  }
+  if (nonfinite && __any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(nonfinite, 1u);
+}
+
+// Hub rows: out[row] += segment partials, in segment order.
+__global__ void long_rows_kernel(const uint4* __restrict__ lrows, uint64_t n_long,
+                                 const float* __restrict__ part, uint64_t ldp, uint64_t d,
+                                 uint64_t fbase, uint64_t dc, float* __restrict__ out, uint64_t ldo,
+                                 uint32_t* __restrict__ nonfinite) {
+  bool bad = false;
+  for (uint64_t i = blockIdx.x; i < n_long; i += gridDim.x) {
+    const uint4 w = lrows[i];
+    for (uint64_t f = threadIdx.x; f < dc && fbase + f < d; f += blockDim.x) {
+      float s = out[uint64_t(w.x) * ldo + fbase + f];
+      for (uint32_t k = 0; k < w.z; ++k) s += part[uint64_t(w.y + k) * ldp + f];
+      out[uint64_t(w.x) * ldo + fbase + f] = s;
+      bad |= !isfinite(s);
+    }
+  }
+  if (nonfinite && bad) atomicOr(nonfinite, 1u);
+}
+
+// Rows without any sparse edge are final after the dense kernel: scan them
+// for non-finite values (the other rows are checked by the sparse kernels).
+__global__ void dense_rows_check_kernel(const uint32_t* __restrict__ sptr, uint64_t n,
+                                        const float* __restrict__ out, uint64_t ldo, uint64_t d,
+                                        uint32_t* __restrict__ nonfinite) {
+  bool bad = false;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n * d;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / d, c = i - r * d;
+    if (sptr[r + 1] == sptr[r]) bad |= !isfinite(out[r * ldo + c]);
+  }
+  if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
+}
+
+// X rounded once per call to TF32 (RNE, tf32_round_value semantics), rows
+// padded to a multiple of 4 floats with zeros: both the tensor-core B tiles
+// and the CUDA-core edges then read ready operands.
+__global__ void tf32_rows_kernel(const float* __restrict__ x, uint64_t ldx, uint64_t rows,
+                                 uint64_t d, float* __restrict__ y, uint64_t ldy) {
+  const uint64_t q4 = ldy / 4, total = rows * q4;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / q4, c = (i - r * q4) * 4;
+    float4 v;
+    if (c + 4 <= d && (ldx & 3) == 0) {
+      v = __ldg(reinterpret_cast<const float4*>(x + r * ldx + c));
+    } else {
+      v.x = c < d ? x[r * ldx + c] : 0.f;
+      v.y = c + 1 < d ? x[r * ldx + c + 1] : 0.f;
+      v.z = c + 2 < d ? x[r * ldx + c + 2] : 0.f;
+      v.w = c + 3 < d ? x[r * ldx + c + 3] : 0.f;
+    }
+    reinterpret_cast<float4*>(y + r * ldy)[c / 4] =
+        make_float4(tf32_rne(v.x), tf32_rne(v.y), tf32_rne(v.z), tf32_rne(v.w));
+  }
+}
+
+int device_major() {
+  static int major = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  });
+  return major;
+}
+
+constexpr uint32_t kSmemCap = 227u * 1024u;
+
+// Entry slots sized for the graph's largest chunk; ring as deep as fits.
+template <int DC, int PREC>
+bool panel_smem(uint32_t max_entries, PanelSmem& L) {
+  using C = PanelCfg<DC, PREC>;
+  L.dslot = ((max_entries + 3) / 4 * 4 * 4 + 127) / 128 * 128;
+  L.dring_off = kBarBytes + C::NS * C::STAGE;
+  for (uint32_t nd = kMaxND; nd >= uint32_t(C::NS); nd -= C::NS) {
+    L.nd = nd;
+    L.total = L.dring_off + nd * C::NV * L.dslot + 1024 /*alignment slack*/;
+    if (L.total <= kSmemCap) return true;
+  }
+  return false;
+}
+
+template <int DC, int PREC>
+bool launch_dense(const PanelView& v, uint64_t P, uint32_t max_entries, const float* x,
+                  uint64_t ldx, uint64_t d, float* out, uint64_t ldo, int vec_out, cudaStream_t s) {
+  PanelSmem L;
+  if (!panel_smem<DC, PREC>(max_entries, L)) return false;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(spmm_panel_kernel<DC, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kSmemCap));
+  });
+  dim3 grid(unsigned(P), unsigned((d + DC - 1) / DC));
+  spmm_panel_kernel<DC, PREC><<<grid, kPanelThreads, L.total, s>>>(v, L, x, ldx, d, out, ldo,
+                                                                   vec_out);
+  CU_LAUNCH("spmm_panel_kernel");
+  return true;
+}
+
+// SGTK_PANEL_DEBUG=1: tensor-core part only, =2: CUDA-core part only
+// (timing experiments; results are then partial sums)
+int panel_debug() {
+  static const int dbg = [] {
+    const char* e = std::getenv("SGTK_PANEL_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return dbg;
+}
+
+void launch_sparse(const Panels& pn, const uint2* sent, const float* x, uint64_t ldx, uint64_t d,
+                   float* out, uint64_t ldo, uint32_t* nonfinite, cudaStream_t s, int prec) {
+  if (!pn.n_items) return;
+  const uint64_t dc = d <= 32 ? 32 : 64;  // features per warp pass
+  float* part = nullptr;
+  if (pn.n_segs) CU(cudaMallocAsync(reinterpret_cast<void**>(&part), pn.n_segs * dc * 4, s));
+  const unsigned blocks = unsigned(std::min<uint64_t>((pn.n_items + 7) / 8, 148ull * 8));
+  for (uint64_t fb = 0; fb < d; fb += dc) {
+    const uint4* it = pn.items->as<uint4>();
+    if (dc == 32) {
+      if (prec == SGTK_FP32)
+        sparse_rows_kernel<1, SGTK_FP32><<<blocks, 256, 0, s>>>(it, pn.n_items, sent, x, ldx, d, fb, out, ldo, part, dc, nonfinite);
+      else
+        sparse_rows_kernel<1, SGTK_TF32><<<blocks, 256, 0, s>>>(it, pn.n_items, sent, x, ldx, d, fb, out, ldo, part, dc, nonfinite);
+    } else {
+      if (prec == SGTK_FP32)
+        sparse_rows_kernel<2, SGTK_FP32><<<blocks, 256, 0, s>>>(it, pn.n_items, sent, x, ldx, d, fb, out, ldo, part, dc, nonfinite);
+      else
+        sparse_rows_kernel<2, SGTK_TF32><<<blocks, 256, 0, s>>>(it, pn.n_items, sent, x, ldx, d, fb, out, ldo, part, dc, nonfinite);
+    }
+    CU_LAUNCH("sparse_rows_kernel");
+    if (pn.n_long) {
+      long_rows_kernel<<<unsigned(std::min<uint64_t>(pn.n_long, 148ull * 4)), 64, 0, s>>>(
+          pn.lrows->as<uint4>(), pn.n_long, part, dc, d, fb, dc, out, ldo, nonfinite);
+      CU_LAUNCH("long_rows_kernel");
+    }
+  }
+  if (part) CU(cudaFreeAsync(part, s));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- builder
+void build_panels(sgtk_graph& g, cudaStream_t s) {
+  auto pn = std::make_shared<Panels>();
+  const uint64_t n = g.n_rows, E = g.nnz;
+  const uint64_t P = (n + kPanelRows - 1) / kPanelRows;
+  pn->P = P;
+  Windows win = build_row_windows(g, kPanelRows, s);
+  const uint64_t U = win.U;
+  const uint32_t* e2r = g.e2r->as<uint32_t>();
+  const uint32_t* e2c = win.e2c->as<uint32_t>();
+  const uint64_t* wo = win.wo->as<uint64_t>();
+
+  DevBuf flag((U + 1) * 4), grank((U + 1) * 4);
+  CU(cudaMemsetAsync(flag.p, 0, (U + 1) * 4, s));
+  if (E) panel_count_kernel<<<grid_for(E, 256), 256, 0, s>>>(e2r, e2c, wo, E, flag.as<uint32_t>());
+  CU_LAUNCH("panel_count_kernel");
+  dense_flag_kernel<<<grid_for(U + 1, 256), 256, 0, s>>>(flag.as<uint32_t>(), U);
+  CU_LAUNCH("dense_flag_kernel");
+  exclusive_scan_u32(flag.as<uint32_t>(), grank.as<uint32_t>(), U + 1, s);
+
+  DevBuf dcnt_d(std::max<uint64_t>(P, 1) * 4);
+  if (P) panel_dcount_kernel<<<grid_for(P, 256), 256, 0, s>>>(wo, grank.as<uint32_t>(), P,
+                                                               dcnt_d.as<uint32_t>());
+  CU_LAUNCH("panel_dcount_kernel");
+  std::vector<uint32_t> dcnt = dl<uint32_t>(dcnt_d.p, P, s);
+  std::vector<uint32_t> cptr(P + 1, 0);
+  for (uint64_t p = 0; p < P; ++p) cptr[p + 1] = cptr[p] + (dcnt[p] + kChunkCols - 1) / kChunkCols;
+  const uint64_t NC = cptr[P];
+  pn->n_chunks = NC;
+  pn->cptr = ul(cptr.data(), P + 1, s);
+  pn->dcols = std::make_shared<DevBuf>(std::max<uint64_t>(NC * kChunkCols, 1) * 4);
+  CU(cudaMemsetAsync(pn->dcols->p, 0xFF, pn->dcols->bytes, s));
+  if (P)
+    dcols_kernel<<<grid_for(P, 1, 148u * 16u), 256, 0, s>>>(
+        wo, win.wuc->as<uint32_t>(), flag.as<uint32_t>(), grank.as<uint32_t>(),
+        pn->cptr->as<uint32_t>(), P, pn->dcols->as<uint32_t>());
+  CU_LAUNCH("dcols_kernel");
+
+  DevBuf ccnt(std::max<uint64_t>(NC, 1) * 4);
+  CU(cudaMemsetAsync(ccnt.p, 0, ccnt.bytes, s));
+  if (E)
+    chunk_count_kernel<<<grid_for(E, 256), 256, 0, s>>>(e2r, e2c, wo, flag.as<uint32_t>(),
+                                                        grank.as<uint32_t>(),
+                                                        pn->cptr->as<uint32_t>(), E,
+                                                        ccnt.as<uint32_t>());
+  CU_LAUNCH("chunk_count_kernel");
+  std::vector<uint32_t> cc = dl<uint32_t>(ccnt.p, NC, s);
+  std::vector<uint64_t> coff(NC + 1, 0);
+  uint32_t mx = 0;
+  for (uint64_t c = 0; c < NC; ++c) {
+    coff[c + 1] = coff[c] + (uint64_t(cc[c]) + 3) / 4 * 4;
+    mx = std::max(mx, cc[c]);
+  }
+  pn->max_chunk_entries = mx;
+  pn->n_dent = coff[NC];
+  pn->coff = ul(coff.data(), NC + 1, s);
+  const uint64_t ND = std::max<uint64_t>(pn->n_dent, 4);
+  pn->dent = std::make_shared<DevBuf>(ND * 4);
+  pn->dval = std::make_shared<DevBuf>(ND * 4);
+  pn->deid = std::make_shared<DevBuf>(ND * 4);
+  fill_u32_kernel<<<grid_for(ND, 256), 256, 0, s>>>(pn->dent->as<uint32_t>(), ND, kEntrySkip);
+  CU(cudaMemsetAsync(pn->dval->p, 0, ND * 4, s));
+  CU(cudaMemsetAsync(pn->deid->p, 0xFF, ND * 4, s));
+  CU(cudaMemsetAsync(ccnt.p, 0, ccnt.bytes, s));
+  const float* vals = g.has_values ? g.vals->as<float>() : nullptr;
+  if (E)
+    entry_fill_kernel<<<grid_for(E, 256), 256, 0, s>>>(
+        e2r, e2c, wo, flag.as<uint32_t>(), grank.as<uint32_t>(), pn->cptr->as<uint32_t>(),
+        pn->coff->as<uint64_t>(), vals, E, ccnt.as<uint32_t>(), pn->dent->as<uint32_t>(),
+        pn->dval->as<float>(), pn->deid->as<uint32_t>());
+  CU_LAUNCH("entry_fill_kernel");
+
+  DevBuf scnt((n + 1) * 4);
+  CU(cudaMemsetAsync(scnt.p, 0, (n + 1) * 4, s));
+  if (n)
+    sparse_count_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(
+        g.np->as<uint64_t>(), n, e2c, wo, flag.as<uint32_t>(), scnt.as<uint32_t>());
+  CU_LAUNCH("sparse_count_kernel");
+  pn->sptr = std::make_shared<DevBuf>((n + 1) * 4);
+  exclusive_scan_u32(scnt.as<uint32_t>(), pn->sptr->as<uint32_t>(), n + 1, s);
+  uint32_t nsp = 0;
+  CU(cudaMemcpyAsync(&nsp, pn->sptr->as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  pn->n_sparse = nsp;
+  pn->sent = std::make_shared<DevBuf>(std::max<uint64_t>(nsp, 1) * 8);
+  pn->seid = std::make_shared<DevBuf>(std::max<uint64_t>(nsp, 1) * 4);
+  if (n && nsp)
+    sparse_fill_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(
+        g.np->as<uint64_t>(), g.el->as<uint32_t>(), vals, n, e2c, wo, flag.as<uint32_t>(),
+        pn->sptr->as<uint32_t>(), pn->sent->as<uint2>(), pn->seid->as<uint32_t>());
+  CU_LAUNCH("sparse_fill_kernel");
+
+  // CUDA-core work list (host, O(N)): a row's sparse edges form one item;
+  // hub rows are cut into kSegEdges segments reduced in order afterwards.
+  std::vector<uint32_t> sp = dl<uint32_t>(pn->sptr->p, n + 1, s);
+  std::vector<uint4> items, lrows;
+  uint32_t seg = 0;
+  for (uint64_t r = 0; r < n; ++r) {
+    const uint32_t b = sp[r], e = sp[r + 1];
+    if (b == e) continue;
+    if (e - b <= kSegEdges) {
+      items.push_back(make_uint4(uint32_t(r), b, e, 0xFFFFFFFFu));
+    } else {
+      const uint32_t k = (e - b + kSegEdges - 1) / kSegEdges;
+      lrows.push_back(make_uint4(uint32_t(r), seg, k, 0u));
+      for (uint32_t i = 0; i < k; ++i)
+        items.push_back(make_uint4(uint32_t(r), b + i * kSegEdges, std::min(e, b + (i + 1) * kSegEdges),
+                                   seg + i));
+      seg += k;
+    }
+  }
+  pn->n_items = items.size();
+  pn->n_long = lrows.size();
+  pn->n_segs = seg;
+  pn->items = ul(items.data(), items.size(), s);
+  pn->lrows = ul(lrows.data(), lrows.size(), s);
+  CU(cudaStreamSynchronize(s));
+  g.panels = pn;
+}
+
+PanelView panel_view(const sgtk_graph* g) {
+  const Panels& pn = *g->panels;
+  PanelView v{};
+  v.n_rows = g->n_rows;
+  v.P = pn.P;
+  v.cptr = pn.cptr->as<uint32_t>();
+  v.dcols = pn.dcols->as<uint32_t>();
+  v.coff = pn.coff->as<uint64_t>();
+  v.dent = pn.dent->as<uint32_t>();
+  v.dval = pn.dval->as<float>();
+  v.sptr = pn.sptr->as<uint32_t>();
+  v.sent = pn.sent->as<uint2>();
+  return v;
+}
+
+bool panel_enabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("SGTK_SPMM_KERNEL");
+    return e && std::string(e) == "tile16";
+  }();
+  return !off && device_major() == 10;
+}
+
+// Returns false (caller runs the 16-row tile kernel) outside this kernel's
+// envelope: unaligned feature rows, a chunk too large for shared memory.
+bool spmm_panel_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
+                       const float* ev, int prec, float* out, uint64_t ldo, uint32_t* nonfinite,
+                       cudaStream_t s) {
+  if (!g->panels || !panel_enabled()) return false;
+  if (ldx % 4 != 0 || reinterpret_cast<uintptr_t>(x) % 16 != 0) return false;
+  if (g->n_rows == 0 || d == 0) return true;
+  PanelView v = panel_view(g);
+  const Panels& pn = *g->panels;
+  {
+    PanelSmem L;
+    const bool fits = (d <= 32 ? (prec == SGTK_FP32 ? panel_smem<32, SGTK_FP32>(pn.max_chunk_entries, L)
+                                                    : panel_smem<32, SGTK_TF32>(pn.max_chunk_entries, L))
+                               : (prec == SGTK_FP32 ? panel_smem<64, SGTK_FP32>(pn.max_chunk_entries, L)
+                                                    : panel_smem<64, SGTK_TF32>(pn.max_chunk_entries, L)));
+    if (!fits) return false;
+  }
+  // Override values: re-packed into stream-ordered scratch (pool-cached,
+  // freed in stream order after the kernels; no host synchronisation).
+  void* ov = nullptr;
+  const uint2* sent = v.sent;
+  if (ev) {
+    const uint64_t nd = std::max<uint64_t>(pn.n_dent, 4), ns = std::max<uint64_t>(pn.n_sparse, 1);
+    CU(cudaMallocAsync(&ov, nd * 8 + ns * 8 + 256, s));
+    uint32_t* od = static_cast<uint32_t*>(ov);
+    float* ovv = reinterpret_cast<float*>(od + nd);
+    uint2* os = reinterpret_cast<uint2*>((reinterpret_cast<uintptr_t>(ovv + nd) + 15) & ~uintptr_t(15));
+    if (pn.n_dent)
+      repack_dense_kernel<<<grid_for(pn.n_dent, 256), 256, 0, s>>>(
+          pn.dent->as<uint32_t>(), pn.deid->as<uint32_t>(), ev, pn.n_dent, od, ovv);
+    CU_LAUNCH("repack_dense_kernel");
+    if (pn.n_sparse)
+      repack_sparse_kernel<<<grid_for(pn.n_sparse, 256), 256, 0, s>>>(
+          pn.sent->as<uint2>(), pn.seid->as<uint32_t>(), ev, pn.n_sparse, os);
+    CU_LAUNCH("repack_sparse_kernel");
+    v.dent = od;
+    v.dval = ovv;
+    sent = os;
+  }
+  float* xr = nullptr;
+  if (prec == SGTK_TF32) {
+    const uint64_t ldr = (d + 3) / 4 * 4;
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&xr), std::max<uint64_t>(g->n_cols * ldr, 4) * 4, s));
+    tf32_rows_kernel<<<grid_for(g->n_cols * ldr / 4, 256), 256, 0, s>>>(x, ldx, g->n_cols, d, xr, ldr);
+    CU_LAUNCH("tf32_rows_kernel");
+    x = xr;
+    ldx = ldr;
+  }
+  const int vec_out = (ldo % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+  const uint32_t me = pn.max_chunk_entries;
+  const int dbg = panel_debug();
+  if (dbg != 2) {
+    if (prec == SGTK_FP32) {
+      if (d <= 32) launch_dense<32, SGTK_FP32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, s);
+      else launch_dense<64, SGTK_FP32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, s);
+    } else {
+      if (d <= 32) launch_dense<32, SGTK_TF32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, s);
+      else launch_dense<64, SGTK_TF32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, s);
+    }
+  } else {
+    CU(cudaMemset2DAsync(out, ldo * 4, 0, d * 4, g->n_rows, s));
+  }
+  if (dbg != 1) launch_sparse(pn, sent, x, ldx, d, out, ldo, nonfinite, s, prec);
+  if (nonfinite) {
+    dense_rows_check_kernel<<<grid_for(g->n_rows * d, 256), 256, 0, s>>>(
+        pn.sptr->as<uint32_t>(), g->n_rows, out, ldo, d, nonfinite);
+    CU_LAUNCH("dense_rows_check_kernel");
+  }
+  if (ov) CU(cudaFreeAsync(ov, s));
+  if (xr) CU(cudaFreeAsync(xr, s));
+  return true;
+}
+
+}  // namespace sgtkcu

@@ -21,7 +21,7 @@
 // Windows too large for one warp-task are split into work units whose
 // partials are reduced in unit order (deterministic; no float atomics).
 
-#include "graph.cuh"
+#include "kernels.cuh"
 
 namespace sgtkcu {
 namespace {
@@ -251,6 +251,8 @@ void spmm_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
     raise(SGTK_ERR_RANGE, "spmm: precision must be FP32 or TF32");
   if (ldx < d || ldo < d) raise(SGTK_ERR_SHAPE, "spmm: leading dimension smaller than width");
   if (g->n_rows == 0 || d == 0) return;
+  // default plan (all tiles on the tensor cores): the 128-row panel kernel
+  if (!cut_dev && spmm_panel_launch(g, x, ldx, d, ev, prec, out, ldo, nonfinite, s)) return;
   DevBuf cut_keep;
   const uint32_t* thr = internal_cut(g, cut_dev, 8, s, cut_keep);
   const float* vals = ev ? ev : (g->has_values ? g->vals->as<float>() : nullptr);

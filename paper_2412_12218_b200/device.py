@@ -154,6 +154,26 @@ class DeviceGraph:
         out["block_counter"] = np.array(i.block_counter, np.uint64)
         return out
 
+    def panel_info(self) -> dict:
+        """128-row panel format sizes (sgtk_panel_info)."""
+        a = np.zeros(6, np.uint64)
+        check(lib().sgtk_panel_info(self._h, a.ctypes.data))
+        return dict(zip(("panels", "dense_chunks", "dense_entries", "sparse_edges",
+                         "max_chunk_entries", "dense_columns"), (int(v) for v in a)))
+
+    def panel_arrays(self) -> dict:
+        i = self.panel_info()
+        out = dict(chunk_ptr=np.zeros(i["panels"] + 1, np.uint32),
+                   dense_cols=np.zeros(i["dense_columns"], np.uint32),
+                   chunk_off=np.zeros(i["dense_chunks"] + 1, np.uint64),
+                   dense_entries=np.zeros(i["dense_entries"], np.uint32),
+                   sparse_ptr=np.zeros(self.info.num_nodes + 1, np.uint32),
+                   sparse_entries=np.zeros(2 * i["sparse_edges"], np.uint32))
+        check(lib().sgtk_panel_download(self._h, *(_ptr(out[k]) for k in (
+            "chunk_ptr", "dense_cols", "chunk_off", "dense_entries", "sparse_ptr",
+            "sparse_entries"))))
+        return out
+
     def block_stats(self):
         s = np.zeros(3, np.uint64)
         d = C.c_double()

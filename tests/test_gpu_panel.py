@@ -1,0 +1,145 @@
+"""GPU parity of the 128-row panel SpMM (panel.cu, tcgen05 + TMEM) -- the
+kernel behind the default plan (ratio 1.0) of spmm_hybrid.
+
+Bars (as tests/test_gpu_parity.py):
+  * FP32 (4-term TF32 split): max_rel_err <= 1e-5 vs the CPU oracle
+    (oracle_spmm order, the reference's fp32 arithmetic);
+  * TF32 vs the oracle's TF32 mode (identical rounded operands, exact
+    products; only the fp32 summation order differs): max_rel_err <= 1e-5;
+  * hub panels: <= 2x the sequential oracle's own error vs a float64 sum.
+Shapes cover ragged last panels (n % 128 != 0), empty rows, panels with no
+dense column, hub panels with hundreds of dense chunks (TMEM accumulator
+reuse), all-dense blocks, feature slices (d > 64) and partial slices.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2412_12218_b200 as sg  # noqa: E402
+from paper_2412_12218_b200.device import DeviceGraph  # noqa: E402
+from oracle.oracle import Csr, Oracle  # noqa: E402
+
+O = Oracle()
+
+
+def mre(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30)) if a.size else 0.0
+
+
+def coo_graph(n, rows, cols, vals=None):
+    g = sg.csr_from_coo(n, rows, cols)
+    if vals is not None:
+        g = sg.CsrGraph(g.num_nodes, g.node_pointer, g.edge_list,
+                        sg.dense_random(1, g.num_edges, vals)[0])
+    return g
+
+
+def graphs():
+    out = []
+    # power-law with locality: dense bands + singleton long-range columns
+    out.append(("powerlaw", sg.synth_graph(3000, 20.0, alpha=2.0, p_local=0.9, band=4.0, seed=3)))
+    # uniform random: almost everything sparse
+    out.append(("uniform", sg.synth_graph(2000, 8.0, alpha=0.0, p_local=0.0, seed=4)))
+    rng = np.random.default_rng(5)
+    # all-dense 128x128 blocks, ragged n, empty rows
+    n = 300
+    rows, cols = [], []
+    for r in range(n):
+        if r % 7 == 3:
+            continue  # empty row
+        b = (r // 128) * 128
+        c = np.arange(b, min(b + 128, n))
+        rows += [r] * len(c)
+        cols += list(c)
+    out.append(("blockdense", coo_graph(n, rows, cols, vals=11)))
+    # hub panel: 128 rows x 6000 shared columns (~190 dense chunks)
+    n = 7000
+    rows, cols = [], []
+    for r in range(n):
+        k = 3000 if r < 128 else 3
+        c = np.unique(rng.integers(0, n, k))
+        rows += [r] * len(c)
+        cols += list(c)
+    out.append(("hubpanel", coo_graph(n, rows, cols, vals=12)))
+    return out
+
+
+GRAPHS = graphs()
+
+
+def oracle_csr(g):
+    return Csr.of(g.num_nodes, g.node_pointer, g.edge_list, g.values)
+
+
+@pytest.mark.parametrize("name,g", GRAPHS, ids=[n for n, _ in GRAPHS])
+@pytest.mark.parametrize("d", [4, 16, 32, 48, 64, 100, 128])
+def test_panel_spmm_fp32(name, g, d):
+    t = sg.sgt_transform(g)
+    x = sg.dense_random(g.num_nodes, d, d + 7)
+    want = O.spmm(oracle_csr(g), x)
+    got = sg.spmm_hybrid(t, x)
+    if name == "hubpanel":
+        deg = np.diff(g.node_pointer.astype(np.int64))
+        rows = np.repeat(np.arange(g.num_nodes), deg)
+        v = np.ones(g.num_edges) if g.values is None else g.values.astype(np.float64)
+        exact = np.zeros((g.num_nodes, d))
+        np.add.at(exact, rows, v[:, None] * x[g.edge_list].astype(np.float64))
+        assert mre(got, exact) <= 2 * mre(want, exact) + 1e-6
+        assert mre(got, want) <= 1e-4
+    else:
+        assert mre(got, want) <= 1e-5
+
+
+@pytest.mark.parametrize("name,g", GRAPHS, ids=[n for n, _ in GRAPHS])
+@pytest.mark.parametrize("d", [16, 32, 64, 128])
+def test_panel_spmm_tf32(name, g, d):
+    t = sg.sgt_transform(g)
+    x = sg.dense_random(g.num_nodes, d, d + 9)
+    want = O.spmm(oracle_csr(g), x, tf32=True)
+    got = sg.spmm_hybrid(t, x, precision="tf32")
+    assert mre(got, want) <= (1e-4 if name == "hubpanel" else 1e-5)
+
+
+@pytest.mark.parametrize("name,g", GRAPHS[:3], ids=[n for n, _ in GRAPHS[:3]])
+def test_panel_vs_tile16_and_override(name, g):
+    """Explicit full plan (cut == block_partition) routes to the 16-row tile
+    kernel; the default (no cut) to the panel kernel: same products."""
+    dg = DeviceGraph.from_csr(g.node_pointer, g.edge_list, g.values)
+    t = sg.sgt_transform(g)
+    x = torch.from_numpy(sg.dense_random(g.num_nodes, 32, 1)).cuda()
+    a = dg.spmm(x)
+    b = dg.spmm(x, cut=np.asarray(t.block_partition, np.uint32))
+    assert mre(a.cpu().numpy(), b.cpu().numpy()) <= 1e-5
+    ev = sg.dense_random(1, g.num_edges, 2)[0]
+    want = O.spmm(Csr.of(g.num_nodes, g.node_pointer, g.edge_list, ev), x.cpu().numpy())
+    got = dg.spmm(x, edge_values=torch.from_numpy(ev).cuda())
+    assert mre(got.cpu().numpy(), want) <= 1e-5
+
+
+def test_panel_strided_and_deterministic():
+    g = GRAPHS[0][1]
+    dg = DeviceGraph.from_csr(g.node_pointer, g.edge_list, g.values)
+    big = torch.from_numpy(sg.dense_random(g.num_nodes, 72, 3)).cuda()
+    x = big[:, 4:68]  # ldx = 72, 16-byte aligned start
+    out = torch.zeros((g.num_nodes, 80), device="cuda")
+    dg.spmm(x, out=out[:, 8:72])
+    want = O.spmm(oracle_csr(g), x.cpu().numpy())
+    assert mre(out[:, 8:72].cpu().numpy(), want) <= 1e-5
+    assert torch.all(out[:, :8] == 0) and torch.all(out[:, 72:] == 0)
+    a = dg.spmm(x.contiguous())
+    for _ in range(3):
+        assert torch.equal(a, dg.spmm(x.contiguous()))
+
+
+def test_panel_nonfinite():
+    g = sg.CsrGraph(200, np.array([0] + [2] * 200), np.array([0, 1]), np.ones(2, np.float32))
+    t = sg.sgt_transform(g)
+    x = np.zeros((200, 32), np.float32)
+    x[1, 5] = np.inf
+    with pytest.raises(sg.NonFiniteError):
+        sg.spmm_hybrid(t, x)
