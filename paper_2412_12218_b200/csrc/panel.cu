@@ -38,6 +38,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -248,8 +249,9 @@ struct PanelCfg {
   static constexpr int PB = PREC == SGTK_FP32 ? 3 : 1;  // B planes (split3)
   static constexpr uint32_t A_BYTES = kPanelRows * kChunkCols * 4;  // 16 KB, K-major
   static constexpr uint32_t B_BYTES = kChunkCols * DC * 4;          // MN-major
-  static constexpr uint32_t STAGE = PA * A_BYTES + PB * B_BYTES;    // multiple of 1024
-  static constexpr int NS = PREC == SGTK_FP32 ? 2 : 4;              // stage ring depth
+  static constexpr uint32_t A_STAGE = PA * A_BYTES;                 // multiple of 1024
+  static constexpr uint32_t B_STAGE = PB * B_BYTES;                 // multiple of 1024
+  static constexpr int NS = PREC == SGTK_FP32 ? 2 : 4;              // A ring depth
   static constexpr int GW = 4 / NS;                                 // builder warps per chunk
   static constexpr int NV = PREC == SGTK_FP32 ? 2 : 1;              // entry (+ value) slots
   static constexpr int NF = 512 / DC;                               // TMEM accumulators
@@ -262,9 +264,9 @@ constexpr uint32_t kMaxND = 8;
 
 // Runtime shared-memory layout (host-computed from the graph's largest chunk).
 struct PanelSmem {
-  uint32_t nd;     // entry ring depth (multiple of NS, >= NS)
+  uint32_t nd;     // B-tile and entry ring depth (multiple of NS, >= NS)
   uint32_t dslot;  // bytes of one entry slot
-  uint32_t dring_off, total;
+  uint32_t bring_off, dring_off, total;
 };
 
 // Source of the zero rows that pad a panel's last chunk (cp.async needs a
@@ -295,20 +297,27 @@ __device__ __align__(16) float g_zero_row[64];
 template <int DC, int PREC>
 __global__ void __launch_bounds__(kPanelThreads, 1)
 spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict__ x, uint64_t ldx,
-                  uint64_t d, float* __restrict__ out, uint64_t ldo, int vec_out) {
+                  uint64_t d, float* __restrict__ out, uint64_t ldo, int vec_out,
+                  long long* __restrict__ trace) {
   using C = PanelCfg<DC, PREC>;
+  // optional timeline (SGTK_PANEL_TRACE): trace[(panel * 256 + chunk) * 8 + event]
+  auto mark = [&](uint32_t c, int ev) {
+    if (trace && blockIdx.x < 4 && c < 256) trace[((uint64_t(blockIdx.x) * 256 + c) * 8) + ev] = clock64();
+  };
   extern __shared__ __align__(16) uint8_t smem_raw[];
   // 1024-aligned base, derived by offset so the compiler keeps the shared
   // address space (LDS/STS rather than generic loads)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + C::NS;
-  uint64_t* bfull = empty + C::NS;
-  uint64_t* dfull = bfull + C::NS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // A stage built
+  uint64_t* empty = full + C::NS;                       // A stage consumed
+  uint64_t* bfull = empty + C::NS;                      // B tile landed
+  uint64_t* bempty = bfull + kMaxND;                    // B tile + entry slot consumed
+  uint64_t* dfull = bempty + kMaxND;                    // entries landed
   uint64_t* accfull = dfull + kMaxND;
   uint64_t* accempty = accfull + C::NF;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + C::NF);
-  uint8_t* ring = smem + kBarBytes;      // [NS] stages: A planes, B planes
+  uint8_t* ring = smem + kBarBytes;      // [NS] A stages (PA planes)
+  uint8_t* bring = smem + L.bring_off;   // [nd] B tiles (PB planes)
   uint8_t* dring = smem + L.dring_off;   // [nd] entry slots (+ [nd] value slots, FP32)
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -323,9 +332,12 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
     for (int i = 0; i < C::NS; ++i) {
       mbar_init(full + i, C::GW);  // the builder warps that own the chunk
       mbar_init(empty + i, 1);     // tcgen05.commit
-      mbar_init(bfull + i, 32);    // one cp.async.mbarrier.arrive.noinc per loader lane
     }
-    for (uint32_t i = 0; i < ND; ++i) mbar_init(dfull + i, 1);  // bulk copy (expect_tx)
+    for (uint32_t i = 0; i < ND; ++i) {
+      mbar_init(bfull + i, 32 * C::GW);  // cp.async.mbarrier.arrive.noinc per gathering lane
+      mbar_init(bempty + i, 1);          // tcgen05.commit
+      mbar_init(dfull + i, 1);           // bulk copy (expect_tx)
+    }
     for (int i = 0; i < C::NF; ++i) {
       mbar_init(accfull + i, 1);
       mbar_init(accempty + i, 4);
@@ -340,50 +352,35 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
 
   if (warp == 0) {
     // ------------------------------------------------------------ loader
-    // Entry slot of chunk c is reused by chunk c + nd; that chunk's copy is
-    // issued at iteration c + NS, after empty[] says MMA(c) -- hence the
-    // builder of c -- is done.  So copies run nd - NS chunks ahead.
-    const uint32_t LA = ND - C::NS;
-    auto entries = [&](uint32_t c) {
-      if (lane == 0 && c < nch) {
-        const uint32_t ds = c % ND;
-        const uint64_t e0 = pv.coff[c0 + c], e1 = pv.coff[c0 + c + 1];
-        const uint32_t bytes = uint32_t(e1 - e0) * 4u;
-        mbar_expect_tx(dfull + ds, bytes * C::NV);
-        if (bytes) {
-          bulk_load(dring + ds * L.dslot, pv.dent + e0, bytes, dfull + ds);
-          if constexpr (PREC == SGTK_FP32)
-            bulk_load(dring + (ND + ds) * L.dslot, pv.dval + e0, bytes, dfull + ds);
+    // Entry bulk copies (TMA engine) into a ring nd chunks deep; slot c % nd
+    // is free once MMA(c - nd) retired (bempty).  Chunk offsets are
+    // prefetched kLook chunks ahead so no global load sits on this path.
+    if (lane == 0) {
+      constexpr uint32_t kLook = 4;
+      uint64_t offq[kLook];
+#pragma unroll
+      for (uint32_t i = 0; i < kLook; ++i) offq[i] = i <= nch ? pv.coff[c0 + i] : 0u;
+      uint64_t off_tail = kLook <= nch ? pv.coff[c0 + kLook] : 0u;
+      for (uint32_t cb = 0; cb < nch; cb += kLook) {
+#pragma unroll
+        for (uint32_t i = 0; i < kLook; ++i) {
+          const uint32_t c = cb + i;
+          if (c >= nch) break;
+          const uint64_t e0 = offq[i], e1 = i + 1 < kLook ? offq[(i + 1) % kLook] : off_tail;
+          offq[i] = c + kLook <= nch ? pv.coff[c0 + c + kLook] : 0u;
+          if (i + 1 == kLook) off_tail = c + 1 + kLook <= nch ? pv.coff[c0 + c + 1 + kLook] : 0u;
+          const uint32_t ds = c % ND, dph = (c / ND) & 1u;
+          mbar_wait(bempty + ds, dph ^ 1u);
+          mark(c, 0);
+          const uint32_t bytes = uint32_t(e1 - e0) * 4u;
+          mbar_expect_tx(dfull + ds, bytes * C::NV);
+          if (bytes) {
+            bulk_load(dring + ds * L.dslot, pv.dent + e0, bytes, dfull + ds);
+            if constexpr (PREC == SGTK_FP32)
+              bulk_load(dring + (ND + ds) * L.dslot, pv.dval + e0, bytes, dfull + ds);
+          }
         }
       }
-    };
-    for (uint32_t c = 0; c < LA; ++c) entries(c);
-    uint32_t col = nch ? pv.dcols[uint64_t(c0) * kChunkCols + lane] : 0u;
-    for (uint32_t c = 0; c < nch; ++c) {
-      const uint32_t s = c % C::NS, ph = (c / C::NS) & 1u;
-      const uint32_t col_next =
-          c + 1 < nch ? pv.dcols[uint64_t(c0 + c + 1) * kChunkCols + lane] : 0u;
-      mbar_wait(empty + s, ph ^ 1u);
-      entries(c + LA);
-      const uint32_t bst = smem_u32(ring + s * C::STAGE + C::PA * C::A_BYTES);
-      // Cooperative, coalesced gather: an instruction moves RPI whole rows
-      // (DC / 4 lanes of 16 B per row).  Destination: MN-major
-      // SWIZZLE_128B_BASE32B (tc05.cuh desc_mn32): K-row k, 4-row groups
-      // 512 B apart, 32-feature blocks 4096 B apart, 32-byte chunks XOR (k % 4).
-      constexpr uint32_t LPR = DC / 4, RPI = 32 / LPR;
-      const uint32_t j = lane % LPR, jj = j & 7u;
-#pragma unroll
-      for (uint32_t t = 0; t < 32 / RPI; ++t) {
-        const uint32_t k = t * RPI + lane / LPR;
-        const uint32_t ck = __shfl_sync(0xFFFFFFFFu, col, k);
-        const bool real = ck != 0xFFFFFFFFu && int(4 * j) < dvalid;
-        const uint32_t dst = bst + (j >> 3) * 4096u + (k >> 2) * 512u + (k & 3u) * 128u +
-                             ((((jj >> 1) ^ (k & 3u)) << 5) | ((jj & 1u) << 4));
-        cp_async16(dst, real ? x + uint64_t(ck) * ldx + fbase + 4 * j : g_zero_row);
-      }
-      cp_async_arrive_noinc(bfull + s);
-      __syncwarp();
-      col = col_next;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -394,17 +391,20 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
         const uint32_t g = c / C::FOLD, buf = g % C::NF;
         const bool first = (c % C::FOLD) == 0;
         if (first && g >= uint32_t(C::NF)) mbar_wait(accempty + buf, ((g / C::NF) - 1u) & 1u);
+        const uint32_t ds = c % ND, dph = (c / ND) & 1u;
         mbar_wait(full + s, ph);
+        mark(c, 4);
         if constexpr (PREC == SGTK_TF32) {
           // B went straight from cp.async (generic proxy) to the MMA (async
           // proxy): acquire the copies, then order them for the async proxy.
-          mbar_wait(bfull + s, ph);
+          mbar_wait(bfull + ds, dph);
           fence_async_smem();
         }
         tc_fence_after();
+        mark(c, 5);
         const uint32_t dt = tmem + buf * DC;
-        const uint32_t a0 = smem_u32(ring + s * C::STAGE), a1 = a0 + C::A_BYTES;
-        const uint32_t b0 = a0 + C::PA * C::A_BYTES, b1 = b0 + C::B_BYTES, b2 = b1 + C::B_BYTES;
+        const uint32_t a0 = smem_u32(ring + s * C::A_STAGE), a1 = a0 + C::A_BYTES;
+        const uint32_t b0 = smem_u32(bring + ds * C::B_STAGE), b1 = b0 + C::B_BYTES, b2 = b1 + C::B_BYTES;
 #pragma unroll
         for (uint32_t ks = 0; ks < kChunkCols / 8; ++ks) {
           const uint32_t acc = (first && ks == 0) ? 0u : 1u;
@@ -420,50 +420,106 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
           }
         }
         umma_commit(empty + s);
+        umma_commit(bempty + ds);
         if ((c % C::FOLD) == C::FOLD - 1 || c + 1 == nch) umma_commit(accfull + buf);
       }
     }
   } else if (warp < 6) {
     // ------------------------------------------------------------ A builders
+    // Builder group c % NS owns chunk c: it gathers the chunk's B tile (PD =
+    // nd - NS chunks ahead, cp.async with completion signalled by the copy
+    // engine), zeroes and fills the A tile from the staged entries, and (FP32)
+    // splits B into TF32 planes.  NS chunks are in construction at once.
     const uint32_t b = warp - 2, grp = b % C::NS, sub = b / C::NS;
     const uint32_t gl = sub * 32 + lane;  // thread index inside the chunk's group
     constexpr uint32_t GT = C::GW * 32;
+    const uint32_t PD = ND - C::NS;
+    // gather the 32 feature rows of chunk cg (its B slot is free: MMA(cg - nd)
+    // retired before MMA(c - NS), which this group already waited for)
+    auto id_of = [&](uint32_t cg) {  // this lane's column id of chunk cg (lane = K-row)
+      return cg < nch ? __ldg(pv.dcols + uint64_t(c0 + cg) * kChunkCols + lane) : 0u;
+    };
+    auto gather_b = [&](uint32_t cg, uint32_t myid) {
+      const uint32_t ds = cg % ND;
+      const uint32_t bst = smem_u32(bring + ds * C::B_STAGE);
+      constexpr uint32_t LPR = DC / 4, RPG = GT / LPR;  // rows per group instruction
+      const uint32_t j = gl % LPR, jj = j & 7u;
+#pragma unroll
+      for (uint32_t t = 0; t < 32 / RPG; ++t) {
+        const uint32_t k = t * RPG + gl / LPR;
+        const uint32_t ck = __shfl_sync(0xFFFFFFFFu, myid, k);
+        const bool real = ck != 0xFFFFFFFFu && int(4 * j) < dvalid;
+        // MN-major SWIZZLE_128B_BASE32B (tc05.cuh desc_mn32): K-row k, 4-row
+        // groups 512 B apart, 32-feature blocks 4096 B apart, 32-byte chunks
+        // XOR (k % 4)
+        const uint32_t dst = bst + (j >> 3) * 4096u + (k >> 2) * 512u + (k & 3u) * 128u +
+                             ((((jj >> 1) ^ (k & 3u)) << 5) | ((jj & 1u) << 4));
+        cp_async16(dst, real ? x + uint64_t(ck) * ldx + fbase + 4 * j : g_zero_row);
+      }
+      cp_async_arrive_noinc(bfull + ds);
+    };
+    for (uint32_t c = grp; c < nch && c < grp + PD; c += C::NS) gather_b(c, id_of(c));
+    // ids of the next chunk to gather, loaded one iteration ahead
+    uint32_t idn = id_of(grp + PD);
     for (uint32_t c = grp; c < nch; c += C::NS) {
       const uint32_t s = c % C::NS, ph = (c / C::NS) & 1u;
       const uint32_t ds = c % ND, dph = (c / ND) & 1u;
-      uint8_t* st = ring + s * C::STAGE;
-      const uint32_t abase = smem_u32(st);
+      const uint32_t abase = smem_u32(ring + s * C::A_STAGE);
       const uint64_t e0 = pv.coff[c0 + c], e1 = pv.coff[c0 + c + 1];
       const uint32_t ne = uint32_t(e1 - e0);
       mbar_wait(empty + s, ph ^ 1u);
+      if (lane == 0) mark(c, 1);
+      if (c + PD < nch) gather_b(c + PD, idn);
+      idn = id_of(c + PD + C::NS);
 #pragma unroll 8
       for (uint32_t i = gl; i < C::PA * C::A_BYTES / 16; i += GT)
         st_shared_v4(abase + i * 16, 0u, 0u, 0u, 0u);
       mbar_wait(dfull + ds, dph);
+      if (lane == 0) mark(c, 2);
       if constexpr (C::GW > 1) named_bar(1 + grp, GT);
       else __syncwarp();
-      const uint32_t* ent = reinterpret_cast<const uint32_t*>(dring + ds * L.dslot);
-      const float* dv = reinterpret_cast<const float*>(dring + (ND + ds) * L.dslot);
-#pragma unroll 4
-      for (uint32_t i = gl; i < ne; i += GT) {
-        const uint32_t w = ent[i];
-        if (w & kEntrySkip) continue;
-        const uint32_t row = (w >> 5) & 127u, k = w & 31u;
-        const uint32_t off = (row >> 3) * 1024u + (row & 7u) * 128u +
-                             (((k >> 2) ^ (row & 7u)) << 4) + (k & 3u) * 4u;
-        if constexpr (PREC == SGTK_FP32) {
-          uint32_t s0, s1;
-          split2(dv[i], s0, s1);
-          st_shared_u32(abase + off, s0);
-          st_shared_u32(abase + C::A_BYTES + off, s1);
-        } else {
-          st_shared_u32(abase + off, w & 0xFFFFE000u);
+      // Scatter: each lane takes 4 consecutive entries (one 16-byte LDS),
+      // branch-free: padding entries land on a scratch word.
+      const uint32_t ent = smem_u32(dring + ds * L.dslot);
+      const uint32_t dv = smem_u32(dring + (ND + ds) * L.dslot);
+      const uint32_t junk = smem_u32(tmem_slot + 1);
+      for (uint32_t i0 = gl * 4; i0 < ne; i0 += GT * 4 * 4) {
+        uint4 w4[4];
+        float4 v4[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const uint32_t i = i0 + h * GT * 4;
+          w4[h] = i < ne ? ld_shared_u4(ent + i * 4) : make_uint4(kEntrySkip, kEntrySkip, kEntrySkip, kEntrySkip);
+          if constexpr (PREC == SGTK_FP32)
+            v4[h] = i < ne ? ld_shared_f4(dv + i * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const uint32_t ws[4] = {w4[h].x, w4[h].y, w4[h].z, w4[h].w};
+          const float vs[4] = {v4[h].x, v4[h].y, v4[h].z, v4[h].w};
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const uint32_t w = ws[k4];
+            const uint32_t row = (w >> 5) & 127u, k = w & 31u;
+            const uint32_t off = (row >> 3) * 1024u + (row & 7u) * 128u +
+                                 (((k >> 2) ^ (row & 7u)) << 4) + (k & 3u) * 4u;
+            const bool skip = (w & kEntrySkip) != 0;
+            if constexpr (PREC == SGTK_FP32) {
+              uint32_t s0, s1;
+              split2(vs[k4], s0, s1);
+              st_shared_u32(skip ? junk : abase + off, s0);
+              st_shared_u32(skip ? junk : abase + C::A_BYTES + off, s1);
+            } else {
+              st_shared_u32(skip ? junk : abase + off, w & 0xFFFFE000u);
+            }
+          }
         }
       }
       if constexpr (PREC == SGTK_FP32) {
-        // B tile: exact 3-plane split in place
-        mbar_wait(bfull + s, ph);
-        uint4* B = reinterpret_cast<uint4*>(st + C::PA * C::A_BYTES);
+        // B tile: exact 3-plane split in place (every lane of the group first
+        // waits for all copies of the tile)
+        mbar_wait(bfull + ds, dph);
+        uint4* B = reinterpret_cast<uint4*>(bring + ds * C::B_STAGE);
 #pragma unroll 4
         for (uint32_t i = gl; i < C::B_BYTES / 16; i += GT) {
           const uint4 v = B[i];
@@ -477,7 +533,10 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
       }
       fence_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(full + s);
+      if (lane == 0) {
+        mark(c, 3);
+        mbar_arrive(full + s);
+      }
     }
   } else {
     // ------------------------------------------------------------ accumulators
@@ -663,14 +722,15 @@ int device_major() {
 
 constexpr uint32_t kSmemCap = 227u * 1024u;
 
-// Entry slots sized for the graph's largest chunk; ring as deep as fits.
+// Entry slots sized for the graph's largest chunk; B/entry ring as deep as fits.
 template <int DC, int PREC>
 bool panel_smem(uint32_t max_entries, PanelSmem& L) {
   using C = PanelCfg<DC, PREC>;
   L.dslot = ((max_entries + 3) / 4 * 4 * 4 + 127) / 128 * 128;
-  L.dring_off = kBarBytes + C::NS * C::STAGE;
+  L.bring_off = kBarBytes + C::NS * C::A_STAGE;
   for (uint32_t nd = kMaxND; nd >= uint32_t(C::NS); nd -= C::NS) {
     L.nd = nd;
+    L.dring_off = L.bring_off + nd * C::B_STAGE;
     L.total = L.dring_off + nd * C::NV * L.dslot + 1024 /*alignment slack*/;
     if (L.total <= kSmemCap) return true;
   }
@@ -688,8 +748,24 @@ bool launch_dense(const PanelView& v, uint64_t P, uint32_t max_entries, const fl
                          int(kSmemCap));
   });
   dim3 grid(unsigned(P), unsigned((d + DC - 1) / DC));
+  static long long* trace = [] {
+    long long* t = nullptr;
+    if (std::getenv("SGTK_PANEL_TRACE")) {
+      cudaMalloc(&t, 4 * 256 * 8 * 8);
+      cudaMemset(t, 0, 4 * 256 * 8 * 8);
+    }
+    return t;
+  }();
   spmm_panel_kernel<DC, PREC><<<grid, kPanelThreads, L.total, s>>>(v, L, x, ldx, d, out, ldo,
-                                                                   vec_out);
+                                                                   vec_out, trace);
+  if (trace) {
+    std::vector<long long> h(4 * 256 * 8);
+    cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost);
+    if (FILE* f = std::fopen(std::getenv("SGTK_PANEL_TRACE"), "wb")) {
+      std::fwrite(h.data(), 8, h.size(), f);
+      std::fclose(f);
+    }
+  }
   CU_LAUNCH("spmm_panel_kernel");
   return true;
 }

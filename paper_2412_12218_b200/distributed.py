@@ -1,7 +1,8 @@
 """Multi-GPU row-window partition: one process per GPU, NCCL all-gather over NVLink.
 
-SURVEY.md §8(e).  Rows are split into contiguous ranges of whole 16-row
-windows balanced by edge count (sgtk_partition_windows).  Because windows are
+SURVEY.md §8(e).  Rows are split into contiguous ranges of whole 128-row
+panels (the unit of the tensor-core SpMM, panel.cu; 8 reference 16-row
+windows) balanced by edge count (sgtk_partition_windows).  Because panels are
 independent (the reference's window-independence property,
 /root/reference/proj/tests/test_sgt_transform.cpp:133-158) and work-unit
 splitting depends on a window alone, each rank's transform of its slice equals
@@ -25,8 +26,12 @@ import torch.distributed as dist
 from ._lib import check, lib
 
 
-def partition(node_pointer: np.ndarray, num_nodes: int, parts: int, blk_h: int = 16) -> np.ndarray:
-    """Window bounds u64[parts+1] (edge-balanced, whole windows)."""
+ROW_QUANTUM = 128  # panel height: slices made of whole panels keep every output bit
+
+
+def partition(node_pointer: np.ndarray, num_nodes: int, parts: int,
+              blk_h: int = ROW_QUANTUM) -> np.ndarray:
+    """Panel bounds u64[parts+1] (edge-balanced, whole panels)."""
     b = np.zeros(parts + 1, np.uint64)
     np_ = np.ascontiguousarray(node_pointer, np.uint64)
     check(lib().sgtk_partition_windows(np_.ctypes.data, C.c_uint64(num_nodes), blk_h, parts,
@@ -34,7 +39,8 @@ def partition(node_pointer: np.ndarray, num_nodes: int, parts: int, blk_h: int =
     return b
 
 
-def row_ranges(bounds: np.ndarray, num_nodes: int, blk_h: int = 16) -> list[tuple[int, int]]:
+def row_ranges(bounds: np.ndarray, num_nodes: int,
+               blk_h: int = ROW_QUANTUM) -> list[tuple[int, int]]:
     return [(min(num_nodes, int(bounds[p]) * blk_h), min(num_nodes, int(bounds[p + 1]) * blk_h))
             for p in range(len(bounds) - 1)]
 
@@ -75,8 +81,8 @@ class RowSlice:
 
         self.n = num_nodes
         self.rank, self.world, self.group = rank, world, group
-        self.bounds = partition(node_pointer, num_nodes, world, blk_h)
-        self.ranges = row_ranges(self.bounds, num_nodes, blk_h)
+        self.bounds = partition(node_pointer, num_nodes, world)  # whole 128-row panels
+        self.ranges = row_ranges(self.bounds, num_nodes)
         self.r0, self.r1 = self.ranges[rank]
         np_loc, el_loc, v_loc = local_csr(node_pointer, edge_list, values, self.r0, self.r1)
         if world == 1:
