@@ -1,0 +1,634 @@
+// AGNN layer on 128-row panels: tensor-core attention over the dense
+// columns, CUDA-core attention over the sparse edges, fused normalisation.
+//
+// Replaces one layer of agnn_forward (/root/reference/proj/src/gnn.cpp:107-116):
+//   z = l2_normalize_rows(h)                         (gnn.cpp:74-91)
+//   logits_e = beta * <z_row, z_col>                 (sddmm_hybrid, tile_exec.cpp:316-411)
+//   attn = edge_softmax(logits)                      (gnn.cpp:54-72)
+//   h' = spmm_hybrid(t, h, attn)                     (tile_exec.cpp:200-314)
+// without materialising logits or attention.
+//
+// Softmax offset.  Rows of z have unit (or zero) norm, so every logit lies in
+// [-|beta|, |beta|]: exp(logit - |beta|) is in [exp(-2|beta|), 1] and the
+// softmax needs no running maximum (the reference subtracts the row max,
+// gnn.cpp:60-66; the ratio is the same).  Used for |beta| <= kMaxBeta, where
+// exp(-2|beta|) stays a normal float; larger |beta| runs the other modes.
+//
+// Dense part (agnn_dense_kernel, one CTA per panel, 11 warps):
+//   warps 0-3   softmax, thread per row: Q = z[panel rows] into the K-major A
+//               operand once; per chunk: S row from TMEM, mask, P = exp2(..),
+//               row sum l, P (TF32 / split) into a K-major A tile
+//   warps 4-7   accumulators: fold each FOLD-chunk O group from TMEM into
+//               fp32 registers; write (O, l) partials
+//   warp 8      MMA issuer: S(c+1) = Q Z_c+1^T ahead of O += P(c) H_c
+//   warps 9-10  loaders (even / odd chunks): cp.async gathers of the chunk's
+//               z rows (K-major B of S), h rows (MN-major B of PV), row masks
+// Sparse part + finalisation (agnn_rows_kernel, warp per row / hub segment):
+//   logits of the row's sparse edges (lane = edge dot products), exp, l and O
+//   updates (lane = feature), out = O / l, then the next layer's l2 norm.
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <mutex>
+
+#include "kernels.cuh"
+#include "tc05.cuh"
+
+namespace sgtkcu {
+namespace {
+
+using namespace tc05;
+
+constexpr float kMaxBeta = 40.0f;
+constexpr int kAgnnThreads = 352;
+
+template <int DC, int PREC>
+struct AgnnCfg {
+  static constexpr bool F32 = PREC == SGTK_FP32;
+  static constexpr int PQ = F32 ? 2 : 1;  // Q planes (hi, lo)
+  static constexpr int PZ = F32 ? 2 : 1;  // z-tile planes
+  static constexpr int PH = F32 ? 2 : 1;  // h-tile planes
+  static constexpr int PP = F32 ? 2 : 1;  // P planes
+  static constexpr uint32_t Q_BYTES = kPanelRows * DC * 4;  // K-major, DC/32 K-blocks of 16 KB
+  static constexpr uint32_t T_BYTES = kChunkCols * DC * 4;  // one 32-row tile
+  static constexpr uint32_t M_BYTES = kPanelRows * 4;       // row masks
+  static constexpr uint32_t SLOT = ((PZ + PH) * T_BYTES + M_BYTES + 1023) / 1024 * 1024;
+  static constexpr uint32_t P_BYTES = kPanelRows * kChunkCols * 4;  // 16 KB
+  static constexpr int NB = F32 ? (DC == 32 ? 4 : 2) : 6;  // gather ring
+  static constexpr int NP = 2;                             // P ring
+  static constexpr int NF = DC == 32 ? 8 : 4;              // O accumulators
+  static constexpr uint32_t FOLD = 4;
+  static constexpr uint32_t Q_OFF = 1024;
+  static constexpr uint32_t B_OFF = Q_OFF + PQ * Q_BYTES;
+  static constexpr uint32_t P_OFF = B_OFF + NB * SLOT;
+  static constexpr uint32_t SMEM = P_OFF + NP * PP * P_BYTES + 1024;
+  static_assert(SMEM <= 227u * 1024u, "agnn panel smem");
+};
+
+__device__ __align__(16) float g_agnn_zero[64];
+
+// K-major SWIZZLE_128B offset of element (row, k) in a tile with `rows` rows:
+// 128-byte K blocks of 32 fp32, rows*128 bytes apart.
+__device__ __forceinline__ uint32_t kmaj_off(uint32_t row, uint32_t k, uint32_t rows) {
+  return (k >> 5) * rows * 128u + (row >> 3) * 1024u + (row & 7u) * 128u +
+         ((((k >> 2) & 7u) ^ (row & 7u)) << 4) + (k & 3u) * 4u;
+}
+
+template <int DC, int PREC>
+__global__ void __launch_bounds__(kAgnnThreads, 1)
+agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const float* __restrict__ z,
+                  const float* __restrict__ z1, const float* __restrict__ h,
+                  const float* __restrict__ h1, uint64_t ld, uint64_t d, uint64_t row_offset,
+                  float beta, float* __restrict__ opart, float* __restrict__ lpart) {
+  using C = AgnnCfg<DC, PREC>;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(smem);  // [NB] gathers landed
+  uint64_t* bempty = bfull + C::NB;                     // [NB] PV(c) retired
+  uint64_t* sfull = bempty + C::NB;                     // [2]  S(c) in TMEM
+  uint64_t* pfull = sfull + 2;                          // [NP] P(c) written
+  uint64_t* pempty = pfull + C::NP;                     // [NP] PV(c) retired
+  uint64_t* qfull = pempty + C::NP;                     // [1]  Q operand ready
+  uint64_t* accfull = qfull + 1;                        // [NF]
+  uint64_t* accempty = accfull + C::NF;                 // [NF]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + C::NF);
+  float* lbuf = reinterpret_cast<float*>(smem + 512);   // [128] row sums
+  uint8_t* qs = smem + C::Q_OFF;
+  uint8_t* bs = smem + C::B_OFF;
+  uint8_t* ps = smem + C::P_OFF;
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t p = blockIdx.x;
+  const uint32_t c0 = pv.cptr[p], nch = pv.cptr[p + 1] - c0;
+  const uint32_t ngroups = (nch + C::FOLD - 1) / C::FOLD;
+  const int dvalid = d < uint64_t(DC) ? int(d) : DC;
+  const float bl2 = beta * 1.4426950408889634f, off = fabsf(beta) * 1.4426950408889634f;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NB; ++i) {
+      mbar_init(bfull + i, 32);  // cp.async.mbarrier.arrive.noinc, one per loader lane
+      mbar_init(bempty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) mbar_init(sfull + i, 1);
+    for (int i = 0; i < C::NP; ++i) {
+      mbar_init(pfull + i, 4);
+      mbar_init(pempty + i, 1);
+    }
+    mbar_init(qfull, 4);
+    for (int i = 0; i < C::NF; ++i) {
+      mbar_init(accfull + i, 1);
+      mbar_init(accempty + i, 4);
+    }
+    mbar_init_fence();
+  }
+  if (warp == 8) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t s_col = 0, o_col = 64;  // TMEM columns: S[2] x 32, O[NF] x DC
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ softmax
+    const uint32_t r = warp * 32 + lane;
+    const uint64_t grow = p * kPanelRows + r;
+    const bool rv = grow < pv.n_rows;
+    {  // Q = z[panel rows]: K-major A operand (TF32: RNE; FP32: split2)
+      const float* src = zraw + (row_offset + grow) * ld;
+      const uint32_t qb = smem_u32(qs);
+#pragma unroll
+      for (int j = 0; j < DC / 4; ++j) {
+        float4 v = (rv && 4 * j < dvalid) ? __ldg(reinterpret_cast<const float4*>(src) + j)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        const uint32_t o = kmaj_off(r, 4 * j, kPanelRows);
+        if constexpr (C::F32) {
+          uint32_t a0, a1, b0, b1, c0_, c1, d0, d1;
+          split2(v.x, a0, a1); split2(v.y, b0, b1); split2(v.z, c0_, c1); split2(v.w, d0, d1);
+          st_shared_v4(qb + o, a0, b0, c0_, d0);
+          st_shared_v4(qb + C::Q_BYTES + o, a1, b1, c1, d1);
+        } else {
+          st_shared_v4(qb + o, tf32_op(v.x), tf32_op(v.y), tf32_op(v.z), tf32_op(v.w));
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qfull);
+    }
+    float l = 0.0f;
+    const uint32_t pb = smem_u32(ps);
+    for (uint32_t c = 0; c < nch; ++c) {
+      const uint32_t sb = c & 1u, sph = (c >> 1) & 1u;
+      const uint32_t ds = c % C::NB, dph = (c / C::NB) & 1u;
+      const uint32_t pslot = c % C::NP, pph = (c / C::NP) & 1u;
+      mbar_wait(bfull + ds, dph);  // row masks of the chunk
+      const uint32_t mask = ld_shared_u32(smem_u32(bs + ds * C::SLOT) + (C::PZ + C::PH) * C::T_BYTES + r * 4);
+      mbar_wait(sfull + sb, sph);
+      tc_fence_after();
+      uint32_t sv[32];
+      tmem_ld16(tmem + ((warp * 32u) << 16) + s_col + sb * 32, *reinterpret_cast<uint32_t(*)[16]>(sv));
+      tmem_ld16(tmem + ((warp * 32u) << 16) + s_col + sb * 32 + 16,
+                *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
+      tmem_ld_wait();
+      tc_fence_before();
+      float pr[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float e = exp2f(fmaf(__uint_as_float(sv[j]), bl2, -off));
+        pr[j] = (mask >> j) & 1u ? e : 0.0f;
+        if constexpr (!C::F32) pr[j] = tf32_rne(pr[j]);
+        l += pr[j];
+      }
+      mbar_wait(pempty + pslot, pph ^ 1u);  // PV(c - NP) done with this P slot
+      const uint32_t pt = pb + pslot * C::PP * C::P_BYTES;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t o = kmaj_off(r, 4 * q, kPanelRows);
+        if constexpr (C::F32) {
+          uint32_t a0, a1, b0, b1, c0_, c1, d0, d1;
+          split2(pr[4 * q], a0, a1); split2(pr[4 * q + 1], b0, b1);
+          split2(pr[4 * q + 2], c0_, c1); split2(pr[4 * q + 3], d0, d1);
+          st_shared_v4(pt + o, a0, b0, c0_, d0);
+          st_shared_v4(pt + C::P_BYTES + o, a1, b1, c1, d1);
+        } else {
+          st_shared_v4(pt + o, __float_as_uint(pr[4 * q]), __float_as_uint(pr[4 * q + 1]),
+                       __float_as_uint(pr[4 * q + 2]), __float_as_uint(pr[4 * q + 3]));
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(pfull + pslot);
+    }
+    lbuf[r] = l;
+    named_bar(1, 256);  // l handed to the accumulator warps
+  } else if (warp < 8) {
+    // ------------------------------------------------------------ accumulators
+    const uint32_t q = warp & 3u;
+    const uint32_t r = q * 32 + lane;
+    const uint64_t grow = p * kPanelRows + r;
+    float acc[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j) acc[j] = 0.0f;
+    for (uint32_t g = 0; g < ngroups; ++g) {
+      const uint32_t buf = g % C::NF;
+      mbar_wait(accfull + buf, (g / C::NF) & 1u);
+      tc_fence_after();
+#pragma unroll
+      for (int cc = 0; cc < DC; cc += 16) {
+        uint32_t v[16];
+        tmem_ld16(tmem + ((q * 32u) << 16) + o_col + buf * DC + cc, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[cc + j] += __uint_as_float(v[j]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(accempty + buf);
+    }
+    named_bar(1, 256);
+    if (grow < pv.n_rows) {
+      float* o = opart + grow * DC;
+#pragma unroll
+      for (int j = 0; j < DC / 4; ++j)
+        reinterpret_cast<float4*>(o)[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+      lpart[grow] = lbuf[r];
+    }
+  } else if (warp == 8) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && nch) {
+      constexpr uint32_t id_s = idesc_tf32(32, false);  // N = 32 chunk columns, B K-major
+      constexpr uint32_t id_o = idesc_tf32(DC, true);   // N = DC features, B MN-major
+      const uint32_t qb = smem_u32(qs), pb = smem_u32(ps);
+      mbar_wait(qfull, 0);
+      tc_fence_after();
+      auto issue_s = [&](uint32_t c) {
+        const uint32_t ds = c % C::NB;
+        mbar_wait(bfull + ds, (c / C::NB) & 1u);
+        fence_async_smem();  // cp.async (generic proxy) -> MMA (async proxy)
+        tc_fence_after();
+        const uint32_t zt = smem_u32(bs + ds * C::SLOT);
+        const uint32_t dt = tmem + s_col + (c & 1u) * 32;
+#pragma unroll
+        for (uint32_t ks = 0; ks < DC / 8; ++ks) {
+          const uint32_t ko = (ks >> 2) * 16384u + (ks & 3u) * 32u;  // Q: 128-row K blocks
+          const uint32_t kz = (ks >> 2) * 4096u + (ks & 3u) * 32u;   // z tile: 32-row K blocks
+          const uint64_t q0 = umma_desc(qb + ko), z0 = umma_desc(zt + kz);
+          if constexpr (C::F32) {
+            umma_tf32(dt, q0, umma_desc(zt + C::T_BYTES + kz), id_s, ks ? 1u : 0u);
+            umma_tf32(dt, umma_desc(qb + C::Q_BYTES + ko), z0, id_s, 1u);
+            umma_tf32(dt, q0, z0, id_s, 1u);
+          } else {
+            umma_tf32(dt, q0, z0, id_s, ks ? 1u : 0u);
+          }
+        }
+        umma_commit(sfull + (c & 1u));
+      };
+      issue_s(0);
+      for (uint32_t c = 0; c < nch; ++c) {
+        // S(c+1) ahead of PV(c): its S buffer was released by pfull(c - 1)
+        if (c + 1 < nch) issue_s(c + 1);
+        const uint32_t ds = c % C::NB, pslot = c % C::NP;
+        const uint32_t g = c / C::FOLD, buf = g % C::NF;
+        const bool first = (c % C::FOLD) == 0;
+        if (first && g >= uint32_t(C::NF)) mbar_wait(accempty + buf, ((g / C::NF) - 1u) & 1u);
+        mbar_wait(pfull + pslot, (c / C::NP) & 1u);
+        tc_fence_after();
+        const uint32_t pt = pb + pslot * C::PP * C::P_BYTES;
+        const uint32_t ht = smem_u32(bs + ds * C::SLOT) + C::PZ * C::T_BYTES;
+        const uint32_t dt = tmem + o_col + buf * DC;
+#pragma unroll
+        for (uint32_t ks = 0; ks < kChunkCols / 8; ++ks) {
+          const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+          const uint64_t p0 = umma_desc(pt + ks * 32), h0 = desc_mn32(ht + ks * 1024, 4096, 512);
+          if constexpr (C::F32) {
+            umma_tf32(dt, p0, desc_mn32(ht + C::T_BYTES + ks * 1024, 4096, 512), id_o, acc);
+            umma_tf32(dt, umma_desc(pt + C::P_BYTES + ks * 32), h0, id_o, 1u);
+            umma_tf32(dt, p0, h0, id_o, 1u);
+          } else {
+            umma_tf32(dt, p0, h0, id_o, acc);
+          }
+        }
+        umma_commit(pempty + pslot);
+        umma_commit(bempty + ds);
+        if ((c % C::FOLD) == C::FOLD - 1 || c + 1 == nch) umma_commit(accfull + buf);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ loaders
+    // warp 9 takes even chunks, warp 10 odd ones.  Per chunk: 32 z rows
+    // (K-major SWIZZLE_128B B of S), 32 h rows (MN-major SWIZZLE_128B_BASE32B
+    // B of PV), 128 row masks; completion via cp.async.mbarrier.arrive.noinc.
+    const uint32_t par = warp - 9;
+    for (uint32_t c = par; c < nch; c += 2) {
+      const uint32_t ds = c % C::NB;
+      mbar_wait(bempty + ds, ((c / C::NB) & 1u) ^ 1u);
+      const uint32_t col = pv.dcols[uint64_t(c0 + c) * kChunkCols + lane];
+      const uint32_t zt = smem_u32(bs + ds * C::SLOT);
+      const uint32_t ht = zt + C::PZ * C::T_BYTES;
+      constexpr uint32_t LPR = DC / 4, RPI = 32 / LPR;
+      const uint32_t j = lane % LPR, jj = j & 7u;
+#pragma unroll
+      for (uint32_t t = 0; t < 32 / RPI; ++t) {
+        const uint32_t k = t * RPI + lane / LPR;  // chunk row (B row / K row)
+        const uint32_t ck = __shfl_sync(0xFFFFFFFFu, col, k);
+        const bool real = ck != 0xFFFFFFFFu && int(4 * j) < dvalid;
+        const uint64_t gofs = uint64_t(ck) * ld + 4 * j;
+        // z: K-major SWIZZLE_128B, row k, 16-byte piece j
+        const uint32_t zo = (j >> 3) * 4096u + (k >> 3) * 1024u + (k & 7u) * 128u + ((jj ^ (k & 7u)) << 4);
+        // h: MN-major SWIZZLE_128B_BASE32B (tc05.cuh desc_mn32)
+        const uint32_t ho = (j >> 3) * 4096u + (k >> 2) * 512u + (k & 3u) * 128u +
+                            ((((jj >> 1) ^ (k & 3u)) << 5) | ((jj & 1u) << 4));
+        cp_async16(zt + zo, real ? z + gofs : g_agnn_zero);
+        cp_async16(ht + ho, real ? h + gofs : g_agnn_zero);
+        if constexpr (C::F32) {  // lo planes (pre-split once per layer)
+          cp_async16(zt + C::T_BYTES + zo, real ? z1 + gofs : g_agnn_zero);
+          cp_async16(ht + C::T_BYTES + ho, real ? h1 + gofs : g_agnn_zero);
+        }
+      }
+      cp_async16(zt + (C::PZ + C::PH) * C::T_BYTES + lane * 16,
+                 pv.dmask + (uint64_t(c0 + c) * kPanelRows) + lane * 4);
+      cp_async_arrive_noinc(bfull + ds);
+    }
+    cp_async_wait<0>();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Sparse edges + finalisation.  One warp per item: a row (all rows are items:
+// every row needs out = O / l), or a <= kSegEdges segment of a hub row whose
+// (O, l) partial is combined in order by agnn_long_rows_kernel.
+//   logits: lane = edge, dot(z_row, z_col) over the features (z_row held in
+//           registers, z_col rows read whole: 128/256-byte lines);
+//   update: lane = feature, 8 edges' h rows in flight (coalesced).
+// Finalise: out = O / l (l = 0: no edges -> 0, as spmm of an empty row);
+// then the next layer's l2 norm (double sum, gnn.cpp:74-91), z_next and the
+// TF32 / split operand copies for the next dense pass.
+// ---------------------------------------------------------------------------
+
+template <int FPL, int PREC>
+__device__ __forceinline__ void agnn_finalize(uint64_t r, const float (&o)[FPL], float l, uint32_t lane,
+                                              int fv, const AgnnNext& nx, unsigned long long& nz) {
+  float v[FPL];
+  const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;
+#pragma unroll
+  for (int i = 0; i < FPL; ++i) v[i] = l > 0.0f ? o[i] * inv_l : 0.0f;
+  const uint64_t f = uint64_t(lane) * FPL;
+#pragma unroll
+  for (int i = 0; i < FPL; ++i)
+    if (i < fv) nx.out[r * nx.ldo + f + i] = v[i];
+  if (!nx.z) return;
+  double sq = 0.0;
+#pragma unroll
+  for (int i = 0; i < FPL; ++i)
+    if (i < fv) sq += double(v[i]) * double(v[i]);
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o2);
+  const float inv = sq == 0.0 ? 0.0f : float(1.0 / sqrt(sq));
+  if (sq == 0.0 && lane == 0) ++nz;
+#pragma unroll
+  for (int i = 0; i < FPL; ++i) {
+    const float zz = i < fv ? v[i] * inv : 0.0f, hh = i < fv ? v[i] : 0.0f;
+    if (i < fv) nx.z[r * nx.ldq + f + i] = zz;
+    if constexpr (PREC == SGTK_FP32) {
+      uint32_t a0, a1, b0, b1;
+      split2(zz, a0, a1);
+      split2(hh, b0, b1);
+      nx.zq[r * nx.ldq + f + i] = __uint_as_float(a0);
+      nx.zq1[r * nx.ldq + f + i] = __uint_as_float(a1);
+      nx.hq[r * nx.ldq + f + i] = __uint_as_float(b0);
+      nx.hq1[r * nx.ldq + f + i] = __uint_as_float(b1);
+    } else {
+      nx.zq[r * nx.ldq + f + i] = tf32_rne(zz);
+      nx.hq[r * nx.ldq + f + i] = tf32_rne(hh);
+    }
+  }
+}
+
+// ld: row stride of z / h (raw fp32 copies, rounded in registers for TF32)
+template <int FPL, int PREC>
+__global__ void __launch_bounds__(256)
+agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2* __restrict__ sent,
+                 const float* __restrict__ z, uint64_t ld, const float* __restrict__ h, uint64_t ldh,
+                 uint64_t d,
+                 uint64_t row_offset, float beta, const float* __restrict__ opart,
+                 const float* __restrict__ lpart, float* __restrict__ seg_o,
+                 float* __restrict__ seg_l, AgnnNext nx) {
+  constexpr int DC = 32 * FPL;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t f = uint64_t(lane) * FPL;
+  const int fv = f >= d ? 0 : (d - f >= uint64_t(FPL) ? FPL : int(d - f));
+  const float bl2 = beta * 1.4426950408889634f, off = fabsf(beta) * 1.4426950408889634f;
+  unsigned long long nz = 0;
+  for (uint64_t it = warp; it < n_items; it += nw) {
+    const uint4 w = items[it];
+    const uint64_t r = w.x;
+    const bool direct = w.w == 0xFFFFFFFFu;
+    // z of the row, whole (every lane): the dot products run lane = edge
+    float zr[DC];
+    const float* zrow = z + (row_offset + r) * ld;
+#pragma unroll
+    for (int k = 0; k < DC / 4; ++k) {
+      const float4 v = 4 * k < int(d) ? __ldg(reinterpret_cast<const float4*>(zrow) + k)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      zr[4 * k] = v.x; zr[4 * k + 1] = v.y; zr[4 * k + 2] = v.z; zr[4 * k + 3] = v.w;
+      if constexpr (PREC == SGTK_TF32) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) zr[4 * k + q] = tf32_rne(zr[4 * k + q]);
+      }
+    }
+    float o[FPL], l;
+    if (direct) {
+#pragma unroll
+      for (int i = 0; i < FPL; ++i) o[i] = i < fv ? opart[r * DC + f + i] : 0.0f;
+      l = lpart[r];
+    } else {
+#pragma unroll
+      for (int i = 0; i < FPL; ++i) o[i] = 0.0f;
+      l = 0.0f;
+    }
+    for (uint32_t e = w.y; e < w.z; e += 32) {
+      const uint32_t cnt = min(32u, w.z - e);
+      const uint32_t col = lane < cnt ? sent[e + lane].x : 0u;
+      // logits, lane = edge
+      float s = 0.0f;
+      if (lane < cnt) {
+        const float4* zc = reinterpret_cast<const float4*>(z + uint64_t(col) * ld);
+#pragma unroll
+        for (int k = 0; k < DC / 4; ++k) {
+          float4 v = 4 * k < int(d) ? __ldg(zc + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+          if constexpr (PREC == SGTK_TF32) {
+            v.x = tf32_rne(v.x); v.y = tf32_rne(v.y); v.z = tf32_rne(v.z); v.w = tf32_rne(v.w);
+          }
+          s = fmaf(zr[4 * k], v.x, s);
+          s = fmaf(zr[4 * k + 1], v.y, s);
+          s = fmaf(zr[4 * k + 2], v.z, s);
+          s = fmaf(zr[4 * k + 3], v.w, s);
+        }
+      }
+      if constexpr (PREC == SGTK_TF32) s = tf32_rne(s);  // sddmm TF32 rounds the dot (tile_exec.cpp:386)
+      float pe = lane < cnt ? exp2f(fmaf(s, bl2, -off)) : 0.0f;
+      if constexpr (PREC == SGTK_TF32) pe = tf32_rne(pe);
+      // update, lane = feature
+      for (uint32_t u0 = 0; u0 < cnt; u0 += 8) {
+        float hv[8][FPL];
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) {
+          const uint32_t c = __shfl_sync(0xFFFFFFFFu, col, (u0 + u) & 31u);
+          const float* src = h + uint64_t(c) * ldh + f;
+#pragma unroll
+          for (int i = 0; i < FPL; ++i) hv[u][i] = (u0 + u < cnt && i < fv) ? __ldg(src + i) : 0.0f;
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) {
+          const float pu = __shfl_sync(0xFFFFFFFFu, pe, (u0 + u) & 31u);
+          if (u0 + u < cnt) {
+            l += pu;
+#pragma unroll
+            for (int i = 0; i < FPL; ++i) {
+              float hh = hv[u][i];
+              if constexpr (PREC == SGTK_TF32) hh = tf32_rne(hh);
+              o[i] = fmaf(pu, hh, o[i]);
+            }
+          }
+        }
+      }
+    }
+    if (direct) {
+      agnn_finalize<FPL, PREC>(r, o, l, lane, fv, nx, nz);
+    } else {
+#pragma unroll
+      for (int i = 0; i < FPL; ++i)
+        if (i < fv) seg_o[uint64_t(w.w) * DC + f + i] = o[i];
+      if (lane == 0) seg_l[w.w] = l;
+    }
+  }
+  if (nx.zeros && lane == 0 && nz) atomicAdd(nx.zeros, nz);
+}
+
+// Hub rows: (O, l) = dense partial + segment partials in segment order, then
+// the same finalisation.  One warp per hub row.
+template <int FPL, int PREC>
+__global__ void agnn_long_rows_kernel(const uint4* __restrict__ lrows, uint64_t n_long, uint64_t d,
+                                      const float* __restrict__ opart, const float* __restrict__ lpart,
+                                      const float* __restrict__ seg_o, const float* __restrict__ seg_l,
+                                      AgnnNext nx) {
+  constexpr int DC = 32 * FPL;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t f = uint64_t(lane) * FPL;
+  const int fv = f >= d ? 0 : (d - f >= uint64_t(FPL) ? FPL : int(d - f));
+  unsigned long long nz = 0;
+  for (uint64_t i = warp; i < n_long; i += nw) {
+    const uint4 w = lrows[i];
+    const uint64_t r = w.x;
+    float o[FPL];
+#pragma unroll
+    for (int k = 0; k < FPL; ++k) o[k] = k < fv ? opart[r * DC + f + k] : 0.0f;
+    float l = lpart[r];
+    for (uint32_t sgi = 0; sgi < w.z; ++sgi) {
+#pragma unroll
+      for (int k = 0; k < FPL; ++k)
+        if (k < fv) o[k] += seg_o[uint64_t(w.y + sgi) * DC + f + k];
+      l += seg_l[w.y + sgi];
+    }
+    agnn_finalize<FPL, PREC>(r, o, l, lane, fv, nx, nz);
+  }
+  if (nx.zeros && lane == 0 && nz) atomicAdd(nx.zeros, nz);
+}
+
+// operand copies of the first layer's input: TF32 -> rounded (z, h);
+// FP32 -> hi / lo planes of z and h
+template <int PREC>
+__global__ void agnn_prep_kernel(const float* __restrict__ z, const float* __restrict__ h, uint64_t ldh,
+                                 uint64_t rows, uint64_t d, uint64_t ldq, float* __restrict__ zq,
+                                 float* __restrict__ zq1, float* __restrict__ hq, float* __restrict__ hq1) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows * ldq;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / ldq, c = i - r * ldq;
+    const float zz = c < d ? z[r * ldq + c] : 0.0f, hh = c < d ? h[r * ldh + c] : 0.0f;
+    if constexpr (PREC == SGTK_FP32) {
+      uint32_t a0, a1, b0, b1;
+      split2(zz, a0, a1);
+      split2(hh, b0, b1);
+      zq[i] = __uint_as_float(a0);
+      zq1[i] = __uint_as_float(a1);
+      hq[i] = __uint_as_float(b0);
+      hq1[i] = __uint_as_float(b1);
+    } else {
+      zq[i] = tf32_rne(zz);
+      hq[i] = tf32_rne(hh);
+    }
+  }
+}
+
+inline unsigned blocks_for(uint64_t n, unsigned bs = 256) {
+  return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + bs - 1) / bs, 148ull * 16)));
+}
+
+template <int DC, int PREC>
+void launch_agnn_dense(const PanelView& v, uint64_t P, const float* zraw, const float* zq, const float* zq1,
+                       const float* hq, const float* hq1, uint64_t ldq, uint64_t d,
+                       uint64_t row_offset, float beta, float* opart, float* lpart, cudaStream_t s) {
+  using C = AgnnCfg<DC, PREC>;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(agnn_dense_kernel<DC, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(C::SMEM));
+  });
+  agnn_dense_kernel<DC, PREC><<<unsigned(P), kAgnnThreads, C::SMEM, s>>>(
+      v, zraw, zq, zq1, hq, hq1, ldq, d, row_offset, beta, opart, lpart);
+  CU_LAUNCH("agnn_dense_kernel");
+}
+
+template <int FPL, int PREC>
+void launch_agnn_rows(const Panels& pn, const float* z, uint64_t ld, const float* h, uint64_t ldh,
+                      uint64_t d,
+                      uint64_t row_offset, float beta, const float* opart, const float* lpart,
+                      float* seg_o, float* seg_l, const AgnnNext& nx, cudaStream_t s) {
+  if (pn.n_aitems) {
+    agnn_rows_kernel<FPL, PREC><<<blocks_for(pn.n_aitems * 32), 256, 0, s>>>(
+        pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), z, ld, h, ldh, d, row_offset, beta,
+        opart, lpart, seg_o, seg_l, nx);
+    CU_LAUNCH("agnn_rows_kernel");
+  }
+  if (pn.n_long) {
+    agnn_long_rows_kernel<FPL, PREC><<<blocks_for(pn.n_long * 32), 256, 0, s>>>(
+        pn.lrows->as<uint4>(), pn.n_long, d, opart, lpart, seg_o, seg_l, nx);
+    CU_LAUNCH("agnn_long_rows_kernel");
+  }
+}
+
+}  // namespace
+
+bool agnn_panel_supported(const sgtk_graph* g, uint64_t d, float beta) {
+  return g->panels && panel_enabled() && d > 0 && d <= 64 && std::fabs(beta) <= kMaxBeta &&
+         g->n_cols <= 0x7FFFFFFFull;
+}
+
+// One AGNN layer.  z: l2-normalised input rows (raw fp32, n_cols x ldq);
+// zq/zq1/hq/hq1: MMA operand copies of z and of the input h (TF32: rounded;
+// FP32: hi / lo planes), stride ldq; h: the raw input rows (stride ldh).
+// Writes nx.out (n_rows x d) and, when nx.z is set, the next layer's z and
+// operand copies (which must not alias the inputs).
+void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, const float* zq1,
+                      const float* hq, const float* hq1, uint64_t ldq, const float* h, uint64_t ldh,
+                      uint64_t d, float beta, int prec, float* opart, float* lpart, float* seg_o,
+                      float* seg_l, const AgnnNext& nx, cudaStream_t s) {
+  const Panels& pn = *g->panels;
+  PanelView v = panel_view(g);
+  const uint64_t ro = g->row_offset;
+  if (prec == SGTK_FP32) {
+    if (ldq == 32) launch_agnn_dense<32, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, s);
+    else launch_agnn_dense<64, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, s);
+    if (ldq == 32) launch_agnn_rows<1, SGTK_FP32>(pn, z, ldq, h, ldh, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
+    else launch_agnn_rows<2, SGTK_FP32>(pn, z, ldq, h, ldh, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
+  } else {
+    if (ldq == 32) launch_agnn_dense<32, SGTK_TF32>(v, pn.P, z, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, s);
+    else launch_agnn_dense<64, SGTK_TF32>(v, pn.P, z, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, s);
+    if (ldq == 32) launch_agnn_rows<1, SGTK_TF32>(pn, z, ldq, hq, ldq, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
+    else launch_agnn_rows<2, SGTK_TF32>(pn, z, ldq, hq, ldq, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
+  }
+}
+
+void agnn_prep_launch(const float* z, const float* h, uint64_t ldh, uint64_t rows, uint64_t d,
+                      uint64_t ldq, int prec, float* zq, float* zq1, float* hq, float* hq1,
+                      cudaStream_t s) {
+  if (!rows) return;
+  if (prec == SGTK_FP32)
+    agnn_prep_kernel<SGTK_FP32><<<blocks_for(rows * ldq), 256, 0, s>>>(z, h, ldh, rows, d, ldq, zq, zq1, hq, hq1);
+  else
+    agnn_prep_kernel<SGTK_TF32><<<blocks_for(rows * ldq), 256, 0, s>>>(z, h, ldh, rows, d, ldq, zq, zq1, hq, hq1);
+  CU_LAUNCH("agnn_prep_kernel");
+}
+
+}  // namespace sgtkcu

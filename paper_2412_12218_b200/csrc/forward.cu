@@ -109,11 +109,90 @@ void gcn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint32_t L,
   if (hf) raise(SGTK_ERR_NONFINITE, "gcn_forward: output contains NaN or Inf");
 }
 
-uint64_t agnn_workspace(const sgtk_graph* g, uint64_t d) {
+uint64_t agnn_workspace_chain(const sgtk_graph* g, uint64_t d) {
   return 2 * align256(g->n_rows * ld4(d) * 4) + align256(g->n_cols * 4) +
          align256(g->n_cols * ld4(d) * 4) +
          align256(std::max<uint64_t>(g->nnz, 1) * 4) + align256(16 * 4);
 }
+
+// mode 2 (panels): two sets of {z, zq, zq1, hq, hq1} (n_cols x ldq; the next
+// layer's set is written while the current one is read), layer outputs
+// (2 x n_rows x ld4(d)), dense partials (n_rows x (ldq + 1)), hub segment
+// partials, zero counter.
+uint64_t agnn_workspace_panel(const sgtk_graph* g, uint64_t d) {
+  if (!g->panels || d > 64) return 0;
+  const uint64_t ldq = d <= 32 ? 32 : 64;
+  const auto& pn = *g->panels;
+  return 10 * align256(g->n_cols * ldq * 4) + 2 * align256(g->n_rows * ld4(d) * 4) +
+         align256(g->n_rows * ldq * 4) + align256(g->n_rows * 4) +
+         align256(std::max<uint64_t>(pn.n_segs, 1) * ldq * 4) +
+         align256(std::max<uint64_t>(pn.n_segs, 1) * 4) + align256(16 * 4);
+}
+
+uint64_t agnn_workspace(const sgtk_graph* g, uint64_t d) {
+  return std::max(agnn_workspace_chain(g, d), agnn_workspace_panel(g, d));
+}
+
+namespace {
+// mode 2: every layer on the 128-row panels (agnn_panel.cu)
+void agnn_forward_panel(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d, uint32_t L,
+                        const float* betas, int prec, void* ws, float* out, uint64_t ldo,
+                        uint64_t* zero_rows_host, cudaStream_t s) {
+  const uint64_t N = g->n_rows, NC = g->n_cols;
+  const uint64_t ldq = d <= 32 ? 32 : 64, ldb = ld4(d);
+  const auto& pn = *g->panels;
+  char* p = static_cast<char*>(ws);
+  auto take = [&](uint64_t bytes) {
+    float* r = reinterpret_cast<float*>(p);
+    p += align256(bytes);
+    return r;
+  };
+  float* set[2][5];
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 5; ++b) set[a][b] = take(NC * ldq * 4);  // z, zq, zq1, hq, hq1
+  float* buf[2] = {take(N * ldb * 4), take(N * ldb * 4)};
+  float* opart = take(N * ldq * 4);
+  float* lpart = take(N * 4);
+  float* seg_o = take(std::max<uint64_t>(pn.n_segs, 1) * ldq * 4);
+  float* seg_l = take(std::max<uint64_t>(pn.n_segs, 1) * 4);
+  uint64_t* zeros = reinterpret_cast<uint64_t*>(p);
+  CU(cudaMemsetAsync(zeros, 0, 8, s));
+  // padding features [d, ldq) of every operand row must read as zeros
+  if (d < ldq)
+    CU(cudaMemsetAsync(set[0][0], 0, reinterpret_cast<char*>(set[1][4]) - reinterpret_cast<char*>(set[0][0]) +
+                                         NC * ldq * 4, s));
+  // layer 0 input: z = l2norm(x), operand copies
+  l2norm_launch(x, NC, d, ldx, set[0][0], ldq, nullptr, zeros, s);
+  agnn_prep_launch(set[0][0], x, ldx, NC, d, ldq, prec, set[0][1], set[0][2], set[0][3], set[0][4], s);
+  const float* h = x;
+  uint64_t ldh = ldx;
+  for (uint32_t l = 0; l < L; ++l) {
+    const bool last = l + 1 == L;
+    float** cur = set[l & 1];
+    float** nxt = set[(l + 1) & 1];
+    AgnnNext nx{};
+    nx.out = last ? out : buf[l & 1];
+    nx.ldo = last ? ldo : ldb;
+    nx.ldq = ldq;
+    nx.zeros = reinterpret_cast<unsigned long long*>(zeros);
+    if (!last) {
+      nx.z = nxt[0];
+      nx.zq = nxt[1];
+      nx.zq1 = nxt[2];
+      nx.hq = nxt[3];
+      nx.hq1 = nxt[4];
+    }
+    agnn_panel_layer(g, cur[0], cur[1], cur[2], cur[3], cur[4], ldq, h, ldh, d, betas[l], prec,
+                     opart, lpart, seg_o, seg_l, nx, s);
+    h = nx.out;
+    ldh = nx.ldo;
+  }
+  if (zero_rows_host) {
+    CU(cudaMemcpyAsync(zero_rows_host, zeros, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+  }
+}
+}  // namespace
 
 void agnn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d, uint32_t L,
                   const float* betas, const uint32_t* cut, int prec, int mode, void* ws,
@@ -133,6 +212,15 @@ void agnn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
   if (g->n_rows != g->n_cols && L > 1)
     raise(SGTK_ERR_SHAPE, "agnn_forward: a row-slice graph runs one layer per call "
                           "(all-gather the slices between layers)");
+  if (mode == 2) {
+    bool ok = !cut && L > 0;
+    for (uint32_t l = 0; ok && l < L; ++l) ok = agnn_panel_supported(g, d, betas[l]);
+    if (ok) {
+      agnn_forward_panel(g, x, ldx, d, L, betas, prec, ws, out, ldo, zero_rows_host, s);
+      return;
+    }
+    mode = 1;  // outside the panel path's envelope: fused 16-row windows
+  }
   CU(cudaMemsetAsync(zeros, 0, 8, s));
 
   if (L == 0) {

@@ -63,6 +63,7 @@ struct Panels {
   std::shared_ptr<DevBuf> dent;   // u32[n_dent]  tf32(value) | skip<<12 | row<<5 | k
   std::shared_ptr<DevBuf> dval;   // f32[n_dent]  full fp32 value
   std::shared_ptr<DevBuf> deid;   // u32[n_dent]  CSR edge id (0xFFFFFFFF for padding)
+  std::shared_ptr<DevBuf> dmask;  // u32[n_chunks * 128] row r's edge bits in the chunk (AGNN)
   std::shared_ptr<DevBuf> sptr;   // u32[n_rows+1] sparse edges of a row
   std::shared_ptr<DevBuf> sent;   // uint2[n_sparse] (column, value bits)
   std::shared_ptr<DevBuf> seid;   // u32[n_sparse] CSR edge id
@@ -72,6 +73,10 @@ struct Panels {
   uint64_t n_items = 0, n_long = 0, n_segs = 0;
   std::shared_ptr<DevBuf> items;  // uint4[n_items] (row, e_begin, e_end, segment | ~0u)
   std::shared_ptr<DevBuf> lrows;  // uint4[n_long]  (row, first segment, segments, 0)
+  // AGNN work list: every row is an item (out = O / l everywhere); hub rows
+  // as the same segments as above
+  uint64_t n_aitems = 0;
+  std::shared_ptr<DevBuf> aitems;  // uint4[n_aitems]
 };
 
 struct PanelView {
@@ -83,6 +88,7 @@ struct PanelView {
   const float* dval;
   const uint32_t* sptr;
   const uint2* sent;
+  const uint32_t* dmask;
 };
 
 // POD view handed to kernels.

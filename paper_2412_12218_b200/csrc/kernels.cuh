@@ -43,6 +43,29 @@ bool spmm_panel_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64
                        const float* ev, int prec, float* out, uint64_t ldo, uint32_t* nonfinite,
                        cudaStream_t s);
 
+// AGNN layer on panels (agnn_panel.cu)
+struct AgnnNext {
+  float* out;         // layer output h'
+  uint64_t ldo;
+  float* z;           // next layer z (raw; nullptr on the last layer)
+  float* zq;          // next-layer MMA operand copies (TF32-rounded / hi planes)
+  float* zq1;         //   lo planes (FP32)
+  float* hq;
+  float* hq1;
+  uint64_t ldq;
+  unsigned long long* zeros;
+};
+bool agnn_panel_supported(const sgtk_graph* g, uint64_t d, float beta);
+void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, const float* zq1,
+                      const float* hq, const float* hq1, uint64_t ldq, const float* h, uint64_t ldh,
+                      uint64_t d, float beta, int prec, float* opart, float* lpart, float* seg_o,
+                      float* seg_l, const AgnnNext& nx, cudaStream_t s);
+void agnn_prep_launch(const float* z, const float* h, uint64_t ldh, uint64_t rows, uint64_t d,
+                      uint64_t ldq, int prec, float* zq, float* zq1, float* hq, float* hq1,
+                      cudaStream_t s);
+PanelView panel_view(const sgtk_graph* g);
+bool panel_enabled();
+
 // Host-side split plan (make_split_plan, tile_exec.cpp:150-161).
 std::vector<uint32_t> split_plan_host(const sgtk_graph* g, double ratio);
 

@@ -150,6 +150,16 @@ __global__ void entry_fill_kernel(const uint32_t* __restrict__ e2r, const uint32
   }
 }
 
+// Row masks per chunk: bit k of dmask[chunk][row] <=> edge (row, chunk col k)
+__global__ void chunk_mask_kernel(const uint64_t* __restrict__ coff, uint64_t NC,
+                                  const uint32_t* __restrict__ dent, uint32_t* __restrict__ dmask) {
+  for (uint64_t c = blockIdx.x; c < NC; c += gridDim.x)
+    for (uint64_t i = coff[c] + threadIdx.x; i < coff[c + 1]; i += blockDim.x) {
+      const uint32_t w = dent[i];
+      if (!(w & kEntrySkip)) atomicOr(dmask + c * kPanelRows + ((w >> 5) & 127u), 1u << (w & 31u));
+    }
+}
+
 // sparse (CUDA-core) edges: per-row count, then per-row stable compaction
 __global__ void sparse_count_kernel(const uint64_t* __restrict__ np, uint64_t n,
                                     const uint32_t* __restrict__ e2c, const uint64_t* __restrict__ wo,
@@ -883,6 +893,12 @@ void build_panels(sgtk_graph& g, cudaStream_t s) {
         pn->coff->as<uint64_t>(), vals, E, ccnt.as<uint32_t>(), pn->dent->as<uint32_t>(),
         pn->dval->as<float>(), pn->deid->as<uint32_t>());
   CU_LAUNCH("entry_fill_kernel");
+  pn->dmask = std::make_shared<DevBuf>(std::max<uint64_t>(NC, 1) * kPanelRows * 4);
+  CU(cudaMemsetAsync(pn->dmask->p, 0, pn->dmask->bytes, s));
+  if (NC)
+    chunk_mask_kernel<<<grid_for(NC, 1, 148u * 16u), 128, 0, s>>>(
+        pn->coff->as<uint64_t>(), NC, pn->dent->as<uint32_t>(), pn->dmask->as<uint32_t>());
+  CU_LAUNCH("chunk_mask_kernel");
 
   DevBuf scnt((n + 1) * 4);
   CU(cudaMemsetAsync(scnt.p, 0, (n + 1) * 4, s));
@@ -907,22 +923,27 @@ void build_panels(sgtk_graph& g, cudaStream_t s) {
   // CUDA-core work list (host, O(N)): a row's sparse edges form one item;
   // hub rows are cut into kSegEdges segments reduced in order afterwards.
   std::vector<uint32_t> sp = dl<uint32_t>(pn->sptr->p, n + 1, s);
-  std::vector<uint4> items, lrows;
+  std::vector<uint4> items, lrows, aitems;
   uint32_t seg = 0;
   for (uint64_t r = 0; r < n; ++r) {
     const uint32_t b = sp[r], e = sp[r + 1];
-    if (b == e) continue;
     if (e - b <= kSegEdges) {
-      items.push_back(make_uint4(uint32_t(r), b, e, 0xFFFFFFFFu));
+      if (b != e) items.push_back(make_uint4(uint32_t(r), b, e, 0xFFFFFFFFu));
+      aitems.push_back(make_uint4(uint32_t(r), b, e, 0xFFFFFFFFu));
     } else {
       const uint32_t k = (e - b + kSegEdges - 1) / kSegEdges;
       lrows.push_back(make_uint4(uint32_t(r), seg, k, 0u));
-      for (uint32_t i = 0; i < k; ++i)
-        items.push_back(make_uint4(uint32_t(r), b + i * kSegEdges, std::min(e, b + (i + 1) * kSegEdges),
-                                   seg + i));
+      for (uint32_t i = 0; i < k; ++i) {
+        const uint4 it = make_uint4(uint32_t(r), b + i * kSegEdges,
+                                    std::min(e, b + (i + 1) * kSegEdges), seg + i);
+        items.push_back(it);
+        aitems.push_back(it);
+      }
       seg += k;
     }
   }
+  pn->n_aitems = aitems.size();
+  pn->aitems = ul(aitems.data(), aitems.size(), s);
   pn->n_items = items.size();
   pn->n_long = lrows.size();
   pn->n_segs = seg;
@@ -944,6 +965,7 @@ PanelView panel_view(const sgtk_graph* g) {
   v.dval = pn.dval->as<float>();
   v.sptr = pn.sptr->as<uint32_t>();
   v.sent = pn.sent->as<uint2>();
+  v.dmask = pn.dmask->as<uint32_t>();
   return v;
 }
 

@@ -143,3 +143,37 @@ def test_panel_nonfinite():
     x[1, 5] = np.inf
     with pytest.raises(sg.NonFiniteError):
         sg.spmm_hybrid(t, x)
+
+
+# ------------------------------------------------------------ AGNN, mode 2
+# agnn_panel.cu: tensor-core attention over dense panel columns, CUDA-core
+# attention over sparse edges.  Bars: FP32 <= 1e-5 (as test_gpu_parity.py),
+# TF32 vs the oracle's TF32 mode <= 2e-3 (the tolerance the fused modes use:
+# rounded logits / attention, tile_exec.cpp:386,402).
+@pytest.mark.parametrize("name,g", GRAPHS, ids=[n for n, _ in GRAPHS])
+@pytest.mark.parametrize("d", [16, 32, 41, 64])
+def test_panel_agnn(name, g, d):
+    t = sg.sgt_transform(g)
+    ga = Csr.of(g.num_nodes, g.node_pointer, g.edge_list)
+    x = sg.dense_random(g.num_nodes, d, d + 3)
+    betas = [1.0, -0.7, 2.5]
+    want, zw = O.agnn_forward(ga, x, betas)
+    got, zg = sg.agnn_forward(t, x, betas, mode=2, return_zeros=True)
+    assert mre(got, want) <= 1e-5
+    assert zg == zw
+    want_t, _ = O.agnn_forward(ga, x, betas, tf32=True)
+    assert mre(sg.agnn_forward(t, x, betas, precision="tf32", mode=2), want_t) <= 2e-3
+
+
+def test_panel_agnn_deterministic_and_fallback():
+    g = GRAPHS[3][1]  # hub panel: segments of a hub row combine in order
+    dg = DeviceGraph.from_csr(g.node_pointer, g.edge_list)
+    x = torch.from_numpy(sg.dense_random(g.num_nodes, 32, 4)).cuda()
+    a = dg.agnn_forward(x, [1.0, 1.0], mode=2)
+    for _ in range(2):
+        assert torch.equal(a, dg.agnn_forward(x, [1.0, 1.0], mode=2))
+    # |beta| beyond the fixed-offset envelope: runs the fused 16-row mode
+    ga = Csr.of(g.num_nodes, g.node_pointer, g.edge_list)
+    want, _ = O.agnn_forward(ga, x.cpu().numpy(), [60.0])
+    got = dg.agnn_forward(x, [60.0], mode=2).cpu().numpy()
+    assert mre(got, want) <= 1e-5

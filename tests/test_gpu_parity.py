@@ -313,10 +313,14 @@ def test_agnn_vs_reference(key):
                    G[f"{key}_agnn/agnn_tf0"]) <= TOL_FP32
     assert mre(sg.agnn_forward(t, x, betas, precision="tf32", mode=1),
                G[f"{key}_agnn/agnn_tf1"]) <= 2e-3
+    # panel mode (agnn_panel.cu)
+    assert mre(sg.agnn_forward(t, x, betas, mode=2), G[f"{key}_agnn/agnn_tf0"]) <= TOL_FP32
+    assert mre(sg.agnn_forward(t, x, betas, precision="tf32", mode=2),
+               G[f"{key}_agnn/agnn_tf1"]) <= 2e-3
 
 
 @pytest.mark.parametrize("name,g", big_graphs())
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 2])
 def test_agnn_large_windows(name, g, mode):
     # split windows: the fused kernel merges (m, l, O) states across units
     c = Csr.of(g.num_nodes, g.node_pointer, g.edge_list)
@@ -328,7 +332,7 @@ def test_agnn_large_windows(name, g, mode):
                want) <= TOL_FP32
 
 
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 2])
 def test_agnn_kats(mode):
     t = sg.sgt_transform(sgcsr(csr("kat_agnn_zero")))
     out, z = sg.agnn_forward(t, G["kat_agnn_zero/x"], [1.0], return_zeros=True, mode=mode)

@@ -4,7 +4,7 @@
 #include "tc05.cuh"
 using namespace sgtkcu::tc05;
 
-template <int N, bool BMN>
+template <int N, bool BMN, bool AMN>
 __global__ void rate(long long* out, int iters) {
   extern __shared__ uint8_t raw[];
   uint8_t* sm = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
@@ -19,13 +19,14 @@ __global__ void rate(long long* out, int iters) {
   __syncthreads();
   tc_fence_after();
   if (tid == 0) {
-    constexpr uint32_t idesc = idesc_tf32(N, BMN);
+    constexpr uint32_t idesc = idesc_tf32(N, BMN) | (AMN ? (1u << 15) : 0u);
     const uint32_t a = smem_u32(sm), b = a + 16384;
     long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
       const uint32_t ks = i & 3;
       const uint64_t bd = BMN ? desc_mn32(b + ks * 1024, 4096, 512) : umma_desc(b + ks * 32);
-      umma_tf32(slot, umma_desc(a + ks * 32), bd, idesc, i ? 1u : 0u);
+      const uint64_t ad = AMN ? desc_mn32(a + ks * 4096, 512, 2048) : umma_desc(a + ks * 32);
+      umma_tf32(slot, ad, bd, idesc, i ? 1u : 0u);
     }
     long long t1 = clock64();
     umma_commit(&bar);
@@ -39,13 +40,13 @@ __global__ void rate(long long* out, int iters) {
   if (warp == 0) { tc_fence_after(); tmem_dealloc(slot, 512); }
 }
 
-template <int N, bool BMN>
+template <int N, bool BMN, bool AMN = false>
 void run(long long* d) {
-  cudaFuncSetAttribute(rate<N, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
-  rate<N, BMN><<<1, 128, 70 * 1024>>>(d, 4000);
+  cudaFuncSetAttribute(rate<N, BMN, AMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+  rate<N, BMN, AMN><<<1, 128, 70 * 1024>>>(d, 4000);
   long long h[2];
   cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-  printf("N=%3d B_MN=%d: issue %.1f cyc/mma, complete %.1f cyc/mma (%s)\n", N, BMN, h[0] / 4000.0, h[1] / 4000.0,
+  printf("A_MN=%d N=%3d B_MN=%d: issue %.1f cyc/mma, complete %.1f cyc/mma (%s)\n", AMN, N, BMN, h[0] / 4000.0, h[1] / 4000.0,
          cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -55,5 +56,6 @@ int main() {
   run<32, false>(d); run<32, true>(d);
   run<64, false>(d); run<64, true>(d);
   run<128, false>(d); run<128, true>(d);
+  run<32, true, true>(d); run<64, true, true>(d); run<128, true, true>(d);
   return 0;
 }
