@@ -247,16 +247,17 @@ def run_b200(args, wl):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     prec = args.precision
-    mode = 1 if args.mode == "fused" else 0
+    mode = {"panel": 2, "fused": 1, "chain": 0}[args.mode]
 
     t0 = time.perf_counter()
     g, gen = make_graph(wl, args.locality)
     N = g.num_nodes
     log(f"[bench] graph {N} nodes {g.num_edges} edges in {time.perf_counter() - t0:.1f}s")
-    # row-window partition (balanced by edges)
+    # row partition in whole 128-row panels (balanced by edges)
+    Q = 128
     bounds = np.zeros(world + 1, np.uint64)
-    check(lib().sgtk_partition_windows(g.node_pointer.ctypes.data, N, 16, world, bounds.ctypes.data))
-    r0, r1 = min(N, int(bounds[rank]) * 16), min(N, int(bounds[rank + 1]) * 16)
+    check(lib().sgtk_partition_windows(g.node_pointer.ctypes.data, N, Q, world, bounds.ctypes.data))
+    r0, r1 = min(N, int(bounds[rank]) * Q), min(N, int(bounds[rank + 1]) * Q)
     e0, e1 = int(g.node_pointer[r0]), int(g.node_pointer[r1])
     np_loc = (g.node_pointer[r0:r1 + 1] - np.uint64(e0)).astype(np.uint64)
     el_loc = g.edge_list[e0:e1]
@@ -294,14 +295,14 @@ def run_b200(args, wl):
     def allgather_rows(local_rows: torch.Tensor) -> torch.Tensor:
         if world == 1:
             return local_rows
-        maxr = int(max(min(N, int(bounds[p + 1]) * 16) - min(N, int(bounds[p]) * 16)
+        maxr = int(max(min(N, int(bounds[p + 1]) * Q) - min(N, int(bounds[p]) * Q)
                        for p in range(world)))
         pad = torch.zeros((maxr, local_rows.shape[1]), dtype=local_rows.dtype, device=dev)
         pad[:local_rows.shape[0]] = local_rows
         full = torch.empty((world * maxr, local_rows.shape[1]), dtype=local_rows.dtype, device=dev)
         dist.all_gather_into_tensor(full, pad)
-        parts = [full[p * maxr: p * maxr + (min(N, int(bounds[p + 1]) * 16) -
-                                            min(N, int(bounds[p]) * 16))] for p in range(world)]
+        parts = [full[p * maxr: p * maxr + (min(N, int(bounds[p + 1]) * Q) -
+                                            min(N, int(bounds[p]) * Q))] for p in range(world)]
         return torch.cat(parts)
 
     if wl["kind"] == "agnn":
@@ -324,8 +325,12 @@ def run_b200(args, wl):
             hh = allgather_rows(D.gemm(x[r0:r1], w_in, relu=True, precision=prec))
             return D.gemm(agnn_stack(hh), w_out, relu=False, precision=prec)
 
-        launches_per_step = L * (2 if mode == 1 else 4) + (
-            L if (mode == 1 and dg_has_splits(dg, 16)) or (mode == 0 and dg_has_splits(dg, 8)) else 0)
+        if mode == 2:
+            pi = dg.panel_info()
+            launches_per_step = 2 + L * (2 + (1 if pi["long_rows"] else 0))
+        else:
+            launches_per_step = L * (2 if mode == 1 else 4) + (
+                L if (mode == 1 and dg_has_splits(dg, 16)) or (mode == 0 and dg_has_splits(dg, 8)) else 0)
         layers_per_step = L
     else:
         layers = [(torch.from_numpy(w).to(dev), r) for w, r in
@@ -422,7 +427,7 @@ def run_b200(args, wl):
             "n_gpus": world, "steps": args.steps, "warmup": warm,
             "ms_per_step": round(step_ms, 4), "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32 (4-term TF32 split on tensor cores)" if prec == "fp32" else "tf32",
+            "dtype": "f32 (split-TF32 on tensor cores)" if prec == "fp32" else "tf32",
             "data": "synthetic (deterministic generator; random-init weights)",
             "config": config_of(args, wl, g, gen, {
                 "step": f"agnn_forward({L} layers) on the whole graph; value = step/{L}"
@@ -433,6 +438,12 @@ def run_b200(args, wl):
             "gpu_launches": launches_per_step * args.steps,
             "model_forward_ms": round(model_ms, 4), "kernels_ms": kern,
         }
+        if "roofline_unfused_formula" in extra and roof:
+            u = extra["roofline_unfused_formula"]
+            u["achieved"] = round(u["algorithmic_bytes"] / (roof["kernel_ms"] * 1e-3) / 1e9, 1)
+            u["unit"] = "GB/s"
+            u["frac"] = round(u["achieved"] / pk["hbm_gbs"], 4)
+            line["roofline_unfused_formula"] = u
         if "roofline_gemm" in extra:
             rg = extra["roofline_gemm"]
             rg["peak"] = pk["hbm_gbs"]
@@ -513,10 +524,33 @@ def kernel_breakdown(args, wl, dg, g, h, D, prec, mode, flush, stream, gcn_layer
                 "algorithmic_bytes": int(Bg), "formula": "s*N*K + 4*K*M + 4*N*M (SURVEY §8d B_gemm)",
                 "tflops": round(2 * N * K * M / (res["in_proj_gemm"] * 1e-3) / 1e12, 2),
                 "kernel_ms": round(res["in_proj_gemm"], 4)}
+        if mode == 2:
+            def panel_one():
+                check(L.sgtk_agnn_forward(dg.handle, h.data_ptr(), d, d, 1,
+                                          np.ones(1, np.float32).ctypes.data, None, pr, 2,
+                                          ws.data_ptr(), ws.numel(), out.data_ptr(), d, None, s))
+            res["agnn_layer_panel(l2norm+prep+dense+rows)"] = ev_time(panel_one)
+            check(L.sgtk_debug_set(1))  # tensor-core part only
+            res["panel_dense_part"] = ev_time(panel_one)
+            check(L.sgtk_debug_set(2))  # CUDA-core part only
+            res["panel_sparse_part"] = ev_time(panel_one)
+            check(L.sgtk_debug_set(0))
+            # one layer inside the 4-layer stack (input normalisation fused into the previous layer)
+            res["agnn_panel_layer"] = res["agnn_layer_panel(l2norm+prep+dense+rows)"] - res["l2norm"]
         s_ = 4
         B_fused = 8 * (N + 1) + 4 * E + 4 * N + 2 * s_ * N * d
         B_spmm = 8 * (N + 1) + 4 * E + 4 * E + s_ * N * d + 4 * N * d
-        if mode == 1:
+        if mode == 2:
+            name, B, t = "agnn_panel_layer (agnn_dense_kernel + agnn_rows_kernel)", B_fused, \
+                res["agnn_panel_layer"]
+            formula = "8(N+1) + 4E + 4N + 2*s*N*d (SURVEY §8d fused AGNN lower bound, s=4)"
+            extra["roofline_unfused_formula"] = {
+                "formula": "B_rownorm + B_sddmm + B_softmax + B_spmm (SURVEY §8d: report fusion "
+                           "against the unfused bytes)",
+                "algorithmic_bytes": int(8 * N * d + (8 * (N + 1) + 8 * E + 4 * N * d) +
+                                         (8 * (N + 1) + 8 * E) + B_spmm),
+            }
+        elif mode == 1:
             name, B, t = "agnn_fused_kernel", B_fused, res["agnn_fused_kernel"]
             formula = "8(N+1) + 4E + 4N + 2*s*N*d (SURVEY §8d fused AGNN lower bound, s=4)"
         else:
@@ -595,8 +629,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="reddit-agnn", choices=sorted(WORKLOADS))
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32"])
-    ap.add_argument("--mode", default="fused", choices=["fused", "chain"])
+    ap.add_argument("--precision", default="tf32", choices=["fp32", "tf32"])
+    ap.add_argument("--mode", default="panel", choices=["panel", "fused", "chain"])
     ap.add_argument("--locality", default="calibrated", choices=sorted(LOCALITY))
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     args = ap.parse_args()

@@ -132,8 +132,12 @@ int sgtk_graph_download(const sgtk_graph* g, uint32_t* edge_to_row,
  * counterpart: it is the device layout that replaces the reference's
  * per-window dense chunk staging, tile_exec.cpp:226-290).
  * info = {panels, dense_chunks, dense_entries (padded), sparse_edges,
- *         max_chunk_entries, dense_columns (padded)} */
-int sgtk_panel_info(const sgtk_graph* g, uint64_t info[6]);
+ *         max_chunk_entries, dense_columns (padded), hub_rows, hub_segments} */
+int sgtk_panel_info(const sgtk_graph* g, uint64_t info[8]);
+
+/* Timing experiments only: 0 = normal; 1 = tensor-core (dense) part of the
+ * panel kernels only; 2 = CUDA-core (sparse) part only (partial results). */
+int sgtk_debug_set(int mode);
 
 /* Download the panel arrays (sizes from sgtk_panel_info; any may be NULL):
  * chunk_ptr u32[P+1], dense_cols u32[32*chunks], chunk_off u64[chunks+1],

@@ -57,7 +57,8 @@ struct AgnnCfg {
   static constexpr uint32_t P_BYTES = kPanelRows * kChunkCols * 4;  // 16 KB
   static constexpr int NB = F32 ? (DC == 32 ? 4 : 2) : 6;  // gather ring
   static constexpr int NP = 2;                             // P ring
-  static constexpr int NF = DC == 32 ? 8 : 4;              // O accumulators
+  static constexpr int NF = DC == 32 ? 6 : 3;              // O accumulators (256 TMEM cols: 2 CTAs/SM)
+  static constexpr uint32_t TMEM_COLS = 256;
   static constexpr uint32_t FOLD = 4;
   static constexpr uint32_t Q_OFF = 1024;
   static constexpr uint32_t B_OFF = Q_OFF + PQ * Q_BYTES;
@@ -122,7 +123,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
     }
     mbar_init_fence();
   }
-  if (warp == 8) tmem_alloc(tmem_slot, 512);
+  if (warp == 8) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -336,7 +337,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
   __syncthreads();
   if (warp == 8) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, C::TMEM_COLS);
   }
 }
 
@@ -372,6 +373,7 @@ __device__ __forceinline__ void agnn_finalize(uint64_t r, const float (&o)[FPL],
   for (int o2 = 16; o2 > 0; o2 >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o2);
   const float inv = sq == 0.0 ? 0.0f : float(1.0 / sqrt(sq));
   if (sq == 0.0 && lane == 0) ++nz;
+  if (lane == 0) nx.norm[r] = float(sqrt(sq));
 #pragma unroll
   for (int i = 0; i < FPL; ++i) {
     const float zz = i < fv ? v[i] * inv : 0.0f, hh = i < fv ? v[i] : 0.0f;
@@ -391,17 +393,27 @@ __device__ __forceinline__ void agnn_finalize(uint64_t r, const float (&o)[FPL],
   }
 }
 
-// ld: row stride of z / h (raw fp32 copies, rounded in registers for TF32)
+// Sparse edges of a row, batches of 32:
+//   lane = edge: gather z_col (whole rows, 128/256 B), dot with z_row (held in
+//     registers by every lane), p = exp2(beta*log2e*s - |beta|*log2e); the
+//     z_col row and its coefficient p * |h_col| go to a per-warp smem tile
+//     (h_col = z_col * |h_col|: z is h scaled to unit norm, gnn.cpp:74-91, so
+//     the aggregation needs no second gather);
+//   lane = feature: O[f] += coef_e * T[e][f] over the batch, e ascending.
+// Row sums l: per-lane partials, reduced by a fixed shuffle tree per item.
 template <int FPL, int PREC>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(FPL == 1 ? 256 : 128)
 agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2* __restrict__ sent,
-                 const float* __restrict__ z, uint64_t ld, const float* __restrict__ h, uint64_t ldh,
-                 uint64_t d,
-                 uint64_t row_offset, float beta, const float* __restrict__ opart,
+                 const float* __restrict__ z, uint64_t ld, const float* __restrict__ norm,
+                 uint64_t d, uint64_t row_offset, float beta, const float* __restrict__ opart,
                  const float* __restrict__ lpart, float* __restrict__ seg_o,
                  float* __restrict__ seg_l, AgnnNext nx) {
   constexpr int DC = 32 * FPL;
-  const uint32_t lane = threadIdx.x & 31;
+  constexpr int TS = DC + 4;  // smem tile row stride (floats): 16-byte rows, spread banks
+  __shared__ __align__(16) float tile[FPL == 1 ? 8 : 4][32 * TS];
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float* T = tile[wib];
+  const uint32_t tb = smem_u32(T);
   const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const uint64_t f = uint64_t(lane) * FPL;
@@ -412,76 +424,73 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
     const uint4 w = items[it];
     const uint64_t r = w.x;
     const bool direct = w.w == 0xFFFFFFFFu;
-    // z of the row, whole (every lane): the dot products run lane = edge
-    float zr[DC];
-    const float* zrow = z + (row_offset + r) * ld;
+    const uint32_t c_first = w.y < w.z && lane < min(32u, w.z - w.y) ? sent[w.y + lane].x : 0u;
+    float zr[DC];  // z of the row, every lane (dot products run lane = edge)
+    const float4* zrow = reinterpret_cast<const float4*>(z + (row_offset + r) * ld);
 #pragma unroll
     for (int k = 0; k < DC / 4; ++k) {
-      const float4 v = 4 * k < int(d) ? __ldg(reinterpret_cast<const float4*>(zrow) + k)
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 v = __ldg(zrow + k);  // padding features are zeros
       zr[4 * k] = v.x; zr[4 * k + 1] = v.y; zr[4 * k + 2] = v.z; zr[4 * k + 3] = v.w;
-      if constexpr (PREC == SGTK_TF32) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) zr[4 * k + q] = tf32_rne(zr[4 * k + q]);
-      }
     }
-    float o[FPL], l;
-    if (direct) {
+    if constexpr (PREC == SGTK_TF32) {
 #pragma unroll
-      for (int i = 0; i < FPL; ++i) o[i] = i < fv ? opart[r * DC + f + i] : 0.0f;
-      l = lpart[r];
-    } else {
-#pragma unroll
-      for (int i = 0; i < FPL; ++i) o[i] = 0.0f;
-      l = 0.0f;
+      for (int k = 0; k < DC; ++k) zr[k] = tf32_rne(zr[k]);
     }
+    float o[FPL], lpp = 0.0f;
+#pragma unroll
+    for (int i = 0; i < FPL; ++i) o[i] = (direct && i < fv) ? opart[r * DC + f + i] : 0.0f;
+    const float l0 = direct ? lpart[r] : 0.0f;
+    uint32_t col = c_first;
     for (uint32_t e = w.y; e < w.z; e += 32) {
       const uint32_t cnt = min(32u, w.z - e);
-      const uint32_t col = lane < cnt ? sent[e + lane].x : 0u;
-      // logits, lane = edge
-      float s = 0.0f;
+      const uint32_t col_next = e + 32 < w.z && lane < min(32u, w.z - e - 32) ? sent[e + 32 + lane].x : 0u;
+      {  // cooperative, coalesced gather of the batch's z rows into the tile
+        constexpr uint32_t LPR = DC / 4, RPI = 32 / LPR;
+        const uint32_t j = lane % LPR;
+#pragma unroll
+        for (uint32_t t = 0; t < 32 / RPI; ++t) {
+          const uint32_t u = t * RPI + lane / LPR;
+          const uint32_t cu = __shfl_sync(0xFFFFFFFFu, col, u);
+          if (u < cnt) cp_async16(tb + (u * TS + 4 * j) * 4, z + uint64_t(cu) * ld + 4 * j);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp();
+      }
       if (lane < cnt) {
-        const float4* zc = reinterpret_cast<const float4*>(z + uint64_t(col) * ld);
+        float s = 0.0f;
 #pragma unroll
         for (int k = 0; k < DC / 4; ++k) {
-          float4 v = 4 * k < int(d) ? __ldg(zc + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+          float4 v = ld_shared_f4(tb + (lane * TS + 4 * k) * 4);
           if constexpr (PREC == SGTK_TF32) {
             v.x = tf32_rne(v.x); v.y = tf32_rne(v.y); v.z = tf32_rne(v.z); v.w = tf32_rne(v.w);
+            st_shared_v4(tb + (lane * TS + 4 * k) * 4, __float_as_uint(v.x), __float_as_uint(v.y),
+                         __float_as_uint(v.z), __float_as_uint(v.w));
           }
           s = fmaf(zr[4 * k], v.x, s);
           s = fmaf(zr[4 * k + 1], v.y, s);
           s = fmaf(zr[4 * k + 2], v.z, s);
           s = fmaf(zr[4 * k + 3], v.w, s);
         }
+        if constexpr (PREC == SGTK_TF32) s = tf32_rne(s);  // sddmm TF32 rounds the dot (tile_exec.cpp:386)
+        float pe = exp2f(fmaf(s, bl2, -off));
+        if constexpr (PREC == SGTK_TF32) pe = tf32_rne(pe);
+        lpp += pe;
+        T[lane * TS + DC] = pe * __ldg(norm + col);
       }
-      if constexpr (PREC == SGTK_TF32) s = tf32_rne(s);  // sddmm TF32 rounds the dot (tile_exec.cpp:386)
-      float pe = lane < cnt ? exp2f(fmaf(s, bl2, -off)) : 0.0f;
-      if constexpr (PREC == SGTK_TF32) pe = tf32_rne(pe);
-      // update, lane = feature
-      for (uint32_t u0 = 0; u0 < cnt; u0 += 8) {
-        float hv[8][FPL];
+      __syncwarp();
+#pragma unroll 8
+      for (uint32_t u = 0; u < cnt; ++u) {
+        const float cf = T[u * TS + DC];
 #pragma unroll
-        for (uint32_t u = 0; u < 8; ++u) {
-          const uint32_t c = __shfl_sync(0xFFFFFFFFu, col, (u0 + u) & 31u);
-          const float* src = h + uint64_t(c) * ldh + f;
-#pragma unroll
-          for (int i = 0; i < FPL; ++i) hv[u][i] = (u0 + u < cnt && i < fv) ? __ldg(src + i) : 0.0f;
-        }
-#pragma unroll
-        for (uint32_t u = 0; u < 8; ++u) {
-          const float pu = __shfl_sync(0xFFFFFFFFu, pe, (u0 + u) & 31u);
-          if (u0 + u < cnt) {
-            l += pu;
-#pragma unroll
-            for (int i = 0; i < FPL; ++i) {
-              float hh = hv[u][i];
-              if constexpr (PREC == SGTK_TF32) hh = tf32_rne(hh);
-              o[i] = fmaf(pu, hh, o[i]);
-            }
-          }
-        }
+        for (int i = 0; i < FPL; ++i) o[i] = fmaf(cf, T[u * TS + lane * FPL + i], o[i]);
       }
+      __syncwarp();
+      col = col_next;
     }
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) lpp += __shfl_xor_sync(0xFFFFFFFFu, lpp, o2);
+    const float l = l0 + lpp;
     if (direct) {
       agnn_finalize<FPL, PREC>(r, o, l, lane, fv, nx, nz);
     } else {
@@ -531,10 +540,12 @@ __global__ void agnn_long_rows_kernel(const uint4* __restrict__ lrows, uint64_t 
 template <int PREC>
 __global__ void agnn_prep_kernel(const float* __restrict__ z, const float* __restrict__ h, uint64_t ldh,
                                  uint64_t rows, uint64_t d, uint64_t ldq, float* __restrict__ zq,
-                                 float* __restrict__ zq1, float* __restrict__ hq, float* __restrict__ hq1) {
+                                 float* __restrict__ zq1, float* __restrict__ hq, float* __restrict__ hq1,
+                                 const float* __restrict__ inv, float* __restrict__ norm) {
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows * ldq;
        i += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t r = i / ldq, c = i - r * ldq;
+    if (c == 0) norm[r] = inv[r] > 0.0f ? 1.0f / inv[r] : 0.0f;  // |h| = 1 / inv
     const float zz = c < d ? z[r * ldq + c] : 0.0f, hh = c < d ? h[r * ldh + c] : 0.0f;
     if constexpr (PREC == SGTK_FP32) {
       uint32_t a0, a1, b0, b1;
@@ -571,13 +582,13 @@ void launch_agnn_dense(const PanelView& v, uint64_t P, const float* zraw, const 
 }
 
 template <int FPL, int PREC>
-void launch_agnn_rows(const Panels& pn, const float* z, uint64_t ld, const float* h, uint64_t ldh,
-                      uint64_t d,
+void launch_agnn_rows(const Panels& pn, const float* z, uint64_t ld, const float* norm, uint64_t d,
                       uint64_t row_offset, float beta, const float* opart, const float* lpart,
                       float* seg_o, float* seg_l, const AgnnNext& nx, cudaStream_t s) {
   if (pn.n_aitems) {
-    agnn_rows_kernel<FPL, PREC><<<blocks_for(pn.n_aitems * 32), 256, 0, s>>>(
-        pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), z, ld, h, ldh, d, row_offset, beta,
+    constexpr unsigned bs = FPL == 1 ? 256 : 128;
+    agnn_rows_kernel<FPL, PREC><<<blocks_for(pn.n_aitems * 32, bs), bs, 0, s>>>(
+        pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), z, ld, norm, d, row_offset, beta,
         opart, lpart, seg_o, seg_l, nx);
     CU_LAUNCH("agnn_rows_kernel");
   }
@@ -601,33 +612,58 @@ bool agnn_panel_supported(const sgtk_graph* g, uint64_t d, float beta) {
 // Writes nx.out (n_rows x d) and, when nx.z is set, the next layer's z and
 // operand copies (which must not alias the inputs).
 void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, const float* zq1,
-                      const float* hq, const float* hq1, uint64_t ldq, const float* h, uint64_t ldh,
+                      const float* hq, const float* hq1, uint64_t ldq, const float* norm,
                       uint64_t d, float beta, int prec, float* opart, float* lpart, float* seg_o,
                       float* seg_l, const AgnnNext& nx, cudaStream_t s) {
   const Panels& pn = *g->panels;
   PanelView v = panel_view(g);
   const uint64_t ro = g->row_offset;
+  const int dbg = panel_debug_mode();  // 1: dense part only, 2: sparse part only (timing)
+  if (dbg == 2) {
+    CU(cudaMemsetAsync(opart, 0, g->n_rows * ldq * 4, s));
+    CU(cudaMemsetAsync(lpart, 0, g->n_rows * 4, s));
+  }
+  if (dbg == 1) {
+    if (prec == SGTK_FP32) {
+      if (ldq == 32) launch_agnn_dense<32, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, s);
+      else launch_agnn_dense<64, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, s);
+    } else {
+      if (ldq == 32) launch_agnn_dense<32, SGTK_TF32>(v, pn.P, z, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, s);
+      else launch_agnn_dense<64, SGTK_TF32>(v, pn.P, z, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, s);
+    }
+    return;
+  }
+  if (dbg == 2) {
+    if (prec == SGTK_FP32) {
+      if (ldq == 32) launch_agnn_rows<1, SGTK_FP32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
+      else launch_agnn_rows<2, SGTK_FP32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
+    } else {
+      if (ldq == 32) launch_agnn_rows<1, SGTK_TF32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
+      else launch_agnn_rows<2, SGTK_TF32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
+    }
+    return;
+  }
   if (prec == SGTK_FP32) {
     if (ldq == 32) launch_agnn_dense<32, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, s);
     else launch_agnn_dense<64, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, s);
-    if (ldq == 32) launch_agnn_rows<1, SGTK_FP32>(pn, z, ldq, h, ldh, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
-    else launch_agnn_rows<2, SGTK_FP32>(pn, z, ldq, h, ldh, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
+    if (ldq == 32) launch_agnn_rows<1, SGTK_FP32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
+    else launch_agnn_rows<2, SGTK_FP32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
   } else {
     if (ldq == 32) launch_agnn_dense<32, SGTK_TF32>(v, pn.P, z, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, s);
     else launch_agnn_dense<64, SGTK_TF32>(v, pn.P, z, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, s);
-    if (ldq == 32) launch_agnn_rows<1, SGTK_TF32>(pn, z, ldq, hq, ldq, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
-    else launch_agnn_rows<2, SGTK_TF32>(pn, z, ldq, hq, ldq, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
+    if (ldq == 32) launch_agnn_rows<1, SGTK_TF32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
+    else launch_agnn_rows<2, SGTK_TF32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
   }
 }
 
 void agnn_prep_launch(const float* z, const float* h, uint64_t ldh, uint64_t rows, uint64_t d,
                       uint64_t ldq, int prec, float* zq, float* zq1, float* hq, float* hq1,
-                      cudaStream_t s) {
+                      const float* inv, float* norm, cudaStream_t s) {
   if (!rows) return;
   if (prec == SGTK_FP32)
-    agnn_prep_kernel<SGTK_FP32><<<blocks_for(rows * ldq), 256, 0, s>>>(z, h, ldh, rows, d, ldq, zq, zq1, hq, hq1);
+    agnn_prep_kernel<SGTK_FP32><<<blocks_for(rows * ldq), 256, 0, s>>>(z, h, ldh, rows, d, ldq, zq, zq1, hq, hq1, inv, norm);
   else
-    agnn_prep_kernel<SGTK_TF32><<<blocks_for(rows * ldq), 256, 0, s>>>(z, h, ldh, rows, d, ldq, zq, zq1, hq, hq1);
+    agnn_prep_kernel<SGTK_TF32><<<blocks_for(rows * ldq), 256, 0, s>>>(z, h, ldh, rows, d, ldq, zq, zq1, hq, hq1, inv, norm);
   CU_LAUNCH("agnn_prep_kernel");
 }
 

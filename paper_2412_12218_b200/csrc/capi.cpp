@@ -147,14 +147,18 @@ int sgtk_graph_info(const sgtk_graph* g, uint64_t info[11]) {
   });
 }
 
-int sgtk_panel_info(const sgtk_graph* g, uint64_t info[6]) {
+int sgtk_panel_info(const sgtk_graph* g, uint64_t info[8]) {
   return guard([&] {
     check_graph(g);
     const auto& p = *g->panels;
-    const uint64_t v[6] = {p.P, p.n_chunks, p.n_dent, p.n_sparse, p.max_chunk_entries,
-                           p.n_chunks * 32};
+    const uint64_t v[8] = {p.P, p.n_chunks, p.n_dent, p.n_sparse, p.max_chunk_entries,
+                           p.n_chunks * 32, p.n_long, p.n_segs};
     std::memcpy(info, v, sizeof v);
   });
+}
+
+int sgtk_debug_set(int mode) {
+  return guard([&] { sgtkcu::panel_debug_set(mode); });
 }
 
 int sgtk_panel_download(const sgtk_graph* g, uint32_t* chunk_ptr, uint32_t* dense_cols,

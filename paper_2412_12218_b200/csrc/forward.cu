@@ -123,7 +123,8 @@ uint64_t agnn_workspace_panel(const sgtk_graph* g, uint64_t d) {
   if (!g->panels || d > 64) return 0;
   const uint64_t ldq = d <= 32 ? 32 : 64;
   const auto& pn = *g->panels;
-  return 10 * align256(g->n_cols * ldq * 4) + 2 * align256(g->n_rows * ld4(d) * 4) +
+  return 10 * align256(g->n_cols * ldq * 4) + 2 * align256(g->n_cols * 4) +
+         align256(g->n_cols * 4) + 2 * align256(g->n_rows * ld4(d) * 4) +
          align256(g->n_rows * ldq * 4) + align256(g->n_rows * 4) +
          align256(std::max<uint64_t>(pn.n_segs, 1) * ldq * 4) +
          align256(std::max<uint64_t>(pn.n_segs, 1) * 4) + align256(16 * 4);
@@ -150,6 +151,8 @@ void agnn_forward_panel(const sgtk_graph* g, const float* x, uint64_t ldx, uint6
   float* set[2][5];
   for (int a = 0; a < 2; ++a)
     for (int b = 0; b < 5; ++b) set[a][b] = take(NC * ldq * 4);  // z, zq, zq1, hq, hq1
+  float* norm[2] = {take(NC * 4), take(NC * 4)};
+  float* inv = take(NC * 4);
   float* buf[2] = {take(N * ldb * 4), take(N * ldb * 4)};
   float* opart = take(N * ldq * 4);
   float* lpart = take(N * 4);
@@ -162,10 +165,9 @@ void agnn_forward_panel(const sgtk_graph* g, const float* x, uint64_t ldx, uint6
     CU(cudaMemsetAsync(set[0][0], 0, reinterpret_cast<char*>(set[1][4]) - reinterpret_cast<char*>(set[0][0]) +
                                          NC * ldq * 4, s));
   // layer 0 input: z = l2norm(x), operand copies
-  l2norm_launch(x, NC, d, ldx, set[0][0], ldq, nullptr, zeros, s);
-  agnn_prep_launch(set[0][0], x, ldx, NC, d, ldq, prec, set[0][1], set[0][2], set[0][3], set[0][4], s);
-  const float* h = x;
-  uint64_t ldh = ldx;
+  l2norm_launch(x, NC, d, ldx, set[0][0], ldq, inv, zeros, s);
+  agnn_prep_launch(set[0][0], x, ldx, NC, d, ldq, prec, set[0][1], set[0][2], set[0][3], set[0][4],
+                   inv, norm[0], s);
   for (uint32_t l = 0; l < L; ++l) {
     const bool last = l + 1 == L;
     float** cur = set[l & 1];
@@ -181,11 +183,10 @@ void agnn_forward_panel(const sgtk_graph* g, const float* x, uint64_t ldx, uint6
       nx.zq1 = nxt[2];
       nx.hq = nxt[3];
       nx.hq1 = nxt[4];
+      nx.norm = norm[(l + 1) & 1];
     }
-    agnn_panel_layer(g, cur[0], cur[1], cur[2], cur[3], cur[4], ldq, h, ldh, d, betas[l], prec,
+    agnn_panel_layer(g, cur[0], cur[1], cur[2], cur[3], cur[4], ldq, norm[l & 1], d, betas[l], prec,
                      opart, lpart, seg_o, seg_l, nx, s);
-    h = nx.out;
-    ldh = nx.ldo;
   }
   if (zero_rows_host) {
     CU(cudaMemcpyAsync(zero_rows_host, zeros, 8, cudaMemcpyDeviceToHost, s));

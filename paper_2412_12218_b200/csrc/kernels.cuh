@@ -52,18 +52,21 @@ struct AgnnNext {
   float* zq1;         //   lo planes (FP32)
   float* hq;
   float* hq1;
+  float* norm;        // next layer |h| per row
   uint64_t ldq;
   unsigned long long* zeros;
 };
 bool agnn_panel_supported(const sgtk_graph* g, uint64_t d, float beta);
 void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, const float* zq1,
-                      const float* hq, const float* hq1, uint64_t ldq, const float* h, uint64_t ldh,
+                      const float* hq, const float* hq1, uint64_t ldq, const float* norm,
                       uint64_t d, float beta, int prec, float* opart, float* lpart, float* seg_o,
                       float* seg_l, const AgnnNext& nx, cudaStream_t s);
 void agnn_prep_launch(const float* z, const float* h, uint64_t ldh, uint64_t rows, uint64_t d,
                       uint64_t ldq, int prec, float* zq, float* zq1, float* hq, float* hq1,
-                      cudaStream_t s);
+                      const float* inv, float* norm, cudaStream_t s);
 PanelView panel_view(const sgtk_graph* g);
+void panel_debug_set(int mode);
+int panel_debug_mode();
 bool panel_enabled();
 
 // Host-side split plan (make_split_plan, tile_exec.cpp:150-161).

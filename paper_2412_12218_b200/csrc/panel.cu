@@ -38,6 +38,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -782,12 +783,15 @@ bool launch_dense(const PanelView& v, uint64_t P, uint32_t max_entries, const fl
 
 // SGTK_PANEL_DEBUG=1: tensor-core part only, =2: CUDA-core part only
 // (timing experiments; results are then partial sums)
+std::atomic<int> g_panel_debug{-1};
 int panel_debug() {
-  static const int dbg = [] {
+  int v = g_panel_debug.load(std::memory_order_relaxed);
+  if (v < 0) {
     const char* e = std::getenv("SGTK_PANEL_DEBUG");
-    return e ? std::atoi(e) : 0;
-  }();
-  return dbg;
+    v = e ? std::atoi(e) : 0;
+    g_panel_debug.store(v, std::memory_order_relaxed);
+  }
+  return v;
 }
 
 void launch_sparse(const Panels& pn, const uint2* sent, const float* x, uint64_t ldx, uint64_t d,
@@ -952,6 +956,9 @@ void build_panels(sgtk_graph& g, cudaStream_t s) {
   CU(cudaStreamSynchronize(s));
   g.panels = pn;
 }
+
+void panel_debug_set(int mode) { g_panel_debug.store(mode, std::memory_order_relaxed); }
+int panel_debug_mode() { return panel_debug(); }
 
 PanelView panel_view(const sgtk_graph* g) {
   const Panels& pn = *g->panels;

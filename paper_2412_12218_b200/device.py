@@ -156,10 +156,11 @@ class DeviceGraph:
 
     def panel_info(self) -> dict:
         """128-row panel format sizes (sgtk_panel_info)."""
-        a = np.zeros(6, np.uint64)
+        a = np.zeros(8, np.uint64)
         check(lib().sgtk_panel_info(self._h, a.ctypes.data))
         return dict(zip(("panels", "dense_chunks", "dense_entries", "sparse_edges",
-                         "max_chunk_entries", "dense_columns"), (int(v) for v in a)))
+                         "max_chunk_entries", "dense_columns", "long_rows", "segments"),
+                        (int(v) for v in a)))
 
     def panel_arrays(self) -> dict:
         i = self.panel_info()

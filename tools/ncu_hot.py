@@ -12,7 +12,8 @@ for row in r[1:]:
     d = dict(zip(h, row))
     if d.get("Metric Name") in want:
         print(f"{d['Kernel Name'][:40]:40s} {d['Metric Name']:32s} {d['Metric Value']} {d['Metric Unit']}")
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
+kf = sys.argv[3:] and ["-k", "regex:" + sys.argv[3]] or []
+out = subprocess.run(["ncu", "-i", rep] + kf + ["--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 h = rows[1]; data = rows[2:]
 iS = h.index("Warp Stall Sampling (All Samples)"); iSrc = h.index("Source")
