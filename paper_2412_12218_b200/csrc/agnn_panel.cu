@@ -29,7 +29,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 #include <mutex>
 
 #include "kernels.cuh"
@@ -81,8 +83,12 @@ __global__ void __launch_bounds__(kAgnnThreads, 1)
 agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const float* __restrict__ z,
                   const float* __restrict__ z1, const float* __restrict__ h,
                   const float* __restrict__ h1, uint64_t ld, uint64_t d, uint64_t row_offset,
-                  float beta, float* __restrict__ opart, float* __restrict__ lpart) {
+                  float beta, float* __restrict__ opart, float* __restrict__ lpart,
+                  long long* __restrict__ trace) {
   using C = AgnnCfg<DC, PREC>;
+  auto mark = [&](uint32_t c, int ev) {
+    if (trace && blockIdx.x < 4 && c < 256) trace[((uint64_t(blockIdx.x) * 256 + c) * 8) + ev] = clock64();
+  };
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bfull = reinterpret_cast<uint64_t*>(smem);  // [NB] gathers landed
@@ -165,6 +171,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       mbar_wait(bfull + ds, dph);  // row masks of the chunk
       const uint32_t mask = ld_shared_u32(smem_u32(bs + ds * C::SLOT) + (C::PZ + C::PH) * C::T_BYTES + r * 4);
       mbar_wait(sfull + sb, sph);
+      if (warp == 0 && lane == 0) mark(c, 1);
       tc_fence_after();
       uint32_t sv[32];
       tmem_ld16(tmem + ((warp * 32u) << 16) + s_col + sb * 32, *reinterpret_cast<uint32_t(*)[16]>(sv));
@@ -172,14 +179,16 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
                 *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
       tmem_ld_wait();
       tc_fence_before();
-      float pr[32];
+      float pr[32], lq[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const float e = exp2f(fmaf(__uint_as_float(sv[j]), bl2, -off));
-        pr[j] = (mask >> j) & 1u ? e : 0.0f;
-        if constexpr (!C::F32) pr[j] = tf32_rne(pr[j]);
-        l += pr[j];
+        const float e = ex2_approx(fmaf(__uint_as_float(sv[j]), bl2, -off));
+        pr[j] = (mask & (1u << j)) ? e : 0.0f;
+        if constexpr (!C::F32) pr[j] = __uint_as_float(tf32_op(pr[j]));  // finite, >= 0
+        lq[j & 3] += pr[j];
       }
+      l += (lq[0] + lq[1]) + (lq[2] + lq[3]);
+      if (warp == 0 && lane == 0) mark(c, 5);
       mbar_wait(pempty + pslot, pph ^ 1u);  // PV(c - NP) done with this P slot
       const uint32_t pt = pb + pslot * C::PP * C::P_BYTES;
 #pragma unroll
@@ -198,6 +207,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       }
       fence_async_smem();
       __syncwarp();
+      if (warp == 0 && lane == 0) mark(c, 2);
       if (lane == 0) mbar_arrive(pfull + pslot);
     }
     lbuf[r] = l;
@@ -263,6 +273,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
           }
         }
         umma_commit(sfull + (c & 1u));
+        mark(c, 0);
       };
       issue_s(0);
       for (uint32_t c = 0; c < nch; ++c) {
@@ -289,6 +300,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
             umma_tf32(dt, p0, h0, id_o, acc);
           }
         }
+        mark(c, 3);
         umma_commit(pempty + pslot);
         umma_commit(bempty + ds);
         if ((c % C::FOLD) == C::FOLD - 1 || c + 1 == nch) umma_commit(accfull + buf);
@@ -303,6 +315,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
     for (uint32_t c = par; c < nch; c += 2) {
       const uint32_t ds = c % C::NB;
       mbar_wait(bempty + ds, ((c / C::NB) & 1u) ^ 1u);
+      if (lane == 0) mark(c, 4);
       const uint32_t col = pv.dcols[uint64_t(c0 + c) * kChunkCols + lane];
       const uint32_t zt = smem_u32(bs + ds * C::SLOT);
       const uint32_t ht = zt + C::PZ * C::T_BYTES;
@@ -401,13 +414,14 @@ __device__ __forceinline__ void agnn_finalize(uint64_t r, const float (&o)[FPL],
 //     the aggregation needs no second gather);
 //   lane = feature: O[f] += coef_e * T[e][f] over the batch, e ascending.
 // Row sums l: per-lane partials, reduced by a fixed shuffle tree per item.
-template <int FPL, int PREC>
+template <int FPL, int PREC, bool SPLIT>
 __global__ void __launch_bounds__(FPL == 1 ? 256 : 128)
 agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2* __restrict__ sent,
                  const float* __restrict__ z, uint64_t ld, const float* __restrict__ norm,
                  uint64_t d, uint64_t row_offset, float beta, const float* __restrict__ opart,
                  const float* __restrict__ lpart, float* __restrict__ seg_o,
-                 float* __restrict__ seg_l, AgnnNext nx) {
+                 float* __restrict__ seg_l, float* __restrict__ osp, float* __restrict__ lsp,
+                 AgnnNext nx) {
   constexpr int DC = 32 * FPL;
   constexpr int TS = DC + 4;  // smem tile row stride (floats): 16-byte rows, spread banks
   __shared__ __align__(16) float tile[FPL == 1 ? 8 : 4][32 * TS];
@@ -438,8 +452,8 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
     }
     float o[FPL], lpp = 0.0f;
 #pragma unroll
-    for (int i = 0; i < FPL; ++i) o[i] = (direct && i < fv) ? opart[r * DC + f + i] : 0.0f;
-    const float l0 = direct ? lpart[r] : 0.0f;
+    for (int i = 0; i < FPL; ++i) o[i] = (!SPLIT && direct && i < fv) ? opart[r * DC + f + i] : 0.0f;
+    const float l0 = (!SPLIT && direct) ? lpart[r] : 0.0f;
     uint32_t col = c_first;
     for (uint32_t e = w.y; e < w.z; e += 32) {
       const uint32_t cnt = min(32u, w.z - e);
@@ -473,8 +487,8 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
           s = fmaf(zr[4 * k + 3], v.w, s);
         }
         if constexpr (PREC == SGTK_TF32) s = tf32_rne(s);  // sddmm TF32 rounds the dot (tile_exec.cpp:386)
-        float pe = exp2f(fmaf(s, bl2, -off));
-        if constexpr (PREC == SGTK_TF32) pe = tf32_rne(pe);
+        float pe = ex2_approx(fmaf(s, bl2, -off));
+        if constexpr (PREC == SGTK_TF32) pe = __uint_as_float(tf32_op(pe));
         lpp += pe;
         T[lane * TS + DC] = pe * __ldg(norm + col);
       }
@@ -491,7 +505,12 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
 #pragma unroll
     for (int o2 = 16; o2 > 0; o2 >>= 1) lpp += __shfl_xor_sync(0xFFFFFFFFu, lpp, o2);
     const float l = l0 + lpp;
-    if (direct) {
+    if (direct && SPLIT) {  // sparse partial; agnn_final_kernel combines
+#pragma unroll
+      for (int i = 0; i < FPL; ++i)
+        if (i < fv) osp[r * DC + f + i] = o[i];
+      if (lane == 0) lsp[r] = l;
+    } else if (direct) {
       agnn_finalize<FPL, PREC>(r, o, l, lane, fv, nx, nz);
     } else {
 #pragma unroll
@@ -499,6 +518,31 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
         if (i < fv) seg_o[uint64_t(w.w) * DC + f + i] = o[i];
       if (lane == 0) seg_l[w.w] = l;
     }
+  }
+  if (nx.zeros && lane == 0 && nz) atomicAdd(nx.zeros, nz);
+}
+
+// Concurrent mode: (dense + sparse) partials of the non-hub rows, finalised.
+template <int FPL, int PREC>
+__global__ void agnn_final_kernel(const uint4* __restrict__ items, uint64_t n_items, uint64_t d,
+                                  const float* __restrict__ opart, const float* __restrict__ lpart,
+                                  const float* __restrict__ osp, const float* __restrict__ lsp,
+                                  AgnnNext nx) {
+  constexpr int DC = 32 * FPL;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t f = uint64_t(lane) * FPL;
+  const int fv = f >= d ? 0 : (d - f >= uint64_t(FPL) ? FPL : int(d - f));
+  unsigned long long nz = 0;
+  for (uint64_t it = warp; it < n_items; it += nw) {
+    const uint4 w = items[it];
+    if (w.w != 0xFFFFFFFFu) continue;  // hub segment: agnn_long_rows_kernel
+    const uint64_t r = w.x;
+    float o[FPL];
+#pragma unroll
+    for (int i = 0; i < FPL; ++i) o[i] = i < fv ? opart[r * DC + f + i] + osp[r * DC + f + i] : 0.0f;
+    agnn_finalize<FPL, PREC>(r, o, lpart[r] + lsp[r], lane, fv, nx, nz);
   }
   if (nx.zeros && lane == 0 && nz) atomicAdd(nx.zeros, nz);
 }
@@ -576,24 +620,72 @@ void launch_agnn_dense(const PanelView& v, uint64_t P, const float* zraw, const 
     cudaFuncSetAttribute(agnn_dense_kernel<DC, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(C::SMEM));
   });
-  agnn_dense_kernel<DC, PREC><<<unsigned(P), kAgnnThreads, C::SMEM, s>>>(
-      v, zraw, zq, zq1, hq, hq1, ldq, d, row_offset, beta, opart, lpart);
+  // SGTK_AGNN_DENSE_SMEM (bytes): pad the dense kernel's shared memory, e.g.
+  // to hold one CTA per SM and leave room for the concurrent CUDA-core kernel
+  static const uint32_t pad = [] {
+    const char* e = std::getenv("SGTK_AGNN_DENSE_SMEM");
+    return e ? uint32_t(std::atoi(e)) : 0u;
+  }();
+  const uint32_t smem = std::max<uint32_t>(C::SMEM, std::min<uint32_t>(pad, 227u * 1024u));
+  static std::once_flag once2;
+  std::call_once(once2, [smem] {
+    cudaFuncSetAttribute(agnn_dense_kernel<DC, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(227u * 1024u));
+  });
+  static long long* trace = [] {
+    long long* t = nullptr;
+    if (std::getenv("SGTK_PANEL_TRACE")) {
+      cudaMalloc(&t, 4 * 256 * 8 * 8);
+      cudaMemset(t, 0, 4 * 256 * 8 * 8);
+    }
+    return t;
+  }();
+  agnn_dense_kernel<DC, PREC><<<unsigned(P), kAgnnThreads, smem, s>>>(
+      v, zraw, zq, zq1, hq, hq1, ldq, d, row_offset, beta, opart, lpart, trace);
+  if (trace) {
+    std::vector<long long> hb(4 * 256 * 8);
+    cudaMemcpy(hb.data(), trace, hb.size() * 8, cudaMemcpyDeviceToHost);
+    if (FILE* f = std::fopen(std::getenv("SGTK_PANEL_TRACE"), "wb")) {
+      std::fwrite(hb.data(), 8, hb.size(), f);
+      std::fclose(f);
+    }
+  }
   CU_LAUNCH("agnn_dense_kernel");
 }
 
 template <int FPL, int PREC>
 void launch_agnn_rows(const Panels& pn, const float* z, uint64_t ld, const float* norm, uint64_t d,
                       uint64_t row_offset, float beta, const float* opart, const float* lpart,
-                      float* seg_o, float* seg_l, const AgnnNext& nx, cudaStream_t s) {
+                      float* seg_o, float* seg_l, float* osp, float* lsp, const AgnnNext& nx,
+                      cudaStream_t s, cudaStream_t s_final) {
+  constexpr unsigned bs = FPL == 1 ? 256 : 128;
   if (pn.n_aitems) {
-    constexpr unsigned bs = FPL == 1 ? 256 : 128;
-    agnn_rows_kernel<FPL, PREC><<<blocks_for(pn.n_aitems * 32, bs), bs, 0, s>>>(
-        pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), z, ld, norm, d, row_offset, beta,
-        opart, lpart, seg_o, seg_l, nx);
+    if (osp)
+      agnn_rows_kernel<FPL, PREC, true><<<blocks_for(pn.n_aitems * 32, bs), bs, 0, s>>>(
+          pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), z, ld, norm, d, row_offset, beta,
+          opart, lpart, seg_o, seg_l, osp, lsp, nx);
+    else
+      agnn_rows_kernel<FPL, PREC, false><<<blocks_for(pn.n_aitems * 32, bs), bs, 0, s>>>(
+          pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), z, ld, norm, d, row_offset, beta,
+          opart, lpart, seg_o, seg_l, osp, lsp, nx);
     CU_LAUNCH("agnn_rows_kernel");
   }
+  if (osp) {  // concurrent mode: join, then finalise on the main stream
+    static cudaEvent_t ev = [] {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      return e;
+    }();
+    CU(cudaEventRecord(ev, s));
+    CU(cudaStreamWaitEvent(s_final, ev, 0));
+    if (pn.n_aitems) {
+      agnn_final_kernel<FPL, PREC><<<blocks_for(pn.n_aitems * 32), 256, 0, s_final>>>(
+          pn.aitems->as<uint4>(), pn.n_aitems, d, opart, lpart, osp, lsp, nx);
+      CU_LAUNCH("agnn_final_kernel");
+    }
+  }
   if (pn.n_long) {
-    agnn_long_rows_kernel<FPL, PREC><<<blocks_for(pn.n_long * 32), 256, 0, s>>>(
+    agnn_long_rows_kernel<FPL, PREC><<<blocks_for(pn.n_long * 32), 256, 0, s_final>>>(
         pn.lrows->as<uint4>(), pn.n_long, d, opart, lpart, seg_o, seg_l, nx);
     CU_LAUNCH("agnn_long_rows_kernel");
   }
@@ -611,49 +703,66 @@ bool agnn_panel_supported(const sgtk_graph* g, uint64_t d, float beta) {
 // FP32: hi / lo planes), stride ldq; h: the raw input rows (stride ldh).
 // Writes nx.out (n_rows x d) and, when nx.z is set, the next layer's z and
 // operand copies (which must not alias the inputs).
+// Concurrent mode (default; SGTK_AGNN_SERIAL=1 turns it off): the dense
+// tensor-core kernel runs on the caller's stream while the CUDA-core kernel
+// runs on an auxiliary stream (the paper's two independent resources); the
+// finalisation joins them.  Serial mode: dense, then rows (which finalises).
 void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, const float* zq1,
                       const float* hq, const float* hq1, uint64_t ldq, const float* norm,
                       uint64_t d, float beta, int prec, float* opart, float* lpart, float* seg_o,
-                      float* seg_l, const AgnnNext& nx, cudaStream_t s) {
+                      float* seg_l, float* osp, float* lsp, const AgnnNext& nx, cudaStream_t s) {
   const Panels& pn = *g->panels;
   PanelView v = panel_view(g);
   const uint64_t ro = g->row_offset;
   const int dbg = panel_debug_mode();  // 1: dense part only, 2: sparse part only (timing)
+  static const bool serial = std::getenv("SGTK_AGNN_SERIAL") != nullptr;
+  auto dense = [&](cudaStream_t st) {
+    if (prec == SGTK_FP32) {
+      if (ldq == 32) launch_agnn_dense<32, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, st);
+      else launch_agnn_dense<64, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, st);
+    } else {
+      if (ldq == 32) launch_agnn_dense<32, SGTK_TF32>(v, pn.P, z, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, st);
+      else launch_agnn_dense<64, SGTK_TF32>(v, pn.P, z, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, st);
+    }
+  };
+  auto rows = [&](cudaStream_t st, float* o_sp, float* l_sp, cudaStream_t st_final) {
+    if (prec == SGTK_FP32) {
+      if (ldq == 32) launch_agnn_rows<1, SGTK_FP32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
+      else launch_agnn_rows<2, SGTK_FP32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
+    } else {
+      if (ldq == 32) launch_agnn_rows<1, SGTK_TF32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
+      else launch_agnn_rows<2, SGTK_TF32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
+    }
+  };
+  if (dbg == 1) {
+    dense(s);
+    return;
+  }
   if (dbg == 2) {
     CU(cudaMemsetAsync(opart, 0, g->n_rows * ldq * 4, s));
     CU(cudaMemsetAsync(lpart, 0, g->n_rows * 4, s));
-  }
-  if (dbg == 1) {
-    if (prec == SGTK_FP32) {
-      if (ldq == 32) launch_agnn_dense<32, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, s);
-      else launch_agnn_dense<64, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, s);
-    } else {
-      if (ldq == 32) launch_agnn_dense<32, SGTK_TF32>(v, pn.P, z, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, s);
-      else launch_agnn_dense<64, SGTK_TF32>(v, pn.P, z, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, s);
-    }
+    rows(s, nullptr, nullptr, s);
     return;
   }
-  if (dbg == 2) {
-    if (prec == SGTK_FP32) {
-      if (ldq == 32) launch_agnn_rows<1, SGTK_FP32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
-      else launch_agnn_rows<2, SGTK_FP32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
-    } else {
-      if (ldq == 32) launch_agnn_rows<1, SGTK_TF32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
-      else launch_agnn_rows<2, SGTK_TF32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
-    }
+  if (serial || !osp) {
+    dense(s);
+    rows(s, nullptr, nullptr, s);
     return;
   }
-  if (prec == SGTK_FP32) {
-    if (ldq == 32) launch_agnn_dense<32, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, s);
-    else launch_agnn_dense<64, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, s);
-    if (ldq == 32) launch_agnn_rows<1, SGTK_FP32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
-    else launch_agnn_rows<2, SGTK_FP32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
-  } else {
-    if (ldq == 32) launch_agnn_dense<32, SGTK_TF32>(v, pn.P, z, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, s);
-    else launch_agnn_dense<64, SGTK_TF32>(v, pn.P, z, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, s);
-    if (ldq == 32) launch_agnn_rows<1, SGTK_TF32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
-    else launch_agnn_rows<2, SGTK_TF32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, nx, s);
-  }
+  static cudaStream_t aux = [] {
+    cudaStream_t a;
+    cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking);
+    return a;
+  }();
+  static cudaEvent_t ready = [] {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    return e;
+  }();
+  CU(cudaEventRecord(ready, s));  // inputs of the layer are on s
+  CU(cudaStreamWaitEvent(aux, ready, 0));
+  dense(s);
+  rows(aux, osp, lsp, s);  // sparse partials on aux; final + hub rows join on s
 }
 
 void agnn_prep_launch(const float* z, const float* h, uint64_t ldh, uint64_t rows, uint64_t d,

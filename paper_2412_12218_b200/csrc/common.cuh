@@ -147,6 +147,13 @@ __device__ __forceinline__ uint32_t tf32_op(float v) {
   return r;
 }
 
+// 2^x on the SFU (ex2.approx.ftz: ~2 ulp); softmax weights only.
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Structure operand per precision: TF32 -> (rne, -), FP32 -> split2.
 template <int PREC>
 __device__ __forceinline__ void split_s(float x, uint32_t& p0, uint32_t& p1) {

@@ -125,7 +125,7 @@ uint64_t agnn_workspace_panel(const sgtk_graph* g, uint64_t d) {
   const auto& pn = *g->panels;
   return 10 * align256(g->n_cols * ldq * 4) + 2 * align256(g->n_cols * 4) +
          align256(g->n_cols * 4) + 2 * align256(g->n_rows * ld4(d) * 4) +
-         align256(g->n_rows * ldq * 4) + align256(g->n_rows * 4) +
+         2 * align256(g->n_rows * ldq * 4) + 2 * align256(g->n_rows * 4) +
          align256(std::max<uint64_t>(pn.n_segs, 1) * ldq * 4) +
          align256(std::max<uint64_t>(pn.n_segs, 1) * 4) + align256(16 * 4);
 }
@@ -156,6 +156,8 @@ void agnn_forward_panel(const sgtk_graph* g, const float* x, uint64_t ldx, uint6
   float* buf[2] = {take(N * ldb * 4), take(N * ldb * 4)};
   float* opart = take(N * ldq * 4);
   float* lpart = take(N * 4);
+  float* osp = take(N * ldq * 4);
+  float* lsp = take(N * 4);
   float* seg_o = take(std::max<uint64_t>(pn.n_segs, 1) * ldq * 4);
   float* seg_l = take(std::max<uint64_t>(pn.n_segs, 1) * 4);
   uint64_t* zeros = reinterpret_cast<uint64_t*>(p);
@@ -186,7 +188,7 @@ void agnn_forward_panel(const sgtk_graph* g, const float* x, uint64_t ldx, uint6
       nx.norm = norm[(l + 1) & 1];
     }
     agnn_panel_layer(g, cur[0], cur[1], cur[2], cur[3], cur[4], ldq, norm[l & 1], d, betas[l], prec,
-                     opart, lpart, seg_o, seg_l, nx, s);
+                     opart, lpart, seg_o, seg_l, osp, lsp, nx, s);
   }
   if (zero_rows_host) {
     CU(cudaMemcpyAsync(zero_rows_host, zeros, 8, cudaMemcpyDeviceToHost, s));

@@ -60,7 +60,7 @@ bool agnn_panel_supported(const sgtk_graph* g, uint64_t d, float beta);
 void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, const float* zq1,
                       const float* hq, const float* hq1, uint64_t ldq, const float* norm,
                       uint64_t d, float beta, int prec, float* opart, float* lpart, float* seg_o,
-                      float* seg_l, const AgnnNext& nx, cudaStream_t s);
+                      float* seg_l, float* osp, float* lsp, const AgnnNext& nx, cudaStream_t s);
 void agnn_prep_launch(const float* z, const float* h, uint64_t ldh, uint64_t rows, uint64_t d,
                       uint64_t ldq, int prec, float* zq, float* zq1, float* hq, float* hq1,
                       const float* inv, float* norm, cudaStream_t s);
