@@ -23,6 +23,7 @@ sddmm_hybrid on reblock(t,16), edge_softmax, spmm_hybrid; gnn.cpp:107-116).
 from __future__ import annotations
 
 import argparse
+import csv
 import ctypes as C
 import json
 import os
@@ -417,6 +418,7 @@ def run_b200(args, wl):
 
     pk, pk_src = peaks()
     if roof:
+        roof["traffic"] = profiled_traffic(roof["kernel"])
         roof["peak"] = pk["hbm_gbs"]
         roof["frac"] = round(roof["achieved"] / pk["hbm_gbs"], 4)
         roof["peak_source"] = f"MEASURED_PEAKS.json hbm_gbs ({pk_src})"
@@ -452,6 +454,34 @@ def run_b200(args, wl):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def profiled_traffic(kernel_field):
+    """DRAM bytes (read + write) per launch of the roofline kernel(s), from the
+    committed ncu launch list of this code (profiles/*_launches.csv, written by
+    tools/profile_round.sh + tools/ncu_summary.py); None if not profiled."""
+    import glob
+
+    names = [k.strip() for k in kernel_field.split("(")[-1].rstrip(")").split("+")] \
+        if "(" in kernel_field else [kernel_field]
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_launches.csv")), key=os.path.getmtime)
+    for path in reversed(files):
+        try:
+            with open(path, newline="") as f:
+                rows = list(csv.reader(f))[1:]
+        except OSError:
+            continue
+        if not rows or len(rows[0]) < 6:
+            continue
+        tot, found = 0.0, 0
+        for nm in names:
+            hit = [r for r in rows if nm.strip() in r[0]]
+            if hit:
+                tot += float(hit[0][5])
+                found += 1
+        if found == len(names):
+            return {"bytes": int(tot), "source": os.path.relpath(path, ROOT)}
+    return None
 
 
 def dg_has_splits(dg, tile_w):
@@ -541,7 +571,7 @@ def kernel_breakdown(args, wl, dg, g, h, D, prec, mode, flush, stream, gcn_layer
         B_fused = 8 * (N + 1) + 4 * E + 4 * N + 2 * s_ * N * d
         B_spmm = 8 * (N + 1) + 4 * E + 4 * E + s_ * N * d + 4 * N * d
         if mode == 2:
-            name, B, t = "agnn_panel_layer (agnn_dense_kernel + agnn_rows_kernel)", B_fused, \
+            name, B, t = "agnn_panel_layer (agnn_dense_kernel + agnn_rows_kernel + agnn_final_kernel)", B_fused, \
                 res["agnn_panel_layer"]
             formula = "8(N+1) + 4E + 4N + 2*s*N*d (SURVEY §8d fused AGNN lower bound, s=4)"
             extra["roofline_unfused_formula"] = {
@@ -566,6 +596,7 @@ def kernel_breakdown(args, wl, dg, g, h, D, prec, mode, flush, stream, gcn_layer
         hw.copy_(D.gemm(x, gcn_layers[0][0], precision=prec))
         res["spmm"] = ev_time(lambda: dg.spmm(hw, precision=prec, out=outb))
         t = res["spmm"]
+        name = "spmm (spmm_panel_kernel + sparse_rows_kernel)"
         B = 8 * (N + 1) + 4 * E + 4 * E + 4 * N * dd + 4 * N * dd
         formula = "8(N+1) + 4E + 4E*[w] + s*N*d + 4*N*d (SURVEY §8d B_spmm, s=4, w=1)"
     res = {k: round(v, 4) for k, v in res.items()}

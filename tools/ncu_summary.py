@@ -5,7 +5,8 @@ import io
 import subprocess
 import sys
 
-tag, rep, launches = sys.argv[1], sys.argv[2], sys.argv[3]
+tag, rep = sys.argv[1], sys.argv[2]
+launches = sys.argv[3] if len(sys.argv) > 3 else None
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units = rows[0], rows[1]
@@ -37,12 +38,14 @@ for r in rows[2:]:
             out.append(f"| {k} | {r[hdr.index(k)]} | {units[hdr.index(k)]} |")
     out.append("")
 open(f"profiles/{tag}_ncu_full.md", "w").write("\n".join(out) + "\n")
+if not launches:
+    sys.exit(0)
 rows = list(csv.reader(open(launches)))
 i = [k for k, r in enumerate(rows) if r and r[0] == "ID"][0]
 hdr = rows[i]
-iN, iV = hdr.index("Kernel Name"), hdr.index("Metric Value")
-agg = collections.defaultdict(lambda: [0, 0.0])
-for r in rows[i + 2:]:
+iN, iV, iM = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
+agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+for r in rows[i + 1:]:
     if len(r) <= iV:
         continue
     nm = r[iN].split("(")[0].replace("void ", "").strip()
@@ -50,11 +53,15 @@ for r in rows[i + 2:]:
         v = float(r[iV].replace(",", ""))
     except ValueError:
         continue
-    agg[nm][0] += 1
-    agg[nm][1] += v
+    if r[iM] == "gpu__time_duration.sum":
+        agg[nm][0] += 1
+        agg[nm][1] += v
+    elif r[iM].startswith("dram__bytes"):
+        agg[nm][2] += v
 tot = sum(v[1] for v in agg.values())
-with open(f"profiles/{tag}_launches.csv", "w") as f:
-    f.write("kernel,launches,total_ns,share_pct\n")
-    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
-        f.write(f"{k},{n},{t:.0f},{t / tot * 100:.2f}\n")
-print(open(f"profiles/{tag}_launches.csv").read()[:1500])
+with open(f"profiles/{tag}_launches.csv", "w", newline="") as f:
+    w = csv.writer(f)
+    w.writerow(["kernel", "launches", "total_ns", "avg_ns", "share_pct", "dram_bytes_per_launch"])
+    for k, (n, t, b) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        w.writerow([k, n, f"{t:.0f}", f"{t / max(n, 1):.0f}", f"{t / tot * 100:.2f}", f"{b / max(n, 1):.0f}"])
+print(open(f"profiles/{tag}_launches.csv").read()[:2500])
