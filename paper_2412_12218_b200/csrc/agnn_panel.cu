@@ -55,17 +55,26 @@ struct AgnnCfg {
   static constexpr uint32_t Q_BYTES = kPanelRows * DC * 4;  // K-major, DC/32 K-blocks of 16 KB
   static constexpr uint32_t T_BYTES = kChunkCols * DC * 4;  // one 32-row tile
   static constexpr uint32_t M_BYTES = kPanelRows * 4;       // row masks
-  static constexpr uint32_t SLOT = ((PZ + PH) * T_BYTES + M_BYTES + 1023) / 1024 * 1024;
   static constexpr uint32_t P_BYTES = kPanelRows * kChunkCols * 4;  // 16 KB
-  static constexpr int NB = F32 ? (DC == 32 ? 4 : 2) : 6;  // gather ring
+  static constexpr int KB = DC / 32;                       // 128-byte K blocks of z
+  static constexpr int NB = F32 ? (DC == 32 ? 4 : 2) : 6;  // gather ring (even: S pairs)
   static constexpr int NP = 2;                             // P ring
-  static constexpr int NF = DC == 32 ? 6 : 3;              // O accumulators (256 TMEM cols: 2 CTAs/SM)
+  // TMEM: 2 S buffers x 64 columns (S of a chunk pair, N = 64 costs what
+  // N = 32 does), NF O accumulators x DC; 256 columns -> 2 CTAs per SM
+  static constexpr int NF = DC == 32 ? 4 : 2;
   static constexpr uint32_t TMEM_COLS = 256;
   static constexpr uint32_t FOLD = 4;
   static constexpr uint32_t Q_OFF = 1024;
-  static constexpr uint32_t B_OFF = Q_OFF + PQ * Q_BYTES;
-  static constexpr uint32_t P_OFF = B_OFF + NB * SLOT;
+  static constexpr uint32_t Z_OFF = Q_OFF + PQ * Q_BYTES;             // [PZ][KB][NB] x 4 KB
+  static constexpr uint32_t H_OFF = Z_OFF + PZ * KB * NB * 4096;      // [PH][NB] x T_BYTES
+  static constexpr uint32_t M_OFF = H_OFF + PH * NB * T_BYTES;        // [NB] x 512 B
+  static constexpr uint32_t P_OFF = (M_OFF + NB * M_BYTES + 1023) / 1024 * 1024;
   static constexpr uint32_t SMEM = P_OFF + NP * PP * P_BYTES + 1024;
+  static_assert(NB % 2 == 0, "S pairs need an even gather ring");
+  // S of a chunk pair needs both chunks' gathers while PV still lags: a ring
+  // of >= 4 slots; shallower rings compute S chunk by chunk (N = 32)
+  static constexpr bool PAIR = NB >= 4;
+  static constexpr uint32_t SG = PAIR ? 2 : 1;  // chunks per S group
   static_assert(SMEM <= 227u * 1024u, "agnn panel smem");
 };
 
@@ -92,17 +101,17 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bfull = reinterpret_cast<uint64_t*>(smem);  // [NB] gathers landed
-  uint64_t* bempty = bfull + C::NB;                     // [NB] PV(c) retired
-  uint64_t* sfull = bempty + C::NB;                     // [2]  S(c) in TMEM
+  uint64_t* bempty = bfull + C::NB;                     // [NB] PV(c) retired: slot + P(c) free
+  uint64_t* sfull = bempty + C::NB;                     // [2]  S of chunk pair in TMEM
   uint64_t* pfull = sfull + 2;                          // [NP] P(c) written
-  uint64_t* pempty = pfull + C::NP;                     // [NP] PV(c) retired
-  uint64_t* qfull = pempty + C::NP;                     // [1]  Q operand ready
+  uint64_t* qfull = pfull + C::NP;                      // [1]  Q operand ready
   uint64_t* accfull = qfull + 1;                        // [NF]
   uint64_t* accempty = accfull + C::NF;                 // [NF]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + C::NF);
   float* lbuf = reinterpret_cast<float*>(smem + 512);   // [128] row sums
   uint8_t* qs = smem + C::Q_OFF;
-  uint8_t* bs = smem + C::B_OFF;
+  const uint32_t zr_s = smem_u32(smem + C::Z_OFF), hr_s = smem_u32(smem + C::H_OFF);
+  const uint32_t mr_s = smem_u32(smem + C::M_OFF);
   uint8_t* ps = smem + C::P_OFF;
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -118,10 +127,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       mbar_init(bempty + i, 1);
     }
     for (int i = 0; i < 2; ++i) mbar_init(sfull + i, 1);
-    for (int i = 0; i < C::NP; ++i) {
-      mbar_init(pfull + i, 4);
-      mbar_init(pempty + i, 1);
-    }
+    for (int i = 0; i < C::NP; ++i) mbar_init(pfull + i, 4);
     mbar_init(qfull, 4);
     for (int i = 0; i < C::NF; ++i) {
       mbar_init(accfull + i, 1);
@@ -134,7 +140,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t s_col = 0, o_col = 64;  // TMEM columns: S[2] x 32, O[NF] x DC
+  const uint32_t s_col = 0, o_col = 128;  // TMEM columns: S[2] x 64, O[NF] x DC
 
   if (warp < 4) {
     // ------------------------------------------------------------ softmax
@@ -165,19 +171,22 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
     float l = 0.0f;
     const uint32_t pb = smem_u32(ps);
     for (uint32_t c = 0; c < nch; ++c) {
-      const uint32_t sb = c & 1u, sph = (c >> 1) & 1u;
+      const uint32_t sgi = c / C::SG;  // S group of the chunk
+      const uint32_t sb = sgi & 1u, sph = (sgi >> 1) & 1u, shalf = (c % C::SG) * 32;
       const uint32_t ds = c % C::NB, dph = (c / C::NB) & 1u;
-      const uint32_t pslot = c % C::NP, pph = (c / C::NP) & 1u;
+      const uint32_t pslot = c % C::NP;
       mbar_wait(bfull + ds, dph);  // row masks of the chunk
-      const uint32_t mask = ld_shared_u32(smem_u32(bs + ds * C::SLOT) + (C::PZ + C::PH) * C::T_BYTES + r * 4);
+      const uint32_t mask = ld_shared_u32(mr_s + ds * C::M_BYTES + r * 4);
+      if (warp == 0 && lane == 0) mark(c, 7);
       mbar_wait(sfull + sb, sph);
       if (warp == 0 && lane == 0) mark(c, 1);
       tc_fence_after();
       uint32_t sv[32];
-      tmem_ld16(tmem + ((warp * 32u) << 16) + s_col + sb * 32, *reinterpret_cast<uint32_t(*)[16]>(sv));
-      tmem_ld16(tmem + ((warp * 32u) << 16) + s_col + sb * 32 + 16,
+      tmem_ld16(tmem + ((warp * 32u) << 16) + s_col + sb * 64 + shalf, *reinterpret_cast<uint32_t(*)[16]>(sv));
+      tmem_ld16(tmem + ((warp * 32u) << 16) + s_col + sb * 64 + shalf + 16,
                 *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
       tmem_ld_wait();
+      if (warp == 0 && lane == 0) mark(c, 6);
       tc_fence_before();
       float pr[32], lq[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
@@ -189,7 +198,10 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       }
       l += (lq[0] + lq[1]) + (lq[2] + lq[3]);
       if (warp == 0 && lane == 0) mark(c, 5);
-      mbar_wait(pempty + pslot, pph ^ 1u);  // PV(c - NP) done with this P slot
+      if (c >= uint32_t(C::NP)) {  // PV(c - NP) done with this P slot
+        const uint32_t cp = c - C::NP;
+        mbar_wait(bempty + cp % C::NB, (cp / C::NB) & 1u);
+      }
       const uint32_t pt = pb + pslot * C::PP * C::P_BYTES;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -247,38 +259,43 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
   } else if (warp == 8) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0 && nch) {
-      constexpr uint32_t id_s = idesc_tf32(32, false);  // N = 32 chunk columns, B K-major
+      constexpr uint32_t id_s = idesc_tf32(32 * C::SG, false);  // N = a S group's columns, B K-major
       constexpr uint32_t id_o = idesc_tf32(DC, true);   // N = DC features, B MN-major
       const uint32_t qb = smem_u32(qs), pb = smem_u32(ps);
       mbar_wait(qfull, 0);
       tc_fence_after();
-      auto issue_s = [&](uint32_t c) {
-        const uint32_t ds = c % C::NB;
-        mbar_wait(bfull + ds, (c / C::NB) & 1u);
+      // S of chunk pair g (chunks 2g, 2g+1) as one N = 64 MMA chain: the z
+      // tiles of ring slots 2k and 2k+1 are adjacent rows of one K-major tile
+      auto issue_s = [&](uint32_t g) {
+        const uint32_t c = C::SG * g;
+        mbar_wait(bfull + c % C::NB, (c / C::NB) & 1u);
+        if (C::PAIR && c + 1 < nch) mbar_wait(bfull + (c + 1) % C::NB, ((c + 1) / C::NB) & 1u);
         fence_async_smem();  // cp.async (generic proxy) -> MMA (async proxy)
         tc_fence_after();
-        const uint32_t zt = smem_u32(bs + ds * C::SLOT);
-        const uint32_t dt = tmem + s_col + (c & 1u) * 32;
+        const uint32_t s0 = c % C::NB;
+        const uint32_t dt = tmem + s_col + (g & 1u) * 64;
 #pragma unroll
         for (uint32_t ks = 0; ks < DC / 8; ++ks) {
           const uint32_t ko = (ks >> 2) * 16384u + (ks & 3u) * 32u;  // Q: 128-row K blocks
-          const uint32_t kz = (ks >> 2) * 4096u + (ks & 3u) * 32u;   // z tile: 32-row K blocks
-          const uint64_t q0 = umma_desc(qb + ko), z0 = umma_desc(zt + kz);
+          const uint32_t kz = ((ks >> 2) * C::NB + s0) * 4096u + (ks & 3u) * 32u;
+          const uint64_t q0 = umma_desc(qb + ko), z0 = umma_desc(zr_s + kz);
           if constexpr (C::F32) {
-            umma_tf32(dt, q0, umma_desc(zt + C::T_BYTES + kz), id_s, ks ? 1u : 0u);
+            umma_tf32(dt, q0, umma_desc(zr_s + C::KB * C::NB * 4096u + kz), id_s, ks ? 1u : 0u);
             umma_tf32(dt, umma_desc(qb + C::Q_BYTES + ko), z0, id_s, 1u);
             umma_tf32(dt, q0, z0, id_s, 1u);
           } else {
             umma_tf32(dt, q0, z0, id_s, ks ? 1u : 0u);
           }
         }
-        umma_commit(sfull + (c & 1u));
+        umma_commit(sfull + (g & 1u));
         mark(c, 0);
       };
       issue_s(0);
       for (uint32_t c = 0; c < nch; ++c) {
-        // S(c+1) ahead of PV(c): its S buffer was released by pfull(c - 1)
-        if (c + 1 < nch) issue_s(c + 1);
+        // S of the next group, issued at the group's last chunk (before its
+        // PV): its S buffer held group g - 1, whose P was waited for at the
+        // previous iteration; its gathers only need PV(c + 2 - NB) retired
+        if ((c % C::SG) == C::SG - 1 && c + 1 < nch) issue_s(c / C::SG + 1);
         const uint32_t ds = c % C::NB, pslot = c % C::NP;
         const uint32_t g = c / C::FOLD, buf = g % C::NF;
         const bool first = (c % C::FOLD) == 0;
@@ -286,14 +303,14 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
         mbar_wait(pfull + pslot, (c / C::NP) & 1u);
         tc_fence_after();
         const uint32_t pt = pb + pslot * C::PP * C::P_BYTES;
-        const uint32_t ht = smem_u32(bs + ds * C::SLOT) + C::PZ * C::T_BYTES;
+        const uint32_t ht = hr_s + ds * C::T_BYTES;
         const uint32_t dt = tmem + o_col + buf * DC;
 #pragma unroll
         for (uint32_t ks = 0; ks < kChunkCols / 8; ++ks) {
           const uint32_t acc = (first && ks == 0) ? 0u : 1u;
           const uint64_t p0 = umma_desc(pt + ks * 32), h0 = desc_mn32(ht + ks * 1024, 4096, 512);
           if constexpr (C::F32) {
-            umma_tf32(dt, p0, desc_mn32(ht + C::T_BYTES + ks * 1024, 4096, 512), id_o, acc);
+            umma_tf32(dt, p0, desc_mn32(ht + C::NB * C::T_BYTES + ks * 1024, 4096, 512), id_o, acc);
             umma_tf32(dt, umma_desc(pt + C::P_BYTES + ks * 32), h0, id_o, 1u);
             umma_tf32(dt, p0, h0, id_o, 1u);
           } else {
@@ -301,8 +318,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
           }
         }
         mark(c, 3);
-        umma_commit(pempty + pslot);
-        umma_commit(bempty + ds);
+        umma_commit(bempty + ds);  // gather slot and P slot free
         if ((c % C::FOLD) == C::FOLD - 1 || c + 1 == nch) umma_commit(accfull + buf);
       }
     }
@@ -317,8 +333,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       mbar_wait(bempty + ds, ((c / C::NB) & 1u) ^ 1u);
       if (lane == 0) mark(c, 4);
       const uint32_t col = pv.dcols[uint64_t(c0 + c) * kChunkCols + lane];
-      const uint32_t zt = smem_u32(bs + ds * C::SLOT);
-      const uint32_t ht = zt + C::PZ * C::T_BYTES;
+      const uint32_t ht = hr_s + ds * C::T_BYTES;
       constexpr uint32_t LPR = DC / 4, RPI = 32 / LPR;
       const uint32_t j = lane % LPR, jj = j & 7u;
 #pragma unroll
@@ -327,20 +342,20 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
         const uint32_t ck = __shfl_sync(0xFFFFFFFFu, col, k);
         const bool real = ck != 0xFFFFFFFFu && int(4 * j) < dvalid;
         const uint64_t gofs = uint64_t(ck) * ld + 4 * j;
-        // z: K-major SWIZZLE_128B, row k, 16-byte piece j
-        const uint32_t zo = (j >> 3) * 4096u + (k >> 3) * 1024u + (k & 7u) * 128u + ((jj ^ (k & 7u)) << 4);
+        // z: K-major SWIZZLE_128B, row k, 16-byte piece j; K block j>>3 of slot ds
+        const uint32_t zo = ((j >> 3) * C::NB + ds) * 4096u + (k >> 3) * 1024u + (k & 7u) * 128u +
+                            ((jj ^ (k & 7u)) << 4);
         // h: MN-major SWIZZLE_128B_BASE32B (tc05.cuh desc_mn32)
         const uint32_t ho = (j >> 3) * 4096u + (k >> 2) * 512u + (k & 3u) * 128u +
                             ((((jj >> 1) ^ (k & 3u)) << 5) | ((jj & 1u) << 4));
-        cp_async16(zt + zo, real ? z + gofs : g_agnn_zero);
+        cp_async16(zr_s + zo, real ? z + gofs : g_agnn_zero);
         cp_async16(ht + ho, real ? h + gofs : g_agnn_zero);
         if constexpr (C::F32) {  // lo planes (pre-split once per layer)
-          cp_async16(zt + C::T_BYTES + zo, real ? z1 + gofs : g_agnn_zero);
-          cp_async16(ht + C::T_BYTES + ho, real ? h1 + gofs : g_agnn_zero);
+          cp_async16(zr_s + C::KB * C::NB * 4096u + zo, real ? z1 + gofs : g_agnn_zero);
+          cp_async16(ht + C::NB * C::T_BYTES + ho, real ? h1 + gofs : g_agnn_zero);
         }
       }
-      cp_async16(zt + (C::PZ + C::PH) * C::T_BYTES + lane * 16,
-                 pv.dmask + (uint64_t(c0 + c) * kPanelRows) + lane * 4);
+      cp_async16(mr_s + ds * C::M_BYTES + lane * 16, pv.dmask + (uint64_t(c0 + c) * kPanelRows) + lane * 4);
       cp_async_arrive_noinc(bfull + ds);
     }
     cp_async_wait<0>();
