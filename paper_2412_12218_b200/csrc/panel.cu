@@ -265,7 +265,11 @@ struct PanelCfg {
   static constexpr int NS = PREC == SGTK_FP32 ? 2 : 4;              // A ring depth
   static constexpr int GW = 4 / NS;                                 // builder warps per chunk
   static constexpr int NV = PREC == SGTK_FP32 ? 2 : 1;              // entry (+ value) slots
-  static constexpr int NF = 512 / DC;                               // TMEM accumulators
+  // DC = 32 TF32 fits two CTAs per SM (256 TMEM columns, <= 113 KB smem,
+  // <= 102 registers); the others run one
+  static constexpr int CTAS = (DC == 32 && PREC == SGTK_TF32) ? 2 : 1;
+  static constexpr uint32_t TMEM_COLS = CTAS == 2 ? 256 : 512;
+  static constexpr int NF = TMEM_COLS / DC;                         // TMEM accumulators
   static constexpr uint32_t FOLD = 4;                               // chunks per accumulator
 };
 
@@ -306,7 +310,7 @@ __device__ __align__(16) float g_zero_row[64];
 //               tensor-core accumulation chain <= FOLD chunks), store.
 // ---------------------------------------------------------------------------
 template <int DC, int PREC>
-__global__ void __launch_bounds__(kPanelThreads, 1)
+__global__ void __launch_bounds__(kPanelThreads, PanelCfg<DC, PREC>::CTAS)
 spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict__ x, uint64_t ldx,
                   uint64_t d, float* __restrict__ out, uint64_t ldo, int vec_out,
                   long long* __restrict__ trace) {
@@ -355,7 +359,7 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
     }
     mbar_init_fence();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -430,8 +434,7 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
             umma_tf32(dt, ad0, bd0, idesc, acc);
           }
         }
-        umma_commit(empty + s);
-        umma_commit(bempty + ds);
+        umma_commit(bempty + ds);  // A stage, B tile and entry slot of chunk c free
         if ((c % C::FOLD) == C::FOLD - 1 || c + 1 == nch) umma_commit(accfull + buf);
       }
     }
@@ -478,7 +481,10 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
       const uint32_t abase = smem_u32(ring + s * C::A_STAGE);
       const uint64_t e0 = pv.coff[c0 + c], e1 = pv.coff[c0 + c + 1];
       const uint32_t ne = uint32_t(e1 - e0);
-      mbar_wait(empty + s, ph ^ 1u);
+      if (c >= uint32_t(C::NS)) {  // MMA(c - NS) retired: A stage free (one commit per chunk)
+        const uint32_t cp = c - C::NS;
+        mbar_wait(bempty + cp % ND, (cp / ND) & 1u);
+      }
       if (lane == 0) mark(c, 1);
       if (c + PD < nch) gather_b(c + PD, idn);
       idn = id_of(c + PD + C::NS);
@@ -591,7 +597,7 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, C::TMEM_COLS);
   }
 }
 
@@ -739,11 +745,12 @@ bool panel_smem(uint32_t max_entries, PanelSmem& L) {
   using C = PanelCfg<DC, PREC>;
   L.dslot = ((max_entries + 3) / 4 * 4 * 4 + 127) / 128 * 128;
   L.bring_off = kBarBytes + C::NS * C::A_STAGE;
+  const uint32_t cap = C::CTAS == 2 ? kSmemCap / 2 - 1024 : kSmemCap;
   for (uint32_t nd = kMaxND; nd >= uint32_t(C::NS); nd -= C::NS) {
     L.nd = nd;
     L.dring_off = L.bring_off + nd * C::B_STAGE;
     L.total = L.dring_off + nd * C::NV * L.dslot + 1024 /*alignment slack*/;
-    if (L.total <= kSmemCap) return true;
+    if (L.total <= cap) return true;
   }
   return false;
 }
