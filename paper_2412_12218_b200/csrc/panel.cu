@@ -262,14 +262,17 @@ struct PanelCfg {
   static constexpr uint32_t B_BYTES = kChunkCols * DC * 4;          // MN-major
   static constexpr uint32_t A_STAGE = PA * A_BYTES;                 // multiple of 1024
   static constexpr uint32_t B_STAGE = PB * B_BYTES;                 // multiple of 1024
-  static constexpr int NS = PREC == SGTK_FP32 ? 2 : 4;              // A ring depth
+  static constexpr int NS = (PREC == SGTK_FP32 || DC == 64) ? 2 : 4;  // A ring depth
   static constexpr int GW = 4 / NS;                                 // builder warps per chunk
   static constexpr int NV = PREC == SGTK_FP32 ? 2 : 1;              // entry (+ value) slots
   // DC = 32 TF32 fits two CTAs per SM (256 TMEM columns, <= 113 KB smem,
   // <= 102 registers); the others run one
-  static constexpr int CTAS = (DC == 32 && PREC == SGTK_TF32) ? 2 : 1;
+  static constexpr int CTAS = PREC == SGTK_TF32 ? 2 : 1;
   static constexpr uint32_t TMEM_COLS = CTAS == 2 ? 256 : 512;
-  static constexpr int NF = TMEM_COLS / DC;                         // TMEM accumulators
+  // TMEM: running fp32 sum (DC columns, updated by the accumulator warps
+  // 16 columns at a time: few registers) + NF accumulation buffers
+  static constexpr int NF = (TMEM_COLS - DC) / DC;
+  static constexpr uint32_t BUF0 = DC;                              // first buffer column
   static constexpr uint32_t FOLD = 4;                               // chunks per accumulator
 };
 
@@ -417,7 +420,7 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
         }
         tc_fence_after();
         mark(c, 5);
-        const uint32_t dt = tmem + buf * DC;
+        const uint32_t dt = tmem + C::BUF0 + buf * DC;
         const uint32_t a0 = smem_u32(ring + s * C::A_STAGE), a1 = a0 + C::A_BYTES;
         const uint32_t b0 = smem_u32(bring + ds * C::B_STAGE), b1 = b0 + C::B_BYTES, b2 = b1 + C::B_BYTES;
 #pragma unroll
@@ -557,38 +560,57 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
     }
   } else {
     // ------------------------------------------------------------ accumulators
+    // Fold each finished group into the running sum kept in TMEM (IEEE adds,
+    // group order), 16 columns at a time; then stream the sum out.
     const uint32_t q = warp & 3u;
     const uint64_t r = p * kPanelRows + q * 32 + lane;
-    float acc[DC];
-#pragma unroll
-    for (int j = 0; j < DC; ++j) acc[j] = 0.0f;
+    const uint32_t lanes = (q * 32u) << 16;
     for (uint32_t g = 0; g < ngroups; ++g) {
       const uint32_t buf = g % C::NF;
       mbar_wait(accfull + buf, (g / C::NF) & 1u);
       tc_fence_after();
 #pragma unroll
       for (int cc = 0; cc < DC; cc += 16) {
-        uint32_t v[16];
-        tmem_ld16(tmem + ((q * 32u) << 16) + buf * DC + cc, v);
+        uint32_t v[16], sm[16];
+        tmem_ld16(tmem + lanes + C::BUF0 + buf * DC + cc, v);
+        if (g) tmem_ld16(tmem + lanes + cc, sm);
         tmem_ld_wait();
+        if (g) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[cc + j] += __uint_as_float(v[j]);
+          for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(sm[j]) + __uint_as_float(v[j]));
+        }
+        tmem_st16(tmem + lanes + cc, v);
       }
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(accempty + buf);
     }
-    if (r < pv.n_rows) {
-      float* o = out + r * ldo + fbase;
-      if (vec_out && dvalid == DC) {
+    tc_fence_after();
+    const bool rv = r < pv.n_rows;
+    float* o = out + r * ldo + fbase;
 #pragma unroll
-        for (int j = 0; j < DC / 4; ++j)
-          reinterpret_cast<float4*>(o)[j] =
-              make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+    for (int cc = 0; cc < DC; cc += 16) {
+      uint32_t v[16];
+      if (ngroups) {
+        tmem_ld16(tmem + lanes + cc, v);
+        tmem_ld_wait();
       } else {
 #pragma unroll
-        for (int j = 0; j < DC; ++j)
-          if (j < dvalid) o[j] = acc[j];
+        for (int j = 0; j < 16; ++j) v[j] = 0u;
+      }
+      if (rv) {
+        if (vec_out && dvalid == DC) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            reinterpret_cast<float4*>(o + cc)[j] =
+                make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (cc + j < dvalid) o[cc + j] = __uint_as_float(v[j]);
+        }
       }
     }
   }
