@@ -33,7 +33,8 @@
 //               stay <= 4 chunks long) on a schedule fixed by the panel's
 //               shape (deterministic), then the epilogue store.
 // Precision: TF32 = both operands RNE-rounded like tf32_round_value
-// (tile_exec.cpp:131-142); FP32 = the 4-term TF32 split (common.cuh).
+// (tile_exec.cpp:131-142); FP32 = 3-term TF32 split a1*b0 + a0*b1 + a0*b0
+// (dropped terms < 2^-21 relative per product).
 
 #include <cub/device/device_scan.cuh>
 
@@ -257,7 +258,7 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaStrea
 template <int DC, int PREC>
 struct PanelCfg {
   static constexpr int PA = PREC == SGTK_FP32 ? 2 : 1;  // A planes (split2)
-  static constexpr int PB = PREC == SGTK_FP32 ? 3 : 1;  // B planes (split3)
+  static constexpr int PB = PREC == SGTK_FP32 ? 2 : 1;  // B planes (split2)
   static constexpr uint32_t A_BYTES = kPanelRows * kChunkCols * 4;  // 16 KB, K-major
   static constexpr uint32_t B_BYTES = kChunkCols * DC * 4;          // MN-major
   static constexpr uint32_t A_STAGE = PA * A_BYTES;                 // multiple of 1024
@@ -428,9 +429,8 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
           const uint32_t acc = (first && ks == 0) ? 0u : 1u;
           const uint64_t ad0 = umma_desc(a0 + ks * 32);
           const uint64_t bd0 = desc_mn32(b0 + ks * 1024, 4096, 512);
-          if constexpr (PREC == SGTK_FP32) {
-            umma_tf32(dt, ad0, desc_mn32(b2 + ks * 1024, 4096, 512), idesc, acc);
-            umma_tf32(dt, umma_desc(a1 + ks * 32), bd0, idesc, 1u);
+          if constexpr (PREC == SGTK_FP32) {  // 3-term split: a1*b0 + a0*b1 + a0*b0
+            umma_tf32(dt, umma_desc(a1 + ks * 32), bd0, idesc, acc);
             umma_tf32(dt, ad0, desc_mn32(b1 + ks * 1024, 4096, 512), idesc, 1u);
             umma_tf32(dt, ad0, bd0, idesc, 1u);
           } else {
@@ -536,19 +536,18 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
         }
       }
       if constexpr (PREC == SGTK_FP32) {
-        // B tile: exact 3-plane split in place (every lane of the group first
+        // B tile: 2-plane TF32 split in place (every lane of the group first
         // waits for all copies of the tile)
         mbar_wait(bfull + ds, dph);
         uint4* B = reinterpret_cast<uint4*>(bring + ds * C::B_STAGE);
 #pragma unroll 4
         for (uint32_t i = gl; i < C::B_BYTES / 16; i += GT) {
           const uint4 v = B[i];
-          uint32_t xs[4] = {v.x, v.y, v.z, v.w}, q0[4], q1[4], q2[4];
+          uint32_t xs[4] = {v.x, v.y, v.z, v.w}, q0[4], q1[4];
 #pragma unroll
-          for (int jx = 0; jx < 4; ++jx) split3(__uint_as_float(xs[jx]), q0[jx], q1[jx], q2[jx]);
+          for (int jx = 0; jx < 4; ++jx) split2(__uint_as_float(xs[jx]), q0[jx], q1[jx]);
           B[i] = make_uint4(q0[0], q0[1], q0[2], q0[3]);
           B[C::B_BYTES / 16 + i] = make_uint4(q1[0], q1[1], q1[2], q1[3]);
-          B[2 * C::B_BYTES / 16 + i] = make_uint4(q2[0], q2[1], q2[2], q2[3]);
         }
       }
       fence_async_smem();
