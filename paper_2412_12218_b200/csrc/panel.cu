@@ -106,18 +106,6 @@ __device__ __forceinline__ bool dense_slot(const uint32_t* __restrict__ e2r,
   return flag[u] != 0;
 }
 
-__global__ void chunk_count_kernel(const uint32_t* __restrict__ e2r, const uint32_t* __restrict__ e2c,
-                                   const uint64_t* __restrict__ wo, const uint32_t* __restrict__ flag,
-                                   const uint32_t* __restrict__ grank,
-                                   const uint32_t* __restrict__ cptr, uint64_t E,
-                                   uint32_t* __restrict__ ccnt) {
-  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < E;
-       e += uint64_t(gridDim.x) * blockDim.x) {
-    uint32_t p, slot;
-    if (dense_slot(e2r, e2c, wo, flag, grank, e, p, slot))
-      atomicAdd(ccnt + cptr[p] + slot / kChunkCols, 1u);
-  }
-}
 
 __global__ void fill_u32_kernel(uint32_t* __restrict__ p, uint64_t n, uint32_t v) {
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -132,35 +120,74 @@ __device__ __forceinline__ uint32_t pack_entry(float v, uint32_t row, uint32_t k
   return (__float_as_uint(tf32_rne(v)) & 0xFFFFE000u) | (row << 5) | k;
 }
 
-__global__ void entry_fill_kernel(const uint32_t* __restrict__ e2r, const uint32_t* __restrict__ e2c,
-                                  const uint64_t* __restrict__ wo, const uint32_t* __restrict__ flag,
-                                  const uint32_t* __restrict__ grank,
-                                  const uint32_t* __restrict__ cptr, const uint64_t* __restrict__ coff,
-                                  const float* __restrict__ vals, uint64_t E,
-                                  uint32_t* __restrict__ cfill, uint32_t* __restrict__ dent,
-                                  float* __restrict__ dval, uint32_t* __restrict__ deid) {
+// Row masks straight from the edges: bit k of dmask[chunk][row] <=> edge
+// (row, chunk column k).  OR is order-free: deterministic.
+__global__ void edge_mask_kernel(const uint32_t* __restrict__ e2r, const uint32_t* __restrict__ e2c,
+                                 const uint64_t* __restrict__ wo, const uint32_t* __restrict__ flag,
+                                 const uint32_t* __restrict__ grank, const uint32_t* __restrict__ cptr,
+                                 uint64_t E, uint32_t* __restrict__ dmask) {
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < E;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t p, slot;
+    if (dense_slot(e2r, e2c, wo, flag, grank, e, p, slot))
+      atomicOr(dmask + uint64_t(cptr[p] + slot / kChunkCols) * kPanelRows + e2r[e] % kPanelRows,
+               1u << (slot % kChunkCols));
+  }
+}
+
+// Per chunk: entries before each row (exclusive scan of the rows' popcounts).
+__global__ void row_offsets_kernel(const uint32_t* __restrict__ dmask, uint64_t NC,
+                                   uint16_t* __restrict__ rowoff, uint32_t* __restrict__ ccnt) {
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t c = warp; c < NC; c += nw) {
+    const uint4 m = reinterpret_cast<const uint4*>(dmask + c * kPanelRows)[lane];  // rows 4l..4l+3
+    const uint32_t a = __popc(m.x), b = __popc(m.y), cc = __popc(m.z), dd = __popc(m.w);
+    uint32_t s = a + b + cc + dd, incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const uint32_t ex = incl - s;
+    uint16_t* ro = rowoff + c * kPanelRows + 4 * lane;
+    ro[0] = uint16_t(ex);
+    ro[1] = uint16_t(ex + a);
+    ro[2] = uint16_t(ex + a + b);
+    ro[3] = uint16_t(ex + a + b + cc);
+    if (lane == 31) ccnt[c] = incl;
+  }
+}
+
+// Entries of a chunk in (row, column) order -- the CSR order -- so the
+// builders' scattered shared-memory stores of consecutive entries land in
+// few rows (bank-friendly), and the layout is fully deterministic.
+__global__ void entry_fill_sorted_kernel(const uint32_t* __restrict__ e2r, const uint32_t* __restrict__ e2c,
+                                         const uint64_t* __restrict__ wo, const uint32_t* __restrict__ flag,
+                                         const uint32_t* __restrict__ grank,
+                                         const uint32_t* __restrict__ cptr, const uint64_t* __restrict__ coff,
+                                         const uint32_t* __restrict__ dmask,
+                                         const uint16_t* __restrict__ rowoff,
+                                         const float* __restrict__ vals, uint64_t E,
+                                         uint32_t* __restrict__ dent, float* __restrict__ dval,
+                                         uint32_t* __restrict__ deid) {
   for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < E;
        e += uint64_t(gridDim.x) * blockDim.x) {
     uint32_t p, slot;
     if (!dense_slot(e2r, e2c, wo, flag, grank, e, p, slot)) continue;
-    const uint32_t ch = cptr[p] + slot / kChunkCols;
-    const uint64_t i = coff[ch] + atomicAdd(cfill + ch, 1u);
+    const uint64_t ch = cptr[p] + slot / kChunkCols;
+    const uint32_t row = e2r[e] % kPanelRows, k = slot % kChunkCols;
+    const uint32_t m = dmask[ch * kPanelRows + row];
+    const uint64_t i = coff[ch] + rowoff[ch * kPanelRows + row] + __popc(m & ((1u << k) - 1u));
     const float v = vals ? vals[e] : 1.0f;
-    dent[i] = pack_entry(v, e2r[e] % kPanelRows, slot % kChunkCols);
+    dent[i] = pack_entry(v, row, k);
     dval[i] = v;
     deid[i] = uint32_t(e);
   }
 }
 
-// Row masks per chunk: bit k of dmask[chunk][row] <=> edge (row, chunk col k)
-__global__ void chunk_mask_kernel(const uint64_t* __restrict__ coff, uint64_t NC,
-                                  const uint32_t* __restrict__ dent, uint32_t* __restrict__ dmask) {
-  for (uint64_t c = blockIdx.x; c < NC; c += gridDim.x)
-    for (uint64_t i = coff[c] + threadIdx.x; i < coff[c + 1]; i += blockDim.x) {
-      const uint32_t w = dent[i];
-      if (!(w & kEntrySkip)) atomicOr(dmask + c * kPanelRows + ((w >> 5) & 127u), 1u << (w & 31u));
-    }
-}
+
 
 // sparse (CUDA-core) edges: per-row count, then per-row stable compaction
 __global__ void sparse_count_kernel(const uint64_t* __restrict__ np, uint64_t n,
@@ -903,14 +930,19 @@ void build_panels(sgtk_graph& g, cudaStream_t s) {
         pn->cptr->as<uint32_t>(), P, pn->dcols->as<uint32_t>());
   CU_LAUNCH("dcols_kernel");
 
-  DevBuf ccnt(std::max<uint64_t>(NC, 1) * 4);
-  CU(cudaMemsetAsync(ccnt.p, 0, ccnt.bytes, s));
+  // row masks from the edges, per-chunk row offsets, entry counts
+  pn->dmask = std::make_shared<DevBuf>(std::max<uint64_t>(NC, 1) * kPanelRows * 4);
+  CU(cudaMemsetAsync(pn->dmask->p, 0, pn->dmask->bytes, s));
   if (E)
-    chunk_count_kernel<<<grid_for(E, 256), 256, 0, s>>>(e2r, e2c, wo, flag.as<uint32_t>(),
-                                                        grank.as<uint32_t>(),
-                                                        pn->cptr->as<uint32_t>(), E,
-                                                        ccnt.as<uint32_t>());
-  CU_LAUNCH("chunk_count_kernel");
+    edge_mask_kernel<<<grid_for(E, 256), 256, 0, s>>>(e2r, e2c, wo, flag.as<uint32_t>(),
+                                                      grank.as<uint32_t>(), pn->cptr->as<uint32_t>(),
+                                                      E, pn->dmask->as<uint32_t>());
+  CU_LAUNCH("edge_mask_kernel");
+  DevBuf ccnt(std::max<uint64_t>(NC, 1) * 4), rowoff(std::max<uint64_t>(NC, 1) * kPanelRows * 2);
+  if (NC)
+    row_offsets_kernel<<<grid_for(NC * 32, 256), 256, 0, s>>>(pn->dmask->as<uint32_t>(), NC,
+                                                              rowoff.as<uint16_t>(), ccnt.as<uint32_t>());
+  CU_LAUNCH("row_offsets_kernel");
   std::vector<uint32_t> cc = dl<uint32_t>(ccnt.p, NC, s);
   std::vector<uint64_t> coff(NC + 1, 0);
   uint32_t mx = 0;
@@ -928,20 +960,13 @@ void build_panels(sgtk_graph& g, cudaStream_t s) {
   fill_u32_kernel<<<grid_for(ND, 256), 256, 0, s>>>(pn->dent->as<uint32_t>(), ND, kEntrySkip);
   CU(cudaMemsetAsync(pn->dval->p, 0, ND * 4, s));
   CU(cudaMemsetAsync(pn->deid->p, 0xFF, ND * 4, s));
-  CU(cudaMemsetAsync(ccnt.p, 0, ccnt.bytes, s));
   const float* vals = g.has_values ? g.vals->as<float>() : nullptr;
   if (E)
-    entry_fill_kernel<<<grid_for(E, 256), 256, 0, s>>>(
+    entry_fill_sorted_kernel<<<grid_for(E, 256), 256, 0, s>>>(
         e2r, e2c, wo, flag.as<uint32_t>(), grank.as<uint32_t>(), pn->cptr->as<uint32_t>(),
-        pn->coff->as<uint64_t>(), vals, E, ccnt.as<uint32_t>(), pn->dent->as<uint32_t>(),
-        pn->dval->as<float>(), pn->deid->as<uint32_t>());
-  CU_LAUNCH("entry_fill_kernel");
-  pn->dmask = std::make_shared<DevBuf>(std::max<uint64_t>(NC, 1) * kPanelRows * 4);
-  CU(cudaMemsetAsync(pn->dmask->p, 0, pn->dmask->bytes, s));
-  if (NC)
-    chunk_mask_kernel<<<grid_for(NC, 1, 148u * 16u), 128, 0, s>>>(
-        pn->coff->as<uint64_t>(), NC, pn->dent->as<uint32_t>(), pn->dmask->as<uint32_t>());
-  CU_LAUNCH("chunk_mask_kernel");
+        pn->coff->as<uint64_t>(), pn->dmask->as<uint32_t>(), rowoff.as<uint16_t>(), vals, E,
+        pn->dent->as<uint32_t>(), pn->dval->as<float>(), pn->deid->as<uint32_t>());
+  CU_LAUNCH("entry_fill_sorted_kernel");
 
   DevBuf scnt((n + 1) * 4);
   CU(cudaMemsetAsync(scnt.p, 0, (n + 1) * 4, s));
