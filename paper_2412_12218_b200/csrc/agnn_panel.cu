@@ -61,7 +61,12 @@ struct AgnnCfg {
   static constexpr int NP = 2;                             // P ring
   // TMEM: 2 S buffers x 64 columns (S of a chunk pair, N = 64 costs what
   // N = 32 does), NF O accumulators x DC; 256 columns -> 2 CTAs per SM
-  static constexpr int NF = DC == 32 ? 4 : 2;
+  // TF32, DC = 32: P goes from the softmax threads' registers straight into
+  // TMEM (tcgen05.st) and PV reads A from TMEM (no shared-memory P tile)
+  static constexpr bool PT = !F32 && DC == 32;
+  static constexpr uint32_t P_COL = 128;                // P[NP] x 32 columns (PT)
+  static constexpr uint32_t O_COL = PT ? 192 : 128;
+  static constexpr int NF = PT ? 2 : (DC == 32 ? 4 : 2);
   static constexpr uint32_t TMEM_COLS = 256;
   static constexpr uint32_t FOLD = 4;
   static constexpr uint32_t Q_OFF = 1024;
@@ -140,7 +145,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t s_col = 0, o_col = 128;  // TMEM columns: S[2] x 64, O[NF] x DC
+  const uint32_t s_col = 0, o_col = C::O_COL;  // TMEM: S[2] x 64, (P[NP] x 32), O[NF] x DC
 
   if (warp < 4) {
     // ------------------------------------------------------------ softmax
@@ -201,6 +206,15 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       if (c >= uint32_t(C::NP)) {  // PV(c - NP) done with this P slot
         const uint32_t cp = c - C::NP;
         mbar_wait(bempty + cp % C::NB, (cp / C::NB) & 1u);
+      }
+      if constexpr (C::PT) {
+        tmem_st32(tmem + ((warp * 32u) << 16) + C::P_COL + pslot * 32, *reinterpret_cast<uint32_t(*)[32]>(pr));
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (warp == 0 && lane == 0) mark(c, 2);
+        if (lane == 0) mbar_arrive(pfull + pslot);
+        continue;
       }
       const uint32_t pt = pb + pslot * C::PP * C::P_BYTES;
 #pragma unroll
@@ -309,7 +323,9 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
         for (uint32_t ks = 0; ks < kChunkCols / 8; ++ks) {
           const uint32_t acc = (first && ks == 0) ? 0u : 1u;
           const uint64_t p0 = umma_desc(pt + ks * 32), h0 = desc_mn32(ht + ks * 1024, 4096, 512);
-          if constexpr (C::F32) {
+          if constexpr (C::PT) {
+            umma_tf32_ts(dt, tmem + C::P_COL + pslot * 32 + ks * 8, h0, id_o, acc);
+          } else if constexpr (C::F32) {
             umma_tf32(dt, p0, desc_mn32(ht + C::NB * C::T_BYTES + ks * 1024, 4096, 512), id_o, acc);
             umma_tf32(dt, umma_desc(pt + C::P_BYTES + ks * 32), h0, id_o, 1u);
             umma_tf32(dt, p0, h0, id_o, 1u);
