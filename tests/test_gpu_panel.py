@@ -177,3 +177,63 @@ def test_panel_agnn_deterministic_and_fallback():
     want, _ = O.agnn_forward(ga, x.cpu().numpy(), [60.0])
     got = dg.agnn_forward(x, [60.0], mode=2).cpu().numpy()
     assert mre(got, want) <= 1e-5
+
+
+# ------------------------------------------------------- panel format (build)
+def _panel_restatement(g):
+    """numpy restatement of build_panels (panel.cu): per 128-row panel the
+    columns with >= 2 edges are dense (sorted, padded to 32 per panel), a
+    chunk's entries in (row, column) order, row masks, row offsets, sparse
+    edges per row in CSR order."""
+    n = g.num_nodes
+    npz = g.node_pointer.astype(np.int64)
+    el = g.edge_list.astype(np.int64)
+    rows = np.repeat(np.arange(n), np.diff(npz))
+    vals = np.ones(len(el), np.float32) if g.values is None else g.values
+    P = (n + 127) // 128
+    dcols, cptr, masks, ents, sparse = [], [0], [], [], [[] for _ in range(n)]
+    for p in range(P):
+        m = (rows // 128) == p
+        cols, cnt = np.unique(el[m], return_counts=True)
+        dense = cols[cnt >= 2]
+        nch = (len(dense) + 31) // 32
+        cptr.append(cptr[-1] + nch)
+        pad = np.full(nch * 32, 0xFFFFFFFF, np.uint64)
+        pad[:len(dense)] = dense
+        dcols.append(pad)
+        slot = {int(c): i for i, c in enumerate(dense)}
+        cm = np.zeros((nch, 128), np.uint32)
+        ce = [[] for _ in range(nch)]
+        for e in np.nonzero(m)[0]:
+            r, c = int(rows[e]), int(el[e])
+            if c in slot:
+                s = slot[c]
+                cm[s // 32, r % 128] |= np.uint32(1 << (s % 32))
+                ce[s // 32].append((r % 128, s % 32, vals[e]))
+            else:
+                sparse[r].append((c, vals[e]))
+        masks.append(cm)
+        ents += [sorted(x, key=lambda t: (t[0], t[1])) for x in ce]
+    return (np.array(cptr, np.uint32), np.concatenate(dcols) if dcols else np.zeros(0),
+            np.concatenate(masks) if masks else np.zeros((0, 128)), ents, sparse)
+
+
+@pytest.mark.parametrize("name,g", GRAPHS[:3], ids=[n for n, _ in GRAPHS[:3]])
+def test_panel_format_matches_restatement(name, g):
+    dg = DeviceGraph.from_csr(g.node_pointer, g.edge_list, g.values)
+    A = dg.panel_arrays()
+    cptr, dcols, masks, ents, sparse = _panel_restatement(g)
+    np.testing.assert_array_equal(A["chunk_ptr"], cptr)
+    np.testing.assert_array_equal(A["dense_cols"].astype(np.uint64), dcols)
+    off = A["chunk_off"].astype(np.int64)
+    for c, want in enumerate(ents):
+        got = A["dense_entries"][off[c]:off[c + 1]]
+        got = got[(got & 0x1000) == 0]
+        assert [((w >> 5) & 127, w & 31) for w in got] == [(r, k) for r, k, _ in want], c
+        tf = np.array([O.tf32_round_value(float(v)) for _, _, v in want], np.float32)
+        np.testing.assert_array_equal((got & 0xFFFFE000).view(np.float32), tf)
+    sp = A["sparse_ptr"].astype(np.int64)
+    se = A["sparse_entries"].reshape(-1, 2)
+    for r in range(g.num_nodes):
+        got = [(int(c), float(np.uint32(v).view(np.float32))) for c, v in se[sp[r]:sp[r + 1]]]
+        assert got == [(c, float(v)) for c, v in sparse[r]], r
