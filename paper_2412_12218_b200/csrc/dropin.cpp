@@ -384,7 +384,9 @@ SGTK_EXPORT DenseMatrix agnn_forward(const TransformedGraph& t, const DenseMatri
     Dev<char> ws(wsb);
     Dev<float> xd(x.data.data(), x.data.size()), od(out.data.size());
     auto cut = upload_cut(t, plan);
-    const int mode = x.cols <= 64 ? 1 : 0;  // fused single pass when it fits
+    // panel mode (tcgen05 + CUDA cores, agnn_panel.cu); outside its envelope
+    // (|beta| > 40, d > 64, partial plans) it falls back to the fused 16-row mode
+    const int mode = x.cols <= 64 ? 2 : 0;
     ck(sgtk_agnn_forward(dg, xd.p, x.cols, x.cols, uint32_t(layers.size()), betas.data(),
                          cut ? cut->p : nullptr, prec_of(prec), mode, ws.p, wsb, od.p, x.cols,
                          &zeros, nullptr));
