@@ -438,12 +438,15 @@ __device__ __forceinline__ void agnn_finalize(uint64_t r, const float (&o)[FPL],
 }
 
 // Sparse edges of a row, batches of 32:
-//   lane = edge: gather z_col (whole rows, 128/256 B), dot with z_row (held in
-//     registers by every lane), p = exp2(beta*log2e*s - |beta|*log2e); the
-//     z_col row and its coefficient p * |h_col| go to a per-warp smem tile
-//     (h_col = z_col * |h_col|: z is h scaled to unit norm, gnn.cpp:74-91, so
-//     the aggregation needs no second gather);
-//   lane = feature: O[f] += coef_e * T[e][f] over the batch, e ascending.
+//   the batch's z_col rows (128/256 B each) go to a per-warp smem tile T by
+//     cp.async (TF32 mode reads the pre-rounded copy zq, so T is already the
+//     MMA-rounded operand);
+//   lane = edge: dot of T[e] with z_row (held in registers by every lane),
+//     p = exp2(beta*log2e*s - |beta|*log2e), coefficient p * |h_col| in a
+//     register (h_col = z_col * |h_col|: z is h scaled to unit norm,
+//     gnn.cpp:74-91, so the aggregation needs no second gather);
+//   lane = feature: O[f] += coef_e * T[e][f] over the batch, e ascending,
+//     coef_e broadcast by shuffle.
 // Row sums l: per-lane partials, reduced by a fixed shuffle tree per item.
 template <int FPL, int PREC, bool SPLIT>
 __global__ void __launch_bounds__(FPL == 1 ? 256 : 128)
@@ -477,10 +480,6 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
       const float4 v = __ldg(zrow + k);  // padding features are zeros
       zr[4 * k] = v.x; zr[4 * k + 1] = v.y; zr[4 * k + 2] = v.z; zr[4 * k + 3] = v.w;
     }
-    if constexpr (PREC == SGTK_TF32) {
-#pragma unroll
-      for (int k = 0; k < DC; ++k) zr[k] = tf32_rne(zr[k]);
-    }
     float o[FPL], lpp = 0.0f;
 #pragma unroll
     for (int i = 0; i < FPL; ++i) o[i] = (!SPLIT && direct && i < fv) ? opart[r * DC + f + i] : 0.0f;
@@ -502,16 +501,12 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
         cp_async_wait<0>();
         __syncwarp();
       }
+      float cf_l = 0.0f;
       if (lane < cnt) {
         float s = 0.0f;
 #pragma unroll
         for (int k = 0; k < DC / 4; ++k) {
-          float4 v = ld_shared_f4(tb + (lane * TS + 4 * k) * 4);
-          if constexpr (PREC == SGTK_TF32) {
-            v.x = tf32_rne(v.x); v.y = tf32_rne(v.y); v.z = tf32_rne(v.z); v.w = tf32_rne(v.w);
-            st_shared_v4(tb + (lane * TS + 4 * k) * 4, __float_as_uint(v.x), __float_as_uint(v.y),
-                         __float_as_uint(v.z), __float_as_uint(v.w));
-          }
+          const float4 v = ld_shared_f4(tb + (lane * TS + 4 * k) * 4);
           s = fmaf(zr[4 * k], v.x, s);
           s = fmaf(zr[4 * k + 1], v.y, s);
           s = fmaf(zr[4 * k + 2], v.z, s);
@@ -521,12 +516,11 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
         float pe = ex2_approx(fmaf(s, bl2, -off));
         if constexpr (PREC == SGTK_TF32) pe = __uint_as_float(tf32_op(pe));
         lpp += pe;
-        T[lane * TS + DC] = pe * __ldg(norm + col);
+        cf_l = pe * __ldg(norm + col);
       }
-      __syncwarp();
 #pragma unroll 8
       for (uint32_t u = 0; u < cnt; ++u) {
-        const float cf = T[u * TS + DC];
+        const float cf = __shfl_sync(0xFFFFFFFFu, cf_l, u);
 #pragma unroll
         for (int i = 0; i < FPL; ++i) o[i] = fmaf(cf, T[u * TS + lane * FPL + i], o[i]);
       }
@@ -761,8 +755,8 @@ void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, cons
       if (ldq == 32) launch_agnn_rows<1, SGTK_FP32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
       else launch_agnn_rows<2, SGTK_FP32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
     } else {
-      if (ldq == 32) launch_agnn_rows<1, SGTK_TF32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
-      else launch_agnn_rows<2, SGTK_TF32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
+      if (ldq == 32) launch_agnn_rows<1, SGTK_TF32>(pn, zq, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
+      else launch_agnn_rows<2, SGTK_TF32>(pn, zq, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
     }
   };
   if (dbg == 1) {
