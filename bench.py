@@ -3,7 +3,7 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
                     [--workload reddit-agnn|proteins-gcn|pubmed-agnn|cora-gcn|powerlaw-gcn]
-                    [--precision fp32|tf32] [--mode fused|chain] [--locality calibrated|uniform]
+                    [--precision fp32|tf32] [--mode panel|fused|chain] [--locality calibrated|uniform]
 
 Default workload (config C4 of BASELINE.json): AGNN forward on a synthetic
 Reddit-shaped graph (232,965 nodes, ~114.6M edges incl. self-loops; in-proj
@@ -80,27 +80,77 @@ def make_graph(wl, locality, seed=1):
     return g, dict(avg_picks=round(picks, 3), **loc, alpha=wl["alpha"])
 
 
+class _NvmlSampler:
+    """NVML clock/throttle polling thread (every ~2 ms): the timed region of a
+    step is milliseconds long, too short for nvidia-smi's 100 ms loop."""
+
+    def __init__(self, rows):
+        import pynvml as nv
+
+        self.nv, self.rows, self.stop = nv, rows, threading.Event()
+        nv.nvmlInit()
+        self.h = None
+        try:
+            import torch
+
+            pr = torch.cuda.get_device_properties(torch_device_index())
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            self.h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            self.h = nv.nvmlDeviceGetHandleByIndex(torch_device_index())
+        self.mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        self.sample()  # first row before the timed region starts
+        self.th = threading.Thread(target=self.loop, daemon=True)
+        self.th.start()
+
+    def sample(self):
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        act = ["Active" if r & b else "Not Active" for b in bits]
+        self.rows.append(", ".join([str(sm), str(self.mx), "0"] + act))
+
+    def loop(self):
+        while not self.stop.wait(0.002):
+            try:
+                self.sample()
+            except Exception:
+                return
+
+    def terminate(self):
+        self.stop.set()
+        self.th.join(timeout=1)
+        try:
+            self.sample()  # last row after the timed region
+        except Exception:
+            pass
+
+
 def clocks_sampler():
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """Clocks/throttle sampling during the timed region: NVML polling when
+    pynvml loads, else nvidia-smi's loop (rows: sm, max sm, power, reasons)."""
+    rows = []
+    try:
+        return _NvmlSampler(rows), rows
+    except Exception:
+        rows.clear()
     q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
-    idx = os.environ.get("LOCAL_RANK", "0")
     try:
         p = subprocess.Popen(["nvidia-smi", "-i", str(torch_device_index()), f"--query-gpu={q}",
                               "--format=csv,noheader,nounits", "-lms", "100"],
                              stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
     except Exception:
         return None, None
-    rows = []
 
     def reader():
         for line in p.stdout:
             rows.append(line.strip())
 
-    th = threading.Thread(target=reader, daemon=True)
-    th.start()
-    _ = idx
+    threading.Thread(target=reader, daemon=True).start()
     return p, rows
 
 
@@ -435,7 +485,8 @@ def run_b200(args, wl):
                 "step": f"agnn_forward({L} layers) on the whole graph; value = step/{L}"
                 if wl["kind"] == "agnn" else f"gcn_forward({L} layers); value = step/{L}",
                 "tiles16x8": int(bs[0]), "tile_density16x8": round(bs[3], 4),
-                "translate_ms": round(translate_ms, 2)}),
+                "translate_ms": round(translate_ms, 2),
+                "panel_format": dg.panel_info() if mode == 2 else None}),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
             "model_forward_ms": round(model_ms, 4), "kernels_ms": kern,

@@ -38,13 +38,27 @@ __device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the thread sleeps until the phase
+// completes (or ~hint ns pass) instead of returning at once, so waiting warps
+// stop taking issue slots from the working warps of the same SM sub-partition
+__device__ __forceinline__ bool mbar_try_suspend(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity), "r"(0x100000u)
+      : "memory");
+  return ok != 0;
+}
 // Blocking wait with a watchdog: a pipeline bug traps (the launch fails with
 // an error) instead of hanging the GPU.  ~4 s at 2 GHz, far above any
 // legitimate wait in these kernels.
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   if (mbar_try(b, parity)) return;
   const long long t0 = clock64();
-  while (!mbar_try(b, parity))
+  while (!mbar_try_suspend(b, parity))
     if (clock64() - t0 > (1ll << 33)) __trap();
 }
 // Non-blocking probe: true once the phase with this parity has completed.
