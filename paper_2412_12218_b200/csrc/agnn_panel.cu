@@ -451,7 +451,8 @@ __device__ __forceinline__ void agnn_finalize(uint64_t r, const float (&o)[FPL],
 template <int FPL, int PREC, bool SPLIT>
 __global__ void __launch_bounds__(FPL == 1 ? 256 : 128)
 agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2* __restrict__ sent,
-                 const float* __restrict__ z, uint64_t ld, const float* __restrict__ norm,
+                 const float* __restrict__ zown, const float* __restrict__ z, uint64_t ld,
+                 const float* __restrict__ norm,
                  uint64_t d, uint64_t row_offset, float beta, const float* __restrict__ opart,
                  const float* __restrict__ lpart, float* __restrict__ seg_o,
                  float* __restrict__ seg_l, float* __restrict__ osp, float* __restrict__ lsp,
@@ -474,7 +475,7 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
     const bool direct = w.w == 0xFFFFFFFFu;
     const uint32_t c_first = w.y < w.z && lane < min(32u, w.z - w.y) ? sent[w.y + lane].x : 0u;
     float zr[DC];  // z of the row, every lane (dot products run lane = edge)
-    const float4* zrow = reinterpret_cast<const float4*>(z + (row_offset + r) * ld);
+    const float4* zrow = reinterpret_cast<const float4*>(zown + (row_offset + r) * ld);
 #pragma unroll
     for (int k = 0; k < DC / 4; ++k) {
       const float4 v = __ldg(zrow + k);  // padding features are zeros
@@ -503,7 +504,7 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
       }
       float cf_l = 0.0f;
       if (lane < cnt) {
-        float s = 0.0f;
+        float s = 0.0f, n2 = 0.0f;
 #pragma unroll
         for (int k = 0; k < DC / 4; ++k) {
           const float4 v = ld_shared_f4(tb + (lane * TS + 4 * k) * 4);
@@ -511,12 +512,26 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
           s = fmaf(zr[4 * k + 1], v.y, s);
           s = fmaf(zr[4 * k + 2], v.z, s);
           s = fmaf(zr[4 * k + 3], v.w, s);
+          if constexpr (PREC == SGTK_TF32) {
+            n2 = fmaf(v.x, v.x, n2);
+            n2 = fmaf(v.y, v.y, n2);
+            n2 = fmaf(v.z, v.z, n2);
+            n2 = fmaf(v.w, v.w, n2);
+          }
         }
-        if constexpr (PREC == SGTK_TF32) s = tf32_rne(s);  // sddmm TF32 rounds the dot (tile_exec.cpp:386)
+        if constexpr (PREC == SGTK_TF32) {
+          // T holds hq_col = tf32(h_col): z_col = h_col / |h_col| on the fly
+          // (no norm gather); sddmm TF32 rounds the dot (tile_exec.cpp:386)
+          s = tf32_rne(n2 > 0.0f ? s * rsqrtf(n2) : 0.0f);
+        }
         float pe = ex2_approx(fmaf(s, bl2, -off));
-        if constexpr (PREC == SGTK_TF32) pe = __uint_as_float(tf32_op(pe));
+        if constexpr (PREC == SGTK_TF32) {
+          pe = __uint_as_float(tf32_op(pe));
+          cf_l = pe;
+        } else {
+          cf_l = pe * __ldg(norm + col);
+        }
         lpp += pe;
-        cf_l = pe * __ldg(norm + col);
       }
 #pragma unroll 8
       for (uint32_t u = 0; u < cnt; ++u) {
@@ -679,7 +694,7 @@ void launch_agnn_dense(const PanelView& v, uint64_t P, const float* zraw, const 
 }
 
 template <int FPL, int PREC>
-void launch_agnn_rows(const Panels& pn, const float* z, uint64_t ld, const float* norm, uint64_t d,
+void launch_agnn_rows(const Panels& pn, const float* zown, const float* z, uint64_t ld, const float* norm, uint64_t d,
                       uint64_t row_offset, float beta, const float* opart, const float* lpart,
                       float* seg_o, float* seg_l, float* osp, float* lsp, const AgnnNext& nx,
                       cudaStream_t s, cudaStream_t s_final) {
@@ -687,11 +702,11 @@ void launch_agnn_rows(const Panels& pn, const float* z, uint64_t ld, const float
   if (pn.n_aitems) {
     if (osp)
       agnn_rows_kernel<FPL, PREC, true><<<blocks_for(pn.n_aitems * 32, bs), bs, 0, s>>>(
-          pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), z, ld, norm, d, row_offset, beta,
+          pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), zown, z, ld, norm, d, row_offset, beta,
           opart, lpart, seg_o, seg_l, osp, lsp, nx);
     else
       agnn_rows_kernel<FPL, PREC, false><<<blocks_for(pn.n_aitems * 32, bs), bs, 0, s>>>(
-          pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), z, ld, norm, d, row_offset, beta,
+          pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), zown, z, ld, norm, d, row_offset, beta,
           opart, lpart, seg_o, seg_l, osp, lsp, nx);
     CU_LAUNCH("agnn_rows_kernel");
   }
@@ -752,11 +767,11 @@ void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, cons
   };
   auto rows = [&](cudaStream_t st, float* o_sp, float* l_sp, cudaStream_t st_final) {
     if (prec == SGTK_FP32) {
-      if (ldq == 32) launch_agnn_rows<1, SGTK_FP32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
-      else launch_agnn_rows<2, SGTK_FP32>(pn, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
+      if (ldq == 32) launch_agnn_rows<1, SGTK_FP32>(pn, z, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
+      else launch_agnn_rows<2, SGTK_FP32>(pn, z, z, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
     } else {
-      if (ldq == 32) launch_agnn_rows<1, SGTK_TF32>(pn, zq, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
-      else launch_agnn_rows<2, SGTK_TF32>(pn, zq, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
+      if (ldq == 32) launch_agnn_rows<1, SGTK_TF32>(pn, zq, hq, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
+      else launch_agnn_rows<2, SGTK_TF32>(pn, zq, hq, ldq, norm, d, ro, beta, opart, lpart, seg_o, seg_l, o_sp, l_sp, nx, st, st_final);
     }
   };
   if (dbg == 1) {
