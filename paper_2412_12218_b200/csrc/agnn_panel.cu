@@ -405,10 +405,12 @@ __device__ __forceinline__ void agnn_finalize(uint64_t r, const float (&o)[FPL],
 #pragma unroll
   for (int i = 0; i < FPL; ++i) v[i] = l > 0.0f ? o[i] * inv_l : 0.0f;
   const uint64_t f = uint64_t(lane) * FPL;
+  if (nx.out) {
 #pragma unroll
-  for (int i = 0; i < FPL; ++i)
-    if (i < fv) nx.out[r * nx.ldo + f + i] = v[i];
-  if (!nx.z) return;
+    for (int i = 0; i < FPL; ++i)
+      if (i < fv) nx.out[r * nx.ldo + f + i] = v[i];
+  }
+  if (!nx.zq) return;
   double sq = 0.0;
 #pragma unroll
   for (int i = 0; i < FPL; ++i)
@@ -417,11 +419,11 @@ __device__ __forceinline__ void agnn_finalize(uint64_t r, const float (&o)[FPL],
   for (int o2 = 16; o2 > 0; o2 >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o2);
   const float inv = sq == 0.0 ? 0.0f : float(1.0 / sqrt(sq));
   if (sq == 0.0 && lane == 0) ++nz;
-  if (lane == 0) nx.norm[r] = float(sqrt(sq));
+  if (lane == 0 && nx.norm) nx.norm[r] = float(sqrt(sq));
 #pragma unroll
   for (int i = 0; i < FPL; ++i) {
     const float zz = i < fv ? v[i] * inv : 0.0f, hh = i < fv ? v[i] : 0.0f;
-    if (i < fv) nx.z[r * nx.ldq + f + i] = zz;
+    if (i < fv && nx.z) nx.z[r * nx.ldq + f + i] = zz;
     if constexpr (PREC == SGTK_FP32) {
       uint32_t a0, a1, b0, b1;
       split2(zz, a0, a1);
@@ -741,7 +743,7 @@ bool agnn_panel_supported(const sgtk_graph* g, uint64_t d, float beta) {
 // One AGNN layer.  z: l2-normalised input rows (raw fp32, n_cols x ldq);
 // zq/zq1/hq/hq1: MMA operand copies of z and of the input h (TF32: rounded;
 // FP32: hi / lo planes), stride ldq; h: the raw input rows (stride ldh).
-// Writes nx.out (n_rows x d) and, when nx.z is set, the next layer's z and
+// Writes nx.out (n_rows x d, when set) and, when nx.zq is set, the next layer's
 // operand copies (which must not alias the inputs).
 // Concurrent mode (default; SGTK_AGNN_SERIAL=1 turns it off): the dense
 // tensor-core kernel runs on the caller's stream while the CUDA-core kernel
@@ -761,8 +763,8 @@ void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, cons
       if (ldq == 32) launch_agnn_dense<32, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, st);
       else launch_agnn_dense<64, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, st);
     } else {
-      if (ldq == 32) launch_agnn_dense<32, SGTK_TF32>(v, pn.P, z, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, st);
-      else launch_agnn_dense<64, SGTK_TF32>(v, pn.P, z, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, st);
+      if (ldq == 32) launch_agnn_dense<32, SGTK_TF32>(v, pn.P, zq, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, st);
+      else launch_agnn_dense<64, SGTK_TF32>(v, pn.P, zq, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, st);
     }
   };
   auto rows = [&](cudaStream_t st, float* o_sp, float* l_sp, cudaStream_t st_final) {

@@ -180,12 +180,16 @@ void agnn_forward_panel(const sgtk_graph* g, const float* x, uint64_t ldx, uint6
     nx.ldq = ldq;
     nx.zeros = reinterpret_cast<unsigned long long*>(zeros);
     if (!last) {
-      nx.z = nxt[0];
       nx.zq = nxt[1];
-      nx.zq1 = nxt[2];
       nx.hq = nxt[3];
-      nx.hq1 = nxt[4];
-      nx.norm = norm[(l + 1) & 1];
+      if (prec == SGTK_FP32) {  // the FP32 kernels also read raw z, |h| and the lo planes
+        nx.z = nxt[0];
+        nx.zq1 = nxt[2];
+        nx.hq1 = nxt[4];
+        nx.norm = norm[(l + 1) & 1];
+      } else {
+        nx.out = nullptr;  // TF32: the next layer reads only the rounded copies
+      }
     }
     agnn_panel_layer(g, cur[0], cur[1], cur[2], cur[3], cur[4], ldq, norm[l & 1], d, betas[l], prec,
                      opart, lpart, seg_o, seg_l, osp, lsp, nx, s);

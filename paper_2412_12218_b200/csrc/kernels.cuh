@@ -45,9 +45,9 @@ bool spmm_panel_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64
 
 // AGNN layer on panels (agnn_panel.cu)
 struct AgnnNext {
-  float* out;         // layer output h'
+  float* out;         // layer output h' (nullptr: not needed, TF32 inner layers)
   uint64_t ldo;
-  float* z;           // next layer z (raw; nullptr on the last layer)
+  float* z;           // next layer z (raw; FP32 only, nullptr on the last layer)
   float* zq;          // next-layer MMA operand copies (TF32-rounded / hi planes)
   float* zq1;         //   lo planes (FP32)
   float* hq;
