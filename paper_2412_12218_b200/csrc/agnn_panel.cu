@@ -80,6 +80,7 @@ struct AgnnCfg {
   // of >= 4 slots; shallower rings compute S chunk by chunk (N = 32)
   static constexpr bool PAIR = NB >= 4;
   static constexpr uint32_t SG = PAIR ? 2 : 1;  // chunks per S group
+  static constexpr bool EARLY_S = PAIR && NB >= 6;
   static_assert(SMEM <= 227u * 1024u, "agnn panel smem");
 };
 
@@ -306,10 +307,16 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       };
       issue_s(0);
       for (uint32_t c = 0; c < nch; ++c) {
-        // S of the next group, issued at the group's last chunk (before its
-        // PV): its S buffer held group g - 1, whose P was waited for at the
-        // previous iteration; its gathers only need PV(c + 2 - NB) retired
-        if ((c % C::SG) == C::SG - 1 && c + 1 < nch) issue_s(c / C::SG + 1);
+        // S of the next group.  Its S buffer held group g - 1, whose last P
+        // was waited for at the previous iteration.  With a deep gather ring
+        // (EARLY_S) it goes at the group's first chunk -- the softmax then has
+        // a whole group of slack -- since its gathers only need PV(c + 2 - NB)
+        // retired; shallow rings issue it at the group's last chunk.
+        if constexpr (C::EARLY_S) {
+          if ((c % C::SG) == 0 && c + C::SG < nch) issue_s(c / C::SG + 1);
+        } else {
+          if ((c % C::SG) == C::SG - 1 && c + 1 < nch) issue_s(c / C::SG + 1);
+        }
         const uint32_t ds = c % C::NB, pslot = c % C::NP;
         const uint32_t g = c / C::FOLD, buf = g % C::NF;
         const bool first = (c % C::FOLD) == 0;
