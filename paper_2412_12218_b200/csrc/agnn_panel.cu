@@ -102,7 +102,11 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
                   long long* __restrict__ trace) {
   using C = AgnnCfg<DC, PREC>;
   auto mark = [&](uint32_t c, int ev) {
+#ifdef SGTK_TRACE  // pipeline event trace (tools/panel_debug.py); compiled out by default
     if (trace && blockIdx.x < 4 && c < 256) trace[((uint64_t(blockIdx.x) * 256 + c) * 8) + ev] = clock64();
+#else
+    (void)c, (void)ev, (void)trace;
+#endif
   };
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -681,6 +685,8 @@ void launch_agnn_dense(const PanelView& v, uint64_t P, const float* zraw, const 
     cudaFuncSetAttribute(agnn_dense_kernel<DC, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(227u * 1024u));
   });
+  // SGTK_PANEL_TRACE=<file>: per-chunk pipeline timestamps of the first 4
+  // CTAs (only in a build with -DSGTK_TRACE; otherwise the file is zeros)
   static long long* trace = [] {
     long long* t = nullptr;
     if (std::getenv("SGTK_PANEL_TRACE")) {

@@ -348,7 +348,11 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
   using C = PanelCfg<DC, PREC>;
   // optional timeline (SGTK_PANEL_TRACE): trace[(panel * 256 + chunk) * 8 + event]
   auto mark = [&](uint32_t c, int ev) {
+#ifdef SGTK_TRACE  // pipeline event trace (tools/panel_debug.py); compiled out by default
     if (trace && blockIdx.x < 4 && c < 256) trace[((uint64_t(blockIdx.x) * 256 + c) * 8) + ev] = clock64();
+#else
+    (void)c, (void)ev, (void)trace;
+#endif
   };
   extern __shared__ __align__(16) uint8_t smem_raw[];
   // 1024-aligned base, derived by offset so the compiler keeps the shared
@@ -825,6 +829,8 @@ bool launch_dense(const PanelView& v, uint64_t P, uint32_t max_entries, const fl
                          int(kSmemCap));
   });
   dim3 grid(unsigned(P), unsigned((d + DC - 1) / DC));
+  // SGTK_PANEL_TRACE=<file>: per-chunk pipeline timestamps of the first 4
+  // CTAs (only in a build with -DSGTK_TRACE; otherwise the file is zeros)
   static long long* trace = [] {
     long long* t = nullptr;
     if (std::getenv("SGTK_PANEL_TRACE")) {
