@@ -454,15 +454,18 @@ __device__ __forceinline__ void agnn_finalize(uint64_t r, const float (&o)[FPL],
 //   the batch's z_col rows (128/256 B each) go to a per-warp smem tile T by
 //     cp.async (TF32 mode reads the pre-rounded copy zq, so T is already the
 //     MMA-rounded operand);
-//   lane = edge: dot of T[e] with z_row (held in registers by every lane),
+//   lane = edge: dot of T[e] with z_row (tile row 32, a broadcast read),
 //     p = exp2(beta*log2e*s - |beta|*log2e), coefficient p * |h_col| in a
 //     register (h_col = z_col * |h_col|: z is h scaled to unit norm,
 //     gnn.cpp:74-91, so the aggregation needs no second gather);
 //   lane = feature: O[f] += coef_e * T[e][f] over the batch, e ascending,
 //     coef_e broadcast by shuffle.
 // Row sums l: per-lane partials, reduced by a fixed shuffle tree per item.
+#ifndef SGTK_ROWS_MINB
+#define SGTK_ROWS_MINB 5
+#endif
 template <int FPL, int PREC, bool SPLIT>
-__global__ void __launch_bounds__(FPL == 1 ? 256 : 128)
+__global__ void __launch_bounds__(FPL == 1 ? 256 : 128, FPL == 1 ? SGTK_ROWS_MINB : 2 * SGTK_ROWS_MINB)
 agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2* __restrict__ sent,
                  const float* __restrict__ zown, const float* __restrict__ z, uint64_t ld,
                  const float* __restrict__ norm,
@@ -472,7 +475,7 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
                  AgnnNext nx) {
   constexpr int DC = 32 * FPL;
   constexpr int TS = DC + 4;  // smem tile row stride (floats): 16-byte rows, spread banks
-  __shared__ __align__(16) float tile[FPL == 1 ? 8 : 4][32 * TS];
+  __shared__ __align__(16) float tile[FPL == 1 ? 8 : 4][33 * TS];  // 32 z_col rows + z_row
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float* T = tile[wib];
   const uint32_t tb = smem_u32(T);
@@ -487,13 +490,10 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
     const uint64_t r = w.x;
     const bool direct = w.w == 0xFFFFFFFFu;
     const uint32_t c_first = w.y < w.z && lane < min(32u, w.z - w.y) ? sent[w.y + lane].x : 0u;
-    float zr[DC];  // z of the row, every lane (dot products run lane = edge)
-    const float4* zrow = reinterpret_cast<const float4*>(zown + (row_offset + r) * ld);
-#pragma unroll
-    for (int k = 0; k < DC / 4; ++k) {
-      const float4 v = __ldg(zrow + k);  // padding features are zeros
-      zr[4 * k] = v.x; zr[4 * k + 1] = v.y; zr[4 * k + 2] = v.z; zr[4 * k + 3] = v.w;
-    }
+    // z of the row -> tile row 32 (read back as a broadcast by every lane;
+    // lands with the first batch's gathers); padding features are zeros
+    if (w.y < w.z && lane < uint32_t(DC / 4))
+      cp_async16(tb + (32 * TS + 4 * lane) * 4, zown + (row_offset + r) * ld + 4 * lane);
     float o[FPL], lpp = 0.0f;
 #pragma unroll
     for (int i = 0; i < FPL; ++i) o[i] = (!SPLIT && direct && i < fv) ? opart[r * DC + f + i] : 0.0f;
@@ -521,10 +521,11 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
 #pragma unroll
         for (int k = 0; k < DC / 4; ++k) {
           const float4 v = ld_shared_f4(tb + (lane * TS + 4 * k) * 4);
-          s = fmaf(zr[4 * k], v.x, s);
-          s = fmaf(zr[4 * k + 1], v.y, s);
-          s = fmaf(zr[4 * k + 2], v.z, s);
-          s = fmaf(zr[4 * k + 3], v.w, s);
+          const float4 q = ld_shared_f4(tb + (32 * TS + 4 * k) * 4);
+          s = fmaf(q.x, v.x, s);
+          s = fmaf(q.y, v.y, s);
+          s = fmaf(q.z, v.z, s);
+          s = fmaf(q.w, v.w, s);
           if constexpr (PREC == SGTK_TF32) {
             n2 = fmaf(v.x, v.x, n2);
             n2 = fmaf(v.y, v.y, n2);
