@@ -657,7 +657,8 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
 // Sparse part on the CUDA cores: one warp per work item (a row's sparse
 // edges, or a <= kSegEdges segment of a hub row), lanes over features
 // (FPL = 1 or 2 consecutive floats per lane: 128- or 256-byte coalesced
-// rows), 8 edges' rows in flight per warp, edges of a batch broadcast by
+// rows), BATCH / EPI edge rows in flight per lane (small batches keep
+// registers low enough for 4 blocks per SM), edges of a batch broadcast by
 // shuffle.  Direct items continue the row's sum from the dense result in
 // `out` (out = dense + e0 + e1 + ...); segments write partials that
 // long_rows_kernel adds in segment order.  Deterministic throughout.
@@ -672,6 +673,14 @@ sparse_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint
   // instruction -> 4 MACs per lane per edge, 4x fewer instructions than
   // lane = feature; the EPI partial sums merge by a fixed shuffle tree
   constexpr uint32_t DC = 32 * FPL, LPE = DC / 4, EPI = 32 / LPE;
+#ifndef SGTK_SPARSE_BATCH1
+#define SGTK_SPARSE_BATCH1 16
+#endif
+#ifndef SGTK_SPARSE_BATCH2
+#define SGTK_SPARSE_BATCH2 8
+#endif
+  // edges per batch (loads in flight per warp: BATCH / EPI float4 per lane)
+  constexpr uint32_t BATCH = FPL == 1 ? uint32_t(SGTK_SPARSE_BATCH1) : uint32_t(SGTK_SPARSE_BATCH2);
   const uint32_t lane = threadIdx.x & 31, sub = lane / LPE, jq = lane % LPE;
   const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -688,14 +697,14 @@ sparse_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[i] = i < fv ? dst[i] : 0.0f;
     }
-    for (uint32_t e = w.y; e < w.z; e += 32) {
-      const uint32_t cnt = min(32u, w.z - e);
+    for (uint32_t e = w.y; e < w.z; e += BATCH) {
+      const uint32_t cnt = min(BATCH, w.z - e);
       uint2 en = lane < cnt ? sent[e + lane] : make_uint2(0u, 0u);
       if constexpr (PREC == SGTK_TF32) en.y = tf32_op(__uint_as_float(en.y));  // x arrives pre-rounded
-      float4 xv[32 / EPI];
-      float av[32 / EPI];
+      float4 xv[BATCH / EPI];
+      float av[BATCH / EPI];
 #pragma unroll
-      for (uint32_t k = 0; k < 32 / EPI; ++k) {
+      for (uint32_t k = 0; k < BATCH / EPI; ++k) {
         const uint32_t u = k * EPI + sub;
         const uint32_t c = __shfl_sync(0xFFFFFFFFu, en.x, u);
         av[k] = __uint_as_float(__shfl_sync(0xFFFFFFFFu, en.y, u));
@@ -711,7 +720,7 @@ sparse_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint
         if (u >= cnt) av[k] = 0.0f;
       }
 #pragma unroll
-      for (uint32_t k = 0; k < 32 / EPI; ++k) {
+      for (uint32_t k = 0; k < BATCH / EPI; ++k) {
         acc[0] = fmaf(av[k], xv[k].x, acc[0]);
         acc[1] = fmaf(av[k], xv[k].y, acc[1]);
         acc[2] = fmaf(av[k], xv[k].z, acc[2]);
