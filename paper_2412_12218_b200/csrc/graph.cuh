@@ -51,7 +51,6 @@ struct Windows {
 constexpr int kPanelRows = 128;
 constexpr int kChunkCols = 32;
 constexpr uint32_t kDenseMin = 2;
-constexpr uint32_t kEntrySkip = 0x1000u;  // padding entry marker (bit 12)
 constexpr uint32_t kSegEdges = 512;       // sparse edges per CUDA-core work item
 
 struct Panels {
@@ -60,7 +59,7 @@ struct Panels {
   std::shared_ptr<DevBuf> cptr;   // u32[P+1]   first chunk of panel p
   std::shared_ptr<DevBuf> dcols;  // u32[32*n_chunks] dense column ids (pad 0xFFFFFFFF)
   std::shared_ptr<DevBuf> coff;   // u64[n_chunks+1] entry range of a chunk (multiple of 4)
-  std::shared_ptr<DevBuf> dent;   // u32[n_dent]  tf32(value) | skip<<12 | row<<5 | k
+  std::shared_ptr<DevBuf> dent;   // u32[n_dent]  tf32(value) | swizzled A-tile word offset
   std::shared_ptr<DevBuf> dval;   // f32[n_dent]  full fp32 value
   std::shared_ptr<DevBuf> deid;   // u32[n_dent]  CSR edge id (0xFFFFFFFF for padding)
   std::shared_ptr<DevBuf> dmask;  // u32[n_chunks * 128] row r's edge bits in the chunk (AGNN)

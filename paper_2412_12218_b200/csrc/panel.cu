@@ -113,11 +113,18 @@ __global__ void fill_u32_kernel(uint32_t* __restrict__ p, uint64_t n, uint32_t v
     p[i] = v;
 }
 
-// Packed entry: tf32(value) in bits 31..13 (RNE, tf32_round_value), row in
-// the panel in bits 11..5, column in the chunk in bits 4..0.  The position
-// within a chunk is unique, so the (atomic) slot order never affects results.
+// Word offset of A element (row, k) in a chunk's K-major SWIZZLE_128B TF32
+// tile: 8-row core groups of 1 KB, 128-byte rows, 16-byte units XOR (row % 8).
+__host__ __device__ __forceinline__ uint32_t a_word(uint32_t row, uint32_t k) {
+  return (row >> 3) * 256u + (row & 7u) * 32u + (((k >> 2) ^ (row & 7u)) << 2) + (k & 3u);
+}
+// Packed entry: tf32(value) in bits 31..13 (RNE, tf32_round_value), the
+// element's word offset in the swizzled A tile in bits 11..0 (a_word), so a
+// builder stores it with one mask and one address add.  Padding entries
+// (chunk sizes round up to 4) are value 0 at a position the chunk leaves
+// empty: storing them is a no-op on the zeroed tile.
 __device__ __forceinline__ uint32_t pack_entry(float v, uint32_t row, uint32_t k) {
-  return (__float_as_uint(tf32_rne(v)) & 0xFFFFE000u) | (row << 5) | k;
+  return (__float_as_uint(tf32_rne(v)) & 0xFFFFE000u) | a_word(row, k);
 }
 
 // Row masks straight from the edges: bit k of dmask[chunk][row] <=> edge
@@ -189,6 +196,32 @@ __global__ void entry_fill_sorted_kernel(const uint32_t* __restrict__ e2r, const
 
 
 
+// Padding entries of a chunk: value 0 at the first position with no edge
+// (a chunk with all 4096 positions taken has no padding).  Warp per chunk.
+__global__ void entry_pad_kernel(const uint32_t* __restrict__ ccnt, const uint64_t* __restrict__ coff,
+                                 const uint32_t* __restrict__ dmask, uint64_t nc,
+                                 uint32_t* __restrict__ dent) {
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t c = warp; c < nc; c += nw) {
+    const uint64_t b = coff[c] + ccnt[c], e = coff[c + 1];
+    if (b == e) continue;
+    uint32_t row = 0, k = 0;
+    for (uint32_t r0 = 0; r0 < kPanelRows; r0 += 32) {
+      const uint32_t m = dmask[c * kPanelRows + r0 + lane];
+      const uint32_t open = __ballot_sync(0xFFFFFFFFu, m != 0xFFFFFFFFu);
+      if (open) {
+        const uint32_t src = __ffs(open) - 1;
+        row = r0 + src;
+        k = __ffs(~__shfl_sync(0xFFFFFFFFu, m, src)) - 1;
+        break;
+      }
+    }
+    if (b + lane < e) dent[b + lane] = a_word(row, k);
+  }
+}
+
 // sparse (CUDA-core) edges: per-row count, then per-row stable compaction
 __global__ void sparse_count_kernel(const uint64_t* __restrict__ np, uint64_t n,
                                     const uint32_t* __restrict__ e2c, const uint64_t* __restrict__ wo,
@@ -244,7 +277,7 @@ __global__ void repack_dense_kernel(const uint32_t* __restrict__ dent, const uin
       dval_o[i] = 0.0f;
     } else {
       const float v = ev[e];
-      dent_o[i] = pack_entry(v, (w >> 5) & 127u, w & 31u);
+      dent_o[i] = (__float_as_uint(tf32_rne(v)) & 0xFFFFE000u) | (w & 0xFFFu);
       dval_o[i] = v;
     }
   }
@@ -529,40 +562,33 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
       if (lane == 0) mark(c, 2);
       if constexpr (C::GW > 1) named_bar(1 + grp, GT);
       else __syncwarp();
-      // Scatter: each lane takes 4 consecutive entries (one 16-byte LDS),
-      // branch-free: padding entries land on a scratch word.
+      // Scatter: each lane takes 4 consecutive entries (one 16-byte LDS);
+      // the entry carries its swizzled tile offset (pack_entry), padding
+      // entries store 0 on an empty position.
       const uint32_t ent = smem_u32(dring + ds * L.dslot);
       const uint32_t dv = smem_u32(dring + (ND + ds) * L.dslot);
-      const uint32_t junk = smem_u32(tmem_slot + 1);
       for (uint32_t i0 = gl * 4; i0 < ne; i0 += GT * 4 * 4) {
-        uint4 w4[4];
-        float4 v4[4];
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           const uint32_t i = i0 + h * GT * 4;
-          w4[h] = i < ne ? ld_shared_u4(ent + i * 4) : make_uint4(kEntrySkip, kEntrySkip, kEntrySkip, kEntrySkip);
-          if constexpr (PREC == SGTK_FP32)
-            v4[h] = i < ne ? ld_shared_f4(dv + i * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+          if (i >= ne) break;  // ne is a multiple of 4: whole uint4 groups
+          const uint4 w4 = ld_shared_u4(ent + i * 4);
+          const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
+          if constexpr (PREC == SGTK_FP32) {
+            const float4 v4 = ld_shared_f4(dv + i * 4);
+            const float vs[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const uint32_t ws[4] = {w4[h].x, w4[h].y, w4[h].z, w4[h].w};
-          const float vs[4] = {v4[h].x, v4[h].y, v4[h].z, v4[h].w};
-#pragma unroll
-          for (int k4 = 0; k4 < 4; ++k4) {
-            const uint32_t w = ws[k4];
-            const uint32_t row = (w >> 5) & 127u, k = w & 31u;
-            const uint32_t off = (row >> 3) * 1024u + (row & 7u) * 128u +
-                                 (((k >> 2) ^ (row & 7u)) << 4) + (k & 3u) * 4u;
-            const bool skip = (w & kEntrySkip) != 0;
-            if constexpr (PREC == SGTK_FP32) {
+            for (int k4 = 0; k4 < 4; ++k4) {
+              const uint32_t off = (ws[k4] & 0xFFFu) * 4u;
               uint32_t s0, s1;
               split2(vs[k4], s0, s1);
-              st_shared_u32(skip ? junk : abase + off, s0);
-              st_shared_u32(skip ? junk : abase + C::A_BYTES + off, s1);
-            } else {
-              st_shared_u32(skip ? junk : abase + off, w & 0xFFFFE000u);
+              st_shared_u32(abase + off, s0);
+              st_shared_u32(abase + C::A_BYTES + off, s1);
             }
+          } else {
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4)
+              st_shared_u32(abase + (ws[k4] & 0xFFFu) * 4u, ws[k4] & 0xFFFFE000u);
           }
         }
       }
@@ -972,7 +998,6 @@ void build_panels(sgtk_graph& g, cudaStream_t s) {
   pn->dent = std::make_shared<DevBuf>(ND * 4);
   pn->dval = std::make_shared<DevBuf>(ND * 4);
   pn->deid = std::make_shared<DevBuf>(ND * 4);
-  fill_u32_kernel<<<grid_for(ND, 256), 256, 0, s>>>(pn->dent->as<uint32_t>(), ND, kEntrySkip);
   CU(cudaMemsetAsync(pn->dval->p, 0, ND * 4, s));
   CU(cudaMemsetAsync(pn->deid->p, 0xFF, ND * 4, s));
   const float* vals = g.has_values ? g.vals->as<float>() : nullptr;
@@ -982,6 +1007,11 @@ void build_panels(sgtk_graph& g, cudaStream_t s) {
         pn->coff->as<uint64_t>(), pn->dmask->as<uint32_t>(), rowoff.as<uint16_t>(), vals, E,
         pn->dent->as<uint32_t>(), pn->dval->as<float>(), pn->deid->as<uint32_t>());
   CU_LAUNCH("entry_fill_sorted_kernel");
+  if (NC)
+    entry_pad_kernel<<<grid_for(NC * 32, 256), 256, 0, s>>>(ccnt.as<uint32_t>(), pn->coff->as<uint64_t>(),
+                                                           pn->dmask->as<uint32_t>(), NC,
+                                                           pn->dent->as<uint32_t>());
+  CU_LAUNCH("entry_pad_kernel");
 
   DevBuf scnt((n + 1) * 4);
   CU(cudaMemsetAsync(scnt.p, 0, (n + 1) * 4, s));

@@ -183,8 +183,9 @@ def test_panel_agnn_deterministic_and_fallback():
 def _panel_restatement(g):
     """numpy restatement of build_panels (panel.cu): per 128-row panel the
     columns with >= 2 edges are dense (sorted, padded to 32 per panel), a
-    chunk's entries in (row, column) order, row masks, row offsets, sparse
-    edges per row in CSR order."""
+    chunk's entries in (row, column) order (each carrying its swizzled A-tile
+    offset, padded to a multiple of 4 with zeros on empty positions), row
+    masks, sparse edges per row in CSR order."""
     n = g.num_nodes
     npz = g.node_pointer.astype(np.int64)
     el = g.edge_list.astype(np.int64)
@@ -226,12 +227,20 @@ def test_panel_format_matches_restatement(name, g):
     np.testing.assert_array_equal(A["chunk_ptr"], cptr)
     np.testing.assert_array_equal(A["dense_cols"].astype(np.uint64), dcols)
     off = A["chunk_off"].astype(np.int64)
+    def pos(w):  # swizzled K-major A-tile word offset (panel.cu a_word) -> (row, k)
+        o = int(w) & 0xFFF
+        row = (o >> 8) * 8 + ((o >> 5) & 7)
+        return row, ((((o & 31) >> 2) ^ (row & 7)) << 2) | (o & 3)
     for c, want in enumerate(ents):
         got = A["dense_entries"][off[c]:off[c + 1]]
-        got = got[(got & 0x1000) == 0]
-        assert [((w >> 5) & 127, w & 31) for w in got] == [(r, k) for r, k, _ in want], c
+        assert len(got) == (len(want) + 3) // 4 * 4, c
+        real, pad = got[:len(want)], got[len(want):]
+        assert [pos(w) for w in real] == [(r, k) for r, k, _ in want], c
         tf = np.array([O.tf32_round_value(float(v)) for _, _, v in want], np.float32)
-        np.testing.assert_array_equal((got & 0xFFFFE000).view(np.float32), tf)
+        np.testing.assert_array_equal((real & 0xFFFFE000).view(np.float32), tf)
+        taken = {(r, k) for r, k, _ in want}
+        for w in pad:  # value 0 on an empty position
+            assert int(w) & 0xFFFFE000 == 0 and pos(w) not in taken, c
     sp = A["sparse_ptr"].astype(np.int64)
     se = A["sparse_entries"].reshape(-1, 2)
     for r in range(g.num_nodes):
