@@ -107,12 +107,6 @@ __device__ __forceinline__ bool dense_slot(const uint32_t* __restrict__ e2r,
 }
 
 
-__global__ void fill_u32_kernel(uint32_t* __restrict__ p, uint64_t n, uint32_t v) {
-  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x)
-    p[i] = v;
-}
-
 // Word offset of A element (row, k) in a chunk's K-major SWIZZLE_128B TF32
 // tile: 8-row core groups of 1 KB, 128-byte rows, 16-byte units XOR (row % 8).
 __host__ __device__ __forceinline__ uint32_t a_word(uint32_t row, uint32_t k) {
