@@ -24,7 +24,8 @@
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
 //               (M = 128 rows, N = feature slice, K = 8 per instruction);
 //               groups of kFold chunks rotate over TMEM accumulators
-//   warps 2-5   A-tile builders: zero the K-major SWIZZLE_128B A tile,
+//   warps 2-5   A-tile builders: zero the K-major SWIZZLE_128B A tile (a
+//               bulk copy of zeros by the TMA engine),
 //               scatter the chunk's entries (pos | tf32 value packed in one
 //               u32), TF32-round / FP32-split the B tile, fence, arrive
 //   warps 6-9   accumulators, thread per row: sparse edges on CUDA cores in
@@ -345,6 +346,8 @@ struct PanelSmem {
 // Source of the zero rows that pad a panel's last chunk (cp.async needs a
 // global address; 256 B covers a 64-feature slice).
 __device__ __align__(16) float g_zero_row[64];
+// Zeros for an A stage (up to 2 planes x 16 KB), copied in by the TMA engine.
+__device__ __align__(128) uint32_t g_zero_tile[2 * kPanelRows * kChunkCols];
 
 // ---------------------------------------------------------------------------
 // Dense part on the tensor cores: out[rows of panel] = A_dense * x (a store:
@@ -386,8 +389,8 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
   // address space (LDS/STS rather than generic loads)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // A stage built
-  uint64_t* empty = full + C::NS;                       // A stage consumed
-  uint64_t* bfull = empty + C::NS;                      // B tile landed
+  uint64_t* zfull = full + C::NS;                       // A stage zeroed (copy engine)
+  uint64_t* bfull = zfull + C::NS;                      // B tile landed
   uint64_t* bempty = bfull + kMaxND;                    // B tile + entry slot consumed
   uint64_t* dfull = bempty + kMaxND;                    // entries landed
   uint64_t* accfull = dfull + kMaxND;
@@ -408,7 +411,7 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NS; ++i) {
       mbar_init(full + i, C::GW);  // the builder warps that own the chunk
-      mbar_init(empty + i, 1);     // tcgen05.commit
+      mbar_init(zfull + i, 1);     // bulk copy of zeros (expect_tx)
     }
     for (uint32_t i = 0; i < ND; ++i) {
       mbar_init(bfull + i, 32 * C::GW);  // cp.async.mbarrier.arrive.noinc per gathering lane
@@ -503,8 +506,9 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
     // ------------------------------------------------------------ A builders
     // Builder group c % NS owns chunk c: it gathers the chunk's B tile (PD =
     // nd - NS chunks ahead, cp.async with completion signalled by the copy
-    // engine), zeroes and fills the A tile from the staged entries, and (FP32)
-    // splits B into TF32 planes.  NS chunks are in construction at once.
+    // engine), has the TMA engine zero the A tile, scatters the staged
+    // entries into it, and (FP32) splits B into TF32 planes.  NS chunks are
+    // in construction at once.
     const uint32_t b = warp - 2, grp = b % C::NS, sub = b / C::NS;
     const uint32_t gl = sub * 32 + lane;  // thread index inside the chunk's group
     constexpr uint32_t GT = C::GW * 32;
@@ -546,12 +550,14 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
         const uint32_t cp = c - C::NS;
         mbar_wait(bempty + cp % ND, (cp / ND) & 1u);
       }
+      if (gl == 0) {  // the copy engine zeroes the stage (no store loop here)
+        mbar_expect_tx(zfull + s, C::A_STAGE);
+        bulk_load(ring + s * C::A_STAGE, g_zero_tile, C::A_STAGE, zfull + s);
+      }
       if (lane == 0) mark(c, 1);
       if (c + PD < nch) gather_b(c + PD, idn);
       idn = id_of(c + PD + C::NS);
-#pragma unroll 8
-      for (uint32_t i = gl; i < C::PA * C::A_BYTES / 16; i += GT)
-        st_shared_v4(abase + i * 16, 0u, 0u, 0u, 0u);
+      mbar_wait(zfull + s, ph);
       mbar_wait(dfull + ds, dph);
       if (lane == 0) mark(c, 2);
       if constexpr (C::GW > 1) named_bar(1 + grp, GT);
