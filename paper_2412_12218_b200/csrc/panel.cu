@@ -26,8 +26,8 @@
 //               groups of kFold chunks rotate over TMEM accumulators
 //   warps 2-5   A-tile builders: zero the K-major SWIZZLE_128B A tile (a
 //               bulk copy of zeros by the TMA engine),
-//               scatter the chunk's entries (pos | tf32 value packed in one
-//               u32), TF32-round / FP32-split the B tile, fence, arrive
+//               scatter the chunk's entries (tf32 value | tile offset packed
+//               in one u32), FP32-split the B tile, fence, arrive
 //   warps 6-9   accumulators, thread per row: sparse edges on CUDA cores in
 //               fp32 registers; fold every finished TMEM accumulator group
 //               into the same registers (IEEE adds: TC accumulation chains
@@ -362,10 +362,11 @@ __device__ __align__(128) uint32_t g_zero_tile[2 * kPanelRows * kChunkCols];
 //               rows, N = feature slice, K = 8 per instruction); groups of
 //               FOLD chunks rotate over 512/DC TMEM accumulators
 //   warps 2-5   A-tile builders: chunk c is built by the warp group c % NS,
-//               so NS chunks are in construction at once: zero the K-major
-//               SWIZZLE_128B A tile, scatter the entries (tf32 value | row |
-//               column packed in one u32), FP32: split A and B into TF32
-//               planes; fence.proxy.async, arrive
+//               so NS chunks are in construction at once: the TMA engine
+//               zeroes the K-major SWIZZLE_128B A tile, the group scatters
+//               the entries (tf32 value | swizzled tile offset in one u32),
+//               FP32: splits A and B into TF32 planes; fence.proxy.async,
+//               arrive
 //   warps 6-9   accumulators, thread per row: fold each finished TMEM group
 //               into fp32 registers in group order (IEEE adds keep every
 //               tensor-core accumulation chain <= FOLD chunks), store.
