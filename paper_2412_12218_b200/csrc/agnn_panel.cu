@@ -57,15 +57,16 @@ struct AgnnCfg {
   static constexpr uint32_t M_BYTES = kPanelRows * 4;       // row masks
   static constexpr uint32_t P_BYTES = kPanelRows * kChunkCols * 4;  // 16 KB
   static constexpr int KB = DC / 32;                       // 128-byte K blocks of z
-  static constexpr int NB = F32 ? (DC == 32 ? 4 : 2) : 6;  // gather ring (even: S pairs)
-  static constexpr int NP = 2;                             // P ring
-  // TMEM: 2 S buffers x 64 columns (S of a chunk pair, N = 64 costs what
-  // N = 32 does), NF O accumulators x DC; 256 columns -> 2 CTAs per SM
-  // TF32, DC = 32: P goes from the softmax threads' registers straight into
-  // TMEM (tcgen05.st) and PV reads A from TMEM (no shared-memory P tile)
+  // TMEM: NSB S buffers x 64 columns (S of a chunk pair, N = 64 costs what
+  // N = 32 does), NF O accumulators x DC; 256 columns -> 2 CTAs per SM.
+  // TF32, DC = 32 (PT): P goes from the softmax threads' registers straight
+  // back over its own S columns (tcgen05.st) and PV reads A from there -- no
+  // P tile, no P slot to wait for; three S buffers instead of two + P slots.
   static constexpr bool PT = !F32 && DC == 32;
-  static constexpr uint32_t P_COL = 128;                // P[NP] x 32 columns (PT)
-  static constexpr uint32_t O_COL = PT ? 192 : 128;
+  static constexpr int NSB = PT ? 3 : 2;                   // S buffers (chunk pairs)
+  static constexpr int NB = F32 ? (DC == 32 ? 4 : 2) : (PT ? 8 : 6);  // gather ring (even: S pairs)
+  static constexpr int NP = PT ? 4 : 2;  // P slots in smem; PT: pfull barriers only
+  static constexpr uint32_t O_COL = NSB * 64;
   static constexpr int NF = PT ? 2 : (DC == 32 ? 4 : 2);
   static constexpr uint32_t TMEM_COLS = 256;
   static constexpr uint32_t FOLD = 4;
@@ -74,7 +75,7 @@ struct AgnnCfg {
   static constexpr uint32_t H_OFF = Z_OFF + PZ * KB * NB * 4096;      // [PH][NB] x T_BYTES
   static constexpr uint32_t M_OFF = H_OFF + PH * NB * T_BYTES;        // [NB] x 512 B
   static constexpr uint32_t P_OFF = (M_OFF + NB * M_BYTES + 1023) / 1024 * 1024;
-  static constexpr uint32_t SMEM = P_OFF + NP * PP * P_BYTES + 1024;
+  static constexpr uint32_t SMEM = P_OFF + (PT ? 0 : NP * PP * P_BYTES) + 1024;
   static_assert(NB % 2 == 0, "S pairs need an even gather ring");
   // S of a chunk pair needs both chunks' gathers while PV still lags: a ring
   // of >= 4 slots; shallower rings compute S chunk by chunk (N = 32)
@@ -112,8 +113,8 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bfull = reinterpret_cast<uint64_t*>(smem);  // [NB] gathers landed
   uint64_t* bempty = bfull + C::NB;                     // [NB] PV(c) retired: slot + P(c) free
-  uint64_t* sfull = bempty + C::NB;                     // [2]  S of chunk pair in TMEM
-  uint64_t* pfull = sfull + 2;                          // [NP] P(c) written
+  uint64_t* sfull = bempty + C::NB;                     // [NSB] S of chunk pair in TMEM
+  uint64_t* pfull = sfull + C::NSB;                     // [NP] P(c) written
   uint64_t* qfull = pfull + C::NP;                      // [1]  Q operand ready
   uint64_t* accfull = qfull + 1;                        // [NF]
   uint64_t* accempty = accfull + C::NF;                 // [NF]
@@ -136,7 +137,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       mbar_init(bfull + i, 32);  // cp.async.mbarrier.arrive.noinc, one per loader lane
       mbar_init(bempty + i, 1);
     }
-    for (int i = 0; i < 2; ++i) mbar_init(sfull + i, 1);
+    for (int i = 0; i < C::NSB; ++i) mbar_init(sfull + i, 1);
     for (int i = 0; i < C::NP; ++i) mbar_init(pfull + i, 4);
     mbar_init(qfull, 4);
     for (int i = 0; i < C::NF; ++i) {
@@ -150,7 +151,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t s_col = 0, o_col = C::O_COL;  // TMEM: S[2] x 64, (P[NP] x 32), O[NF] x DC
+  const uint32_t s_col = 0, o_col = C::O_COL;  // TMEM: S[NSB] x 64 (PT: P over S), O[NF] x DC
 
   if (warp < 4) {
     // ------------------------------------------------------------ softmax
@@ -182,7 +183,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
     const uint32_t pb = smem_u32(ps);
     for (uint32_t c = 0; c < nch; ++c) {
       const uint32_t sgi = c / C::SG;  // S group of the chunk
-      const uint32_t sb = sgi & 1u, sph = (sgi >> 1) & 1u, shalf = (c % C::SG) * 32;
+      const uint32_t sb = sgi % C::NSB, sph = (sgi / C::NSB) & 1u, shalf = (c % C::SG) * 32;
       const uint32_t ds = c % C::NB, dph = (c / C::NB) & 1u;
       const uint32_t pslot = c % C::NP;
       mbar_wait(bfull + ds, dph);  // row masks of the chunk
@@ -208,18 +209,18 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       }
       l += (lq[0] + lq[1]) + (lq[2] + lq[3]);
       if (warp == 0 && lane == 0) mark(c, 5);
-      if (c >= uint32_t(C::NP)) {  // PV(c - NP) done with this P slot
-        const uint32_t cp = c - C::NP;
-        mbar_wait(bempty + cp % C::NB, (cp / C::NB) & 1u);
-      }
-      if constexpr (C::PT) {
-        tmem_st32(tmem + ((warp * 32u) << 16) + C::P_COL + pslot * 32, *reinterpret_cast<uint32_t(*)[32]>(pr));
+      if constexpr (C::PT) {  // P over this chunk's S columns (already read)
+        tmem_st32(tmem + ((warp * 32u) << 16) + s_col + sb * 64 + shalf, *reinterpret_cast<uint32_t(*)[32]>(pr));
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (warp == 0 && lane == 0) mark(c, 2);
         if (lane == 0) mbar_arrive(pfull + pslot);
         continue;
+      }
+      if (c >= uint32_t(C::NP)) {  // PV(c - NP) done with this P slot
+        const uint32_t cp = c - C::NP;
+        mbar_wait(bempty + cp % C::NB, (cp / C::NB) & 1u);
       }
       const uint32_t pt = pb + pslot * C::PP * C::P_BYTES;
 #pragma unroll
@@ -287,12 +288,16 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       // tiles of ring slots 2k and 2k+1 are adjacent rows of one K-major tile
       auto issue_s = [&](uint32_t g) {
         const uint32_t c = C::SG * g;
+        if (C::PT && g >= uint32_t(C::NSB)) {  // PV of the buffer's previous group read its P
+          const uint32_t cl = C::SG * (g - C::NSB) + C::SG - 1;
+          mbar_wait(bempty + cl % C::NB, (cl / C::NB) & 1u);
+        }
         mbar_wait(bfull + c % C::NB, (c / C::NB) & 1u);
         if (C::PAIR && c + 1 < nch) mbar_wait(bfull + (c + 1) % C::NB, ((c + 1) / C::NB) & 1u);
         fence_async_smem();  // cp.async (generic proxy) -> MMA (async proxy)
         tc_fence_after();
         const uint32_t s0 = c % C::NB;
-        const uint32_t dt = tmem + s_col + (g & 1u) * 64;
+        const uint32_t dt = tmem + s_col + (g % C::NSB) * 64;
 #pragma unroll
         for (uint32_t ks = 0; ks < DC / 8; ++ks) {
           const uint32_t ko = (ks >> 2) * 16384u + (ks & 3u) * 32u;  // Q: 128-row K blocks
@@ -306,7 +311,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
             umma_tf32(dt, q0, z0, id_s, ks ? 1u : 0u);
           }
         }
-        umma_commit(sfull + (g & 1u));
+        umma_commit(sfull + g % C::NSB);
         mark(c, 0);
       };
       issue_s(0);
@@ -335,7 +340,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
           const uint32_t acc = (first && ks == 0) ? 0u : 1u;
           const uint64_t p0 = umma_desc(pt + ks * 32), h0 = desc_mn32(ht + ks * 1024, 4096, 512);
           if constexpr (C::PT) {
-            umma_tf32_ts(dt, tmem + C::P_COL + pslot * 32 + ks * 8, h0, id_o, acc);
+            umma_tf32_ts(dt, tmem + s_col + ((c / C::SG) % C::NSB) * 64 + (c % C::SG) * 32 + ks * 8, h0, id_o, acc);
           } else if constexpr (C::F32) {
             umma_tf32(dt, p0, desc_mn32(ht + C::NB * C::T_BYTES + ks * 1024, 4096, 512), id_o, acc);
             umma_tf32(dt, umma_desc(pt + C::P_BYTES + ks * 32), h0, id_o, 1u);
