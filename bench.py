@@ -228,6 +228,30 @@ def reference_layer_sample(g, h0, beta=1.0, threads=0):
     return layer, kind, cores
 
 
+def reference_gcn_sample(g, x, dims, threads=0):
+    """The GCN layers through the reference's public API (gcn_normalize_values,
+    then gcn_forward on its transform); returns (run, kind, cores)."""
+    from oracle.oracle import Csr
+
+    c = Csr.of(g.num_nodes, g.node_pointer, g.edge_list)
+    cores = threads or os.cpu_count()
+    rng = np.random.default_rng(5)
+    layers = [((rng.standard_normal((a, b)) / np.sqrt(a)).astype(np.float32), i + 1 < len(dims) - 1)
+              for i, (a, b) in enumerate(zip(dims[:-1], dims[1:]))]
+    try:
+        from oracle.oracle import RefLib
+
+        R = RefLib()
+        th = R.transform_handle(R.gcn_normalize_values(c), 16, 8, threads)
+        return (lambda: R.gcn_forward(th, g.num_nodes, x, layers, threads=threads)), "reference", cores
+    except FileNotFoundError:
+        from oracle.oracle import Oracle
+
+        O = Oracle()
+        cn = O.gcn_normalize_values(c)
+        return (lambda: O.gcn_forward(cn, x, layers)), "port", cores
+
+
 def run_reference_arm(args, wl):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -235,27 +259,33 @@ def run_reference_arm(args, wl):
     import paper_2412_12218_b200 as sg
 
     g, gen = make_graph(wl, args.locality)
-    if wl["kind"] != "agnn":
-        raise SystemExit("--impl reference implemented for the AGNN workloads")
-    h0 = sg.dense_random(g.num_nodes, wl["hidden"], 17, -1.0, 1.0)
-    layer, kind, cores = reference_layer_sample(g, h0)
+    if wl["kind"] == "agnn":
+        h0 = sg.dense_random(g.num_nodes, wl["hidden"], 17, -1.0, 1.0)
+        layer, kind, cores = reference_layer_sample(g, h0)
+        per, what = 1, f"one full-size AGNN layer (d={wl['hidden']})"
+    else:  # GCN: the whole gcn_forward per step, reported per layer
+        L = wl["layers"]
+        dims = [wl["d_in"]] + [wl["hidden"]] * (L - 1) + [wl["d_out"]]
+        x0 = sg.dense_random(g.num_nodes, dims[0], 17, -1.0, 1.0)
+        layer, kind, cores = reference_gcn_sample(g, x0, dims)
+        per, what = L, f"gcn_forward ({L} layers, {dims}) / {L}"
+    steps = max(1, min(args.steps, 5))
     for _ in range(min(args.warmup, 1)):
         layer()
-    steps = max(1, min(args.steps, 5))
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
         layer()
-        times.append((time.perf_counter() - t0) * 1e3)
+        times.append((time.perf_counter() - t0) * 1e3 / per)
     ms = statistics.median(times)
     line = {
         "impl": "reference", "metric": metric_name(wl), "value": round(ms, 3), "unit": "ms",
         "n_gpus": args.gpus, "steps": steps, "warmup": min(args.warmup, 1),
-        "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
+        "ms_per_step": round(ms * per, 3), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": config_of(args, wl, g, gen),
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": cores, "kind": kind,
-                         "sample": f"one full-size AGNN layer (d={wl['hidden']}) per step, median "
+                         "sample": f"{what} per step, median "
                                    f"of {steps}; reference threads = all {cores} host cores"},
         "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -465,6 +495,16 @@ def run_b200(args, wl):
         cpu = {"value": round(cpu_ms, 1), "unit": "ms", "cores": cores, "kind": kind,
                "sample": f"one full-size AGNN layer (d={d}, {g.num_edges} edges) through the "
                          "reference's public functions, single run, all host cores"}
+    elif rank == 0 and world == 1 and not args.no_cpu:  # GCN: gcn_forward / layers
+        dims = [wl["d_in"]] + [wl["hidden"]] * (L - 1) + [wl["d_out"]]
+        run, kind, cores = reference_gcn_sample(g, xs.cpu().numpy(), dims)
+        t0 = time.perf_counter()
+        run()
+        cpu_ms = (time.perf_counter() - t0) * 1e3 / L
+        cpu = {"value": round(cpu_ms, 1), "unit": "ms", "cores": cores, "kind": kind,
+               "sample": f"one full-size gcn_forward ({L} layers, dims {dims}, {g.num_edges} "
+                         "edges) through the reference's public API, per layer, single run, "
+                         "all host cores"}
 
     pk, pk_src = peaks()
     if roof:
