@@ -582,28 +582,79 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
 }
 
 // Concurrent mode: (dense + sparse) partials of the non-hub rows, finalised.
+// Streaming: LPR = DC/4 lanes per row (float4 each), 32/LPR rows per warp
+// instruction; the row's l2 norm reduces over its lanes in double by a fixed
+// xor tree.  Same results as agnn_finalize up to the order of that sum.
 template <int FPL, int PREC>
 __global__ void agnn_final_kernel(const uint4* __restrict__ items, uint64_t n_items, uint64_t d,
                                   const float* __restrict__ opart, const float* __restrict__ lpart,
                                   const float* __restrict__ osp, const float* __restrict__ lsp,
                                   AgnnNext nx) {
-  constexpr int DC = 32 * FPL;
-  const uint32_t lane = threadIdx.x & 31;
+  constexpr uint32_t DC = 32 * FPL, LPR = DC / 4, RPW = 32 / LPR;
+  const uint32_t lane = threadIdx.x & 31, sub = lane / LPR, j = lane % LPR;
   const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  const uint64_t f = uint64_t(lane) * FPL;
-  const int fv = f >= d ? 0 : (d - f >= uint64_t(FPL) ? FPL : int(d - f));
+  const uint64_t f = 4u * j;
+  const int fv = f >= d ? 0 : (d - f >= 4 ? 4 : int(d - f));
   unsigned long long nz = 0;
-  for (uint64_t it = warp; it < n_items; it += nw) {
-    const uint4 w = items[it];
-    if (w.w != 0xFFFFFFFFu) continue;  // hub segment: agnn_long_rows_kernel
+  for (uint64_t base = warp * RPW; base < n_items; base += nw * RPW) {
+    const uint64_t it = base + sub;
+    const uint4 w = it < n_items ? items[it] : make_uint4(0, 0, 0, 0);
+    const bool ok = it < n_items && w.w == 0xFFFFFFFFu;  // hub segments: agnn_long_rows_kernel
     const uint64_t r = w.x;
-    float o[FPL];
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    float l = 0.0f;
+    if (ok) {
+      const float4 a = *reinterpret_cast<const float4*>(opart + r * DC + f);
+      const float4 b = *reinterpret_cast<const float4*>(osp + r * DC + f);
+      l = lpart[r] + lsp[r];
+      const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;
+      const float o[4] = {a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w};
 #pragma unroll
-    for (int i = 0; i < FPL; ++i) o[i] = i < fv ? opart[r * DC + f + i] + osp[r * DC + f + i] : 0.0f;
-    agnn_finalize<FPL, PREC>(r, o, lpart[r] + lsp[r], lane, fv, nx, nz);
+      for (int i = 0; i < 4; ++i) v[i] = (l > 0.0f && i < fv) ? o[i] * inv_l : 0.0f;
+      if (nx.out) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (i < fv) nx.out[r * nx.ldo + f + i] = v[i];
+      }
+    }
+    if (!nx.zq) continue;  // last layer
+    double sq = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) sq += double(v[i]) * double(v[i]);
+#pragma unroll
+    for (uint32_t o2 = 1; o2 < LPR; o2 <<= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o2);
+    if (!ok) continue;
+    const float inv = sq == 0.0 ? 0.0f : float(1.0 / sqrt(sq));
+    if (sq == 0.0 && j == 0) ++nz;
+    if (j == 0 && nx.norm) nx.norm[r] = float(sqrt(sq));
+    float zz[4], hh[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      zz[i] = v[i] * inv;  // padding features stay 0
+      hh[i] = v[i];
+    }
+    const uint64_t q = r * nx.ldq + f;
+    if (nx.z) *reinterpret_cast<float4*>(nx.z + q) = make_float4(zz[0], zz[1], zz[2], zz[3]);
+    if constexpr (PREC == SGTK_FP32) {
+      uint32_t a0[4], a1[4], b0[4], b1[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        split2(zz[i], a0[i], a1[i]);
+        split2(hh[i], b0[i], b1[i]);
+      }
+      *reinterpret_cast<uint4*>(nx.zq + q) = make_uint4(a0[0], a0[1], a0[2], a0[3]);
+      *reinterpret_cast<uint4*>(nx.zq1 + q) = make_uint4(a1[0], a1[1], a1[2], a1[3]);
+      *reinterpret_cast<uint4*>(nx.hq + q) = make_uint4(b0[0], b0[1], b0[2], b0[3]);
+      *reinterpret_cast<uint4*>(nx.hq1 + q) = make_uint4(b1[0], b1[1], b1[2], b1[3]);
+    } else {
+      *reinterpret_cast<float4*>(nx.zq + q) =
+          make_float4(tf32_rne(zz[0]), tf32_rne(zz[1]), tf32_rne(zz[2]), tf32_rne(zz[3]));
+      *reinterpret_cast<float4*>(nx.hq + q) =
+          make_float4(tf32_rne(hh[0]), tf32_rne(hh[1]), tf32_rne(hh[2]), tf32_rne(hh[3]));
+    }
   }
-  if (nx.zeros && lane == 0 && nz) atomicAdd(nx.zeros, nz);
+  if (nx.zeros && nz) atomicAdd(nx.zeros, nz);
 }
 
 // Hub rows: (O, l) = dense partial + segment partials in segment order, then

@@ -1,5 +1,7 @@
-for lib in base nb10 nb6 nb8_late nb10_late; do
-  echo "lib [$lib] agnn tf32 total/dense"
-  export SGTK_LIB=$PWD/variants/libsgtk_$lib.so
-  for m in 0 1; do SGTK_PANEL_DEBUG=$m timeout 200 python tools/agnn_only.py 2>&1 | tail -1; done
-done
+timeout 300 python -m pytest tests/test_gpu_panel.py tests/test_gpu_parity.py -x -q -m gpu -k agnn 2>&1 | tail -1
+for rep in 1 2; do
+for lib in variants/libsgtk_base.so ""; do
+  echo "lib [$lib] agnn tf32 total, fp32 total"
+  if [ -n "$lib" ]; then export SGTK_LIB=$PWD/$lib; else unset SGTK_LIB; fi
+  for p in tf32 fp32; do timeout 200 python tools/agnn_only.py --precision $p 2>&1 | tail -1; done
+done; done
