@@ -691,29 +691,60 @@ __global__ void agnn_long_rows_kernel(const uint4* __restrict__ lrows, uint64_t 
 
 // operand copies of the first layer's input: TF32 -> rounded (z, h);
 // FP32 -> hi / lo planes of z and h
-template <int PREC>
-__global__ void agnn_prep_kernel(const float* __restrict__ z, const float* __restrict__ h, uint64_t ldh,
-                                 uint64_t rows, uint64_t d, uint64_t ldq, float* __restrict__ zq,
-                                 float* __restrict__ zq1, float* __restrict__ hq, float* __restrict__ hq1,
-                                 const float* __restrict__ inv, float* __restrict__ norm) {
-  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows * ldq;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t r = i / ldq, c = i - r * ldq;
-    if (c == 0) norm[r] = inv[r] > 0.0f ? 1.0f / inv[r] : 0.0f;  // |h| = 1 / inv
-    const float zz = c < d ? z[r * ldq + c] : 0.0f, hh = c < d ? h[r * ldh + c] : 0.0f;
+// Layer-0 operands in one pass over x: the row's l2 norm (double, fixed xor
+// tree over its LPR = DC/4 lanes), z = x / |x| and the MMA operand copies
+// (TF32: rounded z and h; FP32: raw z, hi/lo planes, |h|); counts zero rows.
+template <int FPL, int PREC>
+__global__ void agnn_input_kernel(const float* __restrict__ x, uint64_t ldx, uint64_t rows, uint64_t d,
+                                  uint64_t ldq, float* __restrict__ z, float* __restrict__ zq,
+                                  float* __restrict__ zq1, float* __restrict__ hq, float* __restrict__ hq1,
+                                  float* __restrict__ norm, unsigned long long* __restrict__ zeros) {
+  constexpr uint32_t DC = 32 * FPL, LPR = DC / 4, RPW = 32 / LPR;
+  const uint32_t lane = threadIdx.x & 31, sub = lane / LPR, j = lane % LPR;
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t f = 4u * j;
+  const int fv = f >= d ? 0 : (d - f >= 4 ? 4 : int(d - f));
+  unsigned long long nz = 0;
+  for (uint64_t base = warp * RPW; base < rows; base += nw * RPW) {
+    const uint64_t r = base + sub;
+    const bool ok = r < rows;
+    float v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = ok && i < fv ? x[r * ldx + f + i] : 0.0f;
+    double sq = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) sq += double(v[i]) * double(v[i]);
+#pragma unroll
+    for (uint32_t o2 = 1; o2 < LPR; o2 <<= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o2);
+    if (!ok) continue;
+    const float inv = sq == 0.0 ? 0.0f : float(1.0 / sqrt(sq));
+    if (sq == 0.0 && j == 0) ++nz;
+    float zz[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) zz[i] = v[i] * inv;
+    const uint64_t q = r * ldq + f;
     if constexpr (PREC == SGTK_FP32) {
-      uint32_t a0, a1, b0, b1;
-      split2(zz, a0, a1);
-      split2(hh, b0, b1);
-      zq[i] = __uint_as_float(a0);
-      zq1[i] = __uint_as_float(a1);
-      hq[i] = __uint_as_float(b0);
-      hq1[i] = __uint_as_float(b1);
+      if (j == 0) norm[r] = inv > 0.0f ? 1.0f / inv : 0.0f;  // |h| = 1 / inv
+      *reinterpret_cast<float4*>(z + q) = make_float4(zz[0], zz[1], zz[2], zz[3]);
+      uint32_t a0[4], a1[4], b0[4], b1[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        split2(zz[i], a0[i], a1[i]);
+        split2(v[i], b0[i], b1[i]);
+      }
+      *reinterpret_cast<uint4*>(zq + q) = make_uint4(a0[0], a0[1], a0[2], a0[3]);
+      *reinterpret_cast<uint4*>(zq1 + q) = make_uint4(a1[0], a1[1], a1[2], a1[3]);
+      *reinterpret_cast<uint4*>(hq + q) = make_uint4(b0[0], b0[1], b0[2], b0[3]);
+      *reinterpret_cast<uint4*>(hq1 + q) = make_uint4(b1[0], b1[1], b1[2], b1[3]);
     } else {
-      zq[i] = tf32_rne(zz);
-      hq[i] = tf32_rne(hh);
+      *reinterpret_cast<float4*>(zq + q) =
+          make_float4(tf32_rne(zz[0]), tf32_rne(zz[1]), tf32_rne(zz[2]), tf32_rne(zz[3]));
+      *reinterpret_cast<float4*>(hq + q) =
+          make_float4(tf32_rne(v[0]), tf32_rne(v[1]), tf32_rne(v[2]), tf32_rne(v[3]));
     }
   }
+  if (zeros && nz) atomicAdd(zeros, nz);
 }
 
 inline unsigned blocks_for(uint64_t n, unsigned bs = 256) {
@@ -877,15 +908,20 @@ void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, cons
   rows(aux, osp, lsp, s);  // sparse partials on aux; final + hub rows join on s
 }
 
-void agnn_prep_launch(const float* z, const float* h, uint64_t ldh, uint64_t rows, uint64_t d,
-                      uint64_t ldq, int prec, float* zq, float* zq1, float* hq, float* hq1,
-                      const float* inv, float* norm, cudaStream_t s) {
+void agnn_input_launch(const float* x, uint64_t ldx, uint64_t rows, uint64_t d, uint64_t ldq, int prec,
+                       float* z, float* zq, float* zq1, float* hq, float* hq1, float* norm,
+                       uint64_t* zeros, cudaStream_t s) {
   if (!rows) return;
-  if (prec == SGTK_FP32)
-    agnn_prep_kernel<SGTK_FP32><<<blocks_for(rows * ldq), 256, 0, s>>>(z, h, ldh, rows, d, ldq, zq, zq1, hq, hq1, inv, norm);
-  else
-    agnn_prep_kernel<SGTK_TF32><<<blocks_for(rows * ldq), 256, 0, s>>>(z, h, ldh, rows, d, ldq, zq, zq1, hq, hq1, inv, norm);
-  CU_LAUNCH("agnn_prep_kernel");
+  auto* zc = reinterpret_cast<unsigned long long*>(zeros);
+  const unsigned nb = blocks_for((rows + 3) / 4 * 32);
+  if (ldq == 32) {
+    if (prec == SGTK_FP32) agnn_input_kernel<1, SGTK_FP32><<<nb, 256, 0, s>>>(x, ldx, rows, d, ldq, z, zq, zq1, hq, hq1, norm, zc);
+    else agnn_input_kernel<1, SGTK_TF32><<<nb, 256, 0, s>>>(x, ldx, rows, d, ldq, z, zq, zq1, hq, hq1, norm, zc);
+  } else {
+    if (prec == SGTK_FP32) agnn_input_kernel<2, SGTK_FP32><<<nb, 256, 0, s>>>(x, ldx, rows, d, ldq, z, zq, zq1, hq, hq1, norm, zc);
+    else agnn_input_kernel<2, SGTK_TF32><<<nb, 256, 0, s>>>(x, ldx, rows, d, ldq, z, zq, zq1, hq, hq1, norm, zc);
+  }
+  CU_LAUNCH("agnn_input_kernel");
 }
 
 }  // namespace sgtkcu

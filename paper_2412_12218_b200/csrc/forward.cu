@@ -152,7 +152,6 @@ void agnn_forward_panel(const sgtk_graph* g, const float* x, uint64_t ldx, uint6
   for (int a = 0; a < 2; ++a)
     for (int b = 0; b < 5; ++b) set[a][b] = take(NC * ldq * 4);  // z, zq, zq1, hq, hq1
   float* norm[2] = {take(NC * 4), take(NC * 4)};
-  float* inv = take(NC * 4);
   float* buf[2] = {take(N * ldb * 4), take(N * ldb * 4)};
   float* opart = take(N * ldq * 4);
   float* lpart = take(N * 4);
@@ -167,9 +166,8 @@ void agnn_forward_panel(const sgtk_graph* g, const float* x, uint64_t ldx, uint6
     CU(cudaMemsetAsync(set[0][0], 0, reinterpret_cast<char*>(set[1][4]) - reinterpret_cast<char*>(set[0][0]) +
                                          NC * ldq * 4, s));
   // layer 0 input: z = l2norm(x), operand copies
-  l2norm_launch(x, NC, d, ldx, set[0][0], ldq, inv, zeros, s);
-  agnn_prep_launch(set[0][0], x, ldx, NC, d, ldq, prec, set[0][1], set[0][2], set[0][3], set[0][4],
-                   inv, norm[0], s);
+  agnn_input_launch(x, ldx, NC, d, ldq, prec, set[0][0], set[0][1], set[0][2], set[0][3], set[0][4],
+                    norm[0], zeros, s);
   for (uint32_t l = 0; l < L; ++l) {
     const bool last = l + 1 == L;
     float** cur = set[l & 1];

@@ -61,9 +61,10 @@ void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, cons
                       const float* hq, const float* hq1, uint64_t ldq, const float* norm,
                       uint64_t d, float beta, int prec, float* opart, float* lpart, float* seg_o,
                       float* seg_l, float* osp, float* lsp, const AgnnNext& nx, cudaStream_t s);
-void agnn_prep_launch(const float* z, const float* h, uint64_t ldh, uint64_t rows, uint64_t d,
-                      uint64_t ldq, int prec, float* zq, float* zq1, float* hq, float* hq1,
-                      const float* inv, float* norm, cudaStream_t s);
+// Layer-0 input of the panel path: l2 norm + operand copies of x in one pass.
+void agnn_input_launch(const float* x, uint64_t ldx, uint64_t rows, uint64_t d, uint64_t ldq, int prec,
+                       float* z, float* zq, float* zq1, float* hq, float* hq1, float* norm,
+                       uint64_t* zeros, cudaStream_t s);
 PanelView panel_view(const sgtk_graph* g);
 void panel_debug_set(int mode);
 int panel_debug_mode();
