@@ -408,7 +408,8 @@ def run_b200(args, wl):
 
         if mode == 2:
             pi = dg.panel_info()
-            launches_per_step = 2 + L * (2 + (1 if pi["long_rows"] else 0))
+            # input kernel, then per layer: dense + rows + final (+ hub rows)
+            launches_per_step = 1 + L * (3 + (1 if pi["long_rows"] else 0))
         else:
             launches_per_step = L * (2 if mode == 1 else 4) + (
                 L if (mode == 1 and dg_has_splits(dg, 16)) or (mode == 0 and dg_has_splits(dg, 8)) else 0)
