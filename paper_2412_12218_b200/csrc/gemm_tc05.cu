@@ -334,11 +334,13 @@ bool gemm_tc05_launch(const float* a, uint64_t lda, const float* w, uint64_t m, 
   }
   const uint32_t a_bytes = kBM * kBK * 4, w_bytes = n_pad * kBK * 4;
   const uint32_t stage_bytes = (P_A * a_bytes + P_W * w_bytes + 1023) & ~1023u;
-  const uint32_t stages = std::max(2u, std::min(4u, (200u * 1024u) / stage_bytes));
+  const uint32_t num_kc = uint32_t(k_pad / kBK);
+  // a ring deeper than the K loop only costs residency: small K (the GCN
+  // hidden layers, K = 64) then fits 4 CTAs per SM instead of 2
+  const uint32_t stages = std::max(2u, std::min(std::min(4u, num_kc), (200u * 1024u) / stage_bytes));
   const size_t smem = size_t(stages) * stage_bytes + 1024 /*align*/ + 256 /*barriers*/;
   uint32_t tmem_cols = 32;
   while (tmem_cols < n_pad) tmem_cols <<= 1;
-  const uint32_t num_kc = uint32_t(k_pad / kBK);
   dim3 grid(unsigned((m + kBM - 1) / kBM));
   // the opt-in smem ceiling is set once per kernel (host overhead, not per call)
   static std::once_flag attr_once;

@@ -1,7 +1,5 @@
-timeout 300 python -m pytest tests/test_gpu_panel.py tests/test_gpu_parity.py -x -q -m gpu -k agnn 2>&1 | tail -1
-for rep in 1 2; do
+timeout 300 python -m pytest tests -x -q -m gpu -k "gemm or gcn" 2>&1 | tail -1
 for lib in variants/libsgtk_base.so ""; do
-  echo "lib [$lib] agnn tf32 total, fp32 total"
   if [ -n "$lib" ]; then export SGTK_LIB=$PWD/$lib; else unset SGTK_LIB; fi
-  for p in tf32 fp32; do timeout 200 python tools/agnn_only.py --precision $p 2>&1 | tail -1; done
-done; done
+  echo "lib [$lib]"; timeout 300 python bench.py --workload proteins-gcn --no-cpu --steps 5 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['kernels_ms'])"
+done
