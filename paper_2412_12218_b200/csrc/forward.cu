@@ -83,21 +83,26 @@ void gcn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint32_t L,
 
   const float* h = x;
   uint64_t ldh = ldx;
+  bool h_tf32 = false;  // h already TF32-rounded by the GEMM epilogue that wrote it
   const float* w = weights;
+  const bool tf = prec == SGTK_TF32;
   for (uint32_t l = 0; l < L; ++l) {
     const uint64_t din = dims[l], dout = dims[l + 1];
     const bool last = l + 1 == L;
     float* dst = last ? out : buf[l & 1];
     const uint64_t ldd = last ? ldo : ld4(dout);
     const bool alt = order == 1 || (order == 2 && dout < din);
-    if (!alt) {  // reference order: (A h) W
-      spmm_launch(g, h, ldh, din, cut, nullptr, prec, tmp, ld4(din), flag, s);
-      gemm_launch(tmp, ld4(din), w, N, din, dout, relu[l], prec, dst, ldd, s);
-      if (last) relu_nonfinite_launch(dst, N, dout, ldd, 0, flag, s);
+    if (!alt) {  // reference order: (A h) W; the GEMM epilogue applies ReLU,
+                 // rounds for the next layer's TF32 SpMM and checks the output
+      spmm_launch(g, h, ldh, din, cut, nullptr, prec, tmp, ld4(din), flag, s, h_tf32);
+      gemm_launch(tmp, ld4(din), w, N, din, dout, relu[l], prec, dst, ldd, s, tf && !last,
+                  last ? flag : nullptr);
+      h_tf32 = tf && !last;
     } else {      // A (h W), ReLU after the aggregation
-      gemm_launch(h, ldh, w, N, din, dout, 0, prec, tmp, ld4(dout), s);
-      spmm_launch(g, tmp, ld4(dout), dout, cut, nullptr, prec, dst, ldd, flag, s);
+      gemm_launch(h, ldh, w, N, din, dout, 0, prec, tmp, ld4(dout), s, tf);
+      spmm_launch(g, tmp, ld4(dout), dout, cut, nullptr, prec, dst, ldd, flag, s, tf);
       if (relu[l] || last) relu_nonfinite_launch(dst, N, dout, ldd, relu[l], flag, s);
+      h_tf32 = false;
     }
     w += din * dout;
     h = dst;

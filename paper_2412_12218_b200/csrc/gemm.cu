@@ -11,6 +11,7 @@
 // FP32 precision uses the 4-term TF32 split (common.cuh) on both paths.
 
 #include "graph.cuh"
+#include "kernels.cuh"
 
 namespace sgtkcu {
 namespace {
@@ -133,10 +134,12 @@ gemm_mma_kernel(const float* __restrict__ a, uint64_t lda, const float* __restri
 }  // namespace
 
 bool gemm_tc05_launch(const float* a, uint64_t lda, const float* w, uint64_t m, uint64_t k,
-                      uint64_t n, int relu, int prec, float* out, uint64_t ldo, cudaStream_t s);
+                      uint64_t n, int relu, int prec, float* out, uint64_t ldo, cudaStream_t s,
+                      bool round_tf32, uint32_t* nonfinite);
 
 void gemm_launch(const float* a, uint64_t lda, const float* w, uint64_t m, uint64_t k, uint64_t n,
-                 int relu, int prec, float* out, uint64_t ldo, cudaStream_t s) {
+                 int relu, int prec, float* out, uint64_t ldo, cudaStream_t s, bool round_tf32,
+                 uint32_t* nonfinite) {
   if (prec != SGTK_FP32 && prec != SGTK_TF32)
     raise(SGTK_ERR_RANGE, "gemm: precision must be FP32 or TF32");
   if (m == 0 || n == 0) return;
@@ -144,7 +147,7 @@ void gemm_launch(const float* a, uint64_t lda, const float* w, uint64_t m, uint6
     CU(cudaMemset2DAsync(out, ldo * 4, 0, n * 4, m, s));
     return;
   }
-  if (gemm_tc05_launch(a, lda, w, m, k, n, relu, prec, out, ldo, s)) return;
+  if (gemm_tc05_launch(a, lda, w, m, k, n, relu, prec, out, ldo, s, round_tf32, nonfinite)) return;
   const bool vec = lda % 4 == 0 && reinterpret_cast<uintptr_t>(a) % 16 == 0;
   dim3 grid(unsigned((m + BM - 1) / BM), unsigned((n + BN - 1) / BN));
   if (prec == SGTK_FP32) {
@@ -155,6 +158,11 @@ void gemm_launch(const float* a, uint64_t lda, const float* w, uint64_t m, uint6
     else gemm_mma_kernel<SGTK_TF32, false><<<grid, NT, 0, s>>>(a, lda, w, m, k, n, relu, out, ldo);
   }
   CU_LAUNCH("gemm_mma_kernel");
+  // outside the tcgen05 envelope: the epilogue options as separate passes
+  // (round_tf32 is for internal buffers: the pass also rounds the padding
+  // columns between rows)
+  if (round_tf32) tf32_launch(out, out, (m - 1) * ldo + n, s);
+  if (nonfinite) relu_nonfinite_launch(out, m, n, ldo, 0, nonfinite, s);
 }
 
 }  // namespace sgtkcu

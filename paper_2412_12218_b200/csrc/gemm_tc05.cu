@@ -98,8 +98,9 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 template <int PREC>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
-                 uint64_t m, uint32_t n, uint32_t n_pad, uint32_t num_kc, int relu,
-                 float* __restrict__ out, uint64_t ldo, uint32_t stages, uint32_t tmem_cols) {
+                 uint64_t m, uint32_t n, uint32_t n_pad, uint32_t num_kc, int relu, int round_tf32,
+                 float* __restrict__ out, uint64_t ldo, uint32_t stages, uint32_t tmem_cols,
+                 uint32_t* __restrict__ nonfinite) {
   constexpr int P_A = PREC == SGTK_FP32 ? 3 : 1;  // A planes
   constexpr int P_W = PREC == SGTK_FP32 ? 2 : 1;  // W planes
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -217,6 +218,7 @@ gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t quad = warp & 3u;  // TMEM lanes [32*quad, 32*quad + 32)
     const uint64_t row = m0 + quad * 32 + lane;
+    bool bad = false;
     for (uint32_t c0 = 0; c0 < n_pad; c0 += 16) {
       uint32_t r[16];
       const uint32_t taddr = tmem_d + ((quad * 32u) << 16) + c0;
@@ -234,10 +236,15 @@ gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         for (int j = 0; j < 16; ++j) {
           float v = __uint_as_float(r[j]);
           if (relu) v = fmaxf(v, 0.0f);
-          if (c0 + j < n) o[j] = v;
+          if (round_tf32) v = tf32_rne(v);  // consumer: a TF32 SpMM (same RNE it would apply)
+          if (c0 + j < n) {
+            o[j] = v;
+            bad |= !isfinite(v);
+          }
         }
       }
     }
+    if (nonfinite && __any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(nonfinite, 1u);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -311,7 +318,8 @@ int device_sm_major() {
 // Returns false (caller uses the mma.sync kernel) when the shape/alignment is
 // outside this kernel's envelope: n > 128, lda % 4 != 0, unaligned base.
 bool gemm_tc05_launch(const float* a, uint64_t lda, const float* w, uint64_t m, uint64_t k,
-                      uint64_t n, int relu, int prec, float* out, uint64_t ldo, cudaStream_t s) {
+                      uint64_t n, int relu, int prec, float* out, uint64_t ldo, cudaStream_t s,
+                      bool round_tf32, uint32_t* nonfinite) {
   if (getenv("SGTK_DISABLE_TC05")) return false;
   if (n == 0 || n > 128 || m == 0 || k == 0) return false;
   if (lda % 4 != 0 || reinterpret_cast<uintptr_t>(a) % 16 != 0) return false;
@@ -352,10 +360,12 @@ bool gemm_tc05_launch(const float* a, uint64_t lda, const float* w, uint64_t m, 
   });
   if (prec == SGTK_FP32) {
     gemm_tc05_kernel<SGTK_FP32><<<grid, kThreads, smem, s>>>(ma, mw, m, uint32_t(n), n_pad, num_kc,
-                                                             relu, out, ldo, stages, tmem_cols);
+                                                             relu, int(round_tf32), out, ldo, stages,
+                                                             tmem_cols, nonfinite);
   } else {
     gemm_tc05_kernel<SGTK_TF32><<<grid, kThreads, smem, s>>>(ma, mw, m, uint32_t(n), n_pad, num_kc,
-                                                             relu, out, ldo, stages, tmem_cols);
+                                                             relu, int(round_tf32), out, ldo, stages,
+                                                             tmem_cols, nonfinite);
   }
   CU_LAUNCH("gemm_tc05_kernel");
   CU(cudaFreeAsync(wt, s));

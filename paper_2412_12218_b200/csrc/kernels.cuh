@@ -16,7 +16,7 @@ sgtk_graph* graph_reblock(const sgtk_graph* src, uint32_t blk_w, cudaStream_t s)
 
 void spmm_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
                  const uint32_t* cut_dev, const float* ev, int prec, float* out, uint64_t ldo,
-                 uint32_t* nonfinite, cudaStream_t s);
+                 uint32_t* nonfinite, cudaStream_t s, bool x_tf32 = false);
 void sddmm_launch(const sgtk_graph* g, const float* x, uint64_t ldx, const float* y, uint64_t ldy,
                   uint64_t d, const uint32_t* cut16_dev, const float* ev, bool unit_values,
                   int prec, const float* inv_norm, float scale, float* out, cudaStream_t s);
@@ -28,8 +28,11 @@ void l2norm_launch(const float* h, uint64_t rows, uint64_t cols, uint64_t ldh, f
 void gcn_normalize_launch(const uint64_t* np, const uint32_t* el, uint64_t n, float* vals,
                           cudaStream_t s);
 void tf32_launch(const float* in, float* out, uint64_t n, cudaStream_t s);
+// round_tf32: store RNE-TF32-rounded results (the consumer is a TF32 SpMM);
+// nonfinite: set to 1 when a stored value is NaN/Inf.
 void gemm_launch(const float* a, uint64_t lda, const float* w, uint64_t m, uint64_t k, uint64_t n,
-                 int relu, int prec, float* out, uint64_t ldo, cudaStream_t s);
+                 int relu, int prec, float* out, uint64_t ldo, cudaStream_t s,
+                 bool round_tf32 = false, uint32_t* nonfinite = nullptr);
 void relu_nonfinite_launch(float* x, uint64_t rows, uint64_t cols, uint64_t ld, int relu,
                            uint32_t* nonfinite, cudaStream_t s);
 void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, const float* z,
@@ -39,9 +42,11 @@ void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, const 
 // 128-row panel format + tcgen05 SpMM (panel.cu)
 Windows build_row_windows(const sgtk_graph& g, uint32_t bh, cudaStream_t s);
 void build_panels(sgtk_graph& g, cudaStream_t s);
+// x_tf32: x is already TF32-rounded (RNE) by its producer (the fused GEMM
+// epilogue), so the TF32 path skips its rounding pass over x.
 bool spmm_panel_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
                        const float* ev, int prec, float* out, uint64_t ldo, uint32_t* nonfinite,
-                       cudaStream_t s);
+                       cudaStream_t s, bool x_tf32 = false);
 
 // AGNN layer on panels (agnn_panel.cu)
 struct AgnnNext {

@@ -375,7 +375,7 @@ template <int DC, int PREC>
 __global__ void __launch_bounds__(kPanelThreads, PanelCfg<DC, PREC>::CTAS)
 spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict__ x, uint64_t ldx,
                   uint64_t d, float* __restrict__ out, uint64_t ldo, int vec_out,
-                  long long* __restrict__ trace) {
+                  uint32_t* __restrict__ nonfinite, long long* __restrict__ trace) {
   using C = PanelCfg<DC, PREC>;
   // optional timeline (SGTK_PANEL_TRACE): trace[(panel * 256 + chunk) * 8 + event]
   auto mark = [&](uint32_t c, int ev) {
@@ -646,6 +646,7 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
     tc_fence_after();
     const bool rv = r < pv.n_rows;
     float* o = out + r * ldo + fbase;
+    bool bad = false;  // a non-finite dense sum stays non-finite after the sparse edges
 #pragma unroll
     for (int cc = 0; cc < DC; cc += 16) {
       uint32_t v[16];
@@ -657,6 +658,9 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
         for (int j = 0; j < 16; ++j) v[j] = 0u;
       }
       if (rv) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          bad |= cc + j < dvalid && (v[j] & 0x7F800000u) == 0x7F800000u;
         if (vec_out && dvalid == DC) {
 #pragma unroll
           for (int j = 0; j < 4; ++j)
@@ -670,6 +674,7 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
         }
       }
     }
+    if (nonfinite && __any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(nonfinite, 1u);
   }
 
   tc_fence_before();
@@ -788,20 +793,6 @@ __global__ void long_rows_kernel(const uint4* __restrict__ lrows, uint64_t n_lon
   if (nonfinite && bad) atomicOr(nonfinite, 1u);
 }
 
-// Rows without any sparse edge are final after the dense kernel: scan them
-// for non-finite values (the other rows are checked by the sparse kernels).
-__global__ void dense_rows_check_kernel(const uint32_t* __restrict__ sptr, uint64_t n,
-                                        const float* __restrict__ out, uint64_t ldo, uint64_t d,
-                                        uint32_t* __restrict__ nonfinite) {
-  bool bad = false;
-  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n * d;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t r = i / d, c = i - r * d;
-    if (sptr[r + 1] == sptr[r]) bad |= !isfinite(out[r * ldo + c]);
-  }
-  if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
-}
-
 // X rounded once per call to TF32 (RNE, tf32_round_value semantics), rows
 // padded to a multiple of 4 floats with zeros: both the tensor-core B tiles
 // and the CUDA-core edges then read ready operands.
@@ -856,7 +847,8 @@ bool panel_smem(uint32_t max_entries, PanelSmem& L) {
 
 template <int DC, int PREC>
 bool launch_dense(const PanelView& v, uint64_t P, uint32_t max_entries, const float* x,
-                  uint64_t ldx, uint64_t d, float* out, uint64_t ldo, int vec_out, cudaStream_t s) {
+                  uint64_t ldx, uint64_t d, float* out, uint64_t ldo, int vec_out,
+                  uint32_t* nonfinite, cudaStream_t s) {
   PanelSmem L;
   if (!panel_smem<DC, PREC>(max_entries, L)) return false;
   static std::once_flag once;
@@ -876,7 +868,7 @@ bool launch_dense(const PanelView& v, uint64_t P, uint32_t max_entries, const fl
     return t;
   }();
   spmm_panel_kernel<DC, PREC><<<grid, kPanelThreads, L.total, s>>>(v, L, x, ldx, d, out, ldo,
-                                                                   vec_out, trace);
+                                                                   vec_out, nonfinite, trace);
   if (trace) {
     std::vector<long long> h(4 * 256 * 8);
     cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost);
@@ -1098,7 +1090,7 @@ bool panel_enabled() {
 // envelope: unaligned feature rows, a chunk too large for shared memory.
 bool spmm_panel_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
                        const float* ev, int prec, float* out, uint64_t ldo, uint32_t* nonfinite,
-                       cudaStream_t s) {
+                       cudaStream_t s, bool x_tf32) {
   if (!g->panels || !panel_enabled()) return false;
   if (ldx % 4 != 0 || reinterpret_cast<uintptr_t>(x) % 16 != 0) return false;
   if (g->n_rows == 0 || d == 0) return true;
@@ -1135,7 +1127,7 @@ bool spmm_panel_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64
     sent = os;
   }
   float* xr = nullptr;
-  if (prec == SGTK_TF32) {
+  if (prec == SGTK_TF32 && !x_tf32) {  // x_tf32: the producer already rounded x (RNE)
     const uint64_t ldr = (d + 3) / 4 * 4;
     CU(cudaMallocAsync(reinterpret_cast<void**>(&xr), std::max<uint64_t>(g->n_cols * ldr, 4) * 4, s));
     tf32_rows_kernel<<<grid_for(g->n_cols * ldr / 4, 256), 256, 0, s>>>(x, ldx, g->n_cols, d, xr, ldr);
@@ -1148,21 +1140,18 @@ bool spmm_panel_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64
   const int dbg = panel_debug();
   if (dbg != 2) {
     if (prec == SGTK_FP32) {
-      if (d <= 32) launch_dense<32, SGTK_FP32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, s);
-      else launch_dense<64, SGTK_FP32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, s);
+      if (d <= 32) launch_dense<32, SGTK_FP32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, nonfinite, s);
+      else launch_dense<64, SGTK_FP32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, nonfinite, s);
     } else {
-      if (d <= 32) launch_dense<32, SGTK_TF32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, s);
-      else launch_dense<64, SGTK_TF32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, s);
+      if (d <= 32) launch_dense<32, SGTK_TF32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, nonfinite, s);
+      else launch_dense<64, SGTK_TF32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, nonfinite, s);
     }
   } else {
     CU(cudaMemset2DAsync(out, ldo * 4, 0, d * 4, g->n_rows, s));
   }
+  // non-finite results: the dense epilogue checks every row it stores, the
+  // sparse kernels the rows they finish
   if (dbg != 1) launch_sparse(pn, sent, x, ldx, d, out, ldo, nonfinite, s, prec);
-  if (nonfinite) {
-    dense_rows_check_kernel<<<grid_for(g->n_rows * d, 256), 256, 0, s>>>(
-        pn.sptr->as<uint32_t>(), g->n_rows, out, ldo, d, nonfinite);
-    CU_LAUNCH("dense_rows_check_kernel");
-  }
   if (ov) CU(cudaFreeAsync(ov, s));
   if (xr) CU(cudaFreeAsync(xr, s));
   return true;

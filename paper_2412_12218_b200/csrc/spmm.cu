@@ -246,13 +246,13 @@ void launch_prec(int dc, const sgtk_graph* g, const uint32_t* thr, const float* 
 
 void spmm_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
                  const uint32_t* cut_dev, const float* ev, int prec, float* out, uint64_t ldo,
-                 uint32_t* nonfinite, cudaStream_t s) {
+                 uint32_t* nonfinite, cudaStream_t s, bool x_tf32) {
   if (prec != SGTK_FP32 && prec != SGTK_TF32)
     raise(SGTK_ERR_RANGE, "spmm: precision must be FP32 or TF32");
   if (ldx < d || ldo < d) raise(SGTK_ERR_SHAPE, "spmm: leading dimension smaller than width");
   if (g->n_rows == 0 || d == 0) return;
   // default plan (all tiles on the tensor cores): the 128-row panel kernel
-  if (!cut_dev && spmm_panel_launch(g, x, ldx, d, ev, prec, out, ldo, nonfinite, s)) return;
+  if (!cut_dev && spmm_panel_launch(g, x, ldx, d, ev, prec, out, ldo, nonfinite, s, x_tf32)) return;
   DevBuf cut_keep;
   const uint32_t* thr = internal_cut(g, cut_dev, 8, s, cut_keep);
   const float* vals = ev ? ev : (g->has_values ? g->vals->as<float>() : nullptr);
