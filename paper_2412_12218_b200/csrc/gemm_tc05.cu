@@ -12,7 +12,9 @@
 //                   TF32: A <- RNE(A) in place (tf32_round_value semantics)
 //                   FP32: A -> A0 + A1 + A2 (11+11+2-bit exact split)
 //                 then fence.proxy.async and arrive; after the K loop the
-//                 same warps are the epilogue (tcgen05.ld 32x32b, ReLU, store)
+//                 same warps are the epilogue (tcgen05.ld 32x32b, ReLU / TF32
+//                 rounding / non-finite check, rows staged in smem, coalesced
+//                 float4 stores)
 //   warp 1        TMEM allocator + single-thread MMA issuer:
 //                   TF32: D += A W0            (per 8-wide k step)
 //                   FP32: D += A2 W0 + A0 W1 + A1 W0 + A0 W0   (4-term split,
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                  uint64_t m, uint32_t n, uint32_t n_pad, uint32_t num_kc, int relu, int round_tf32,
                  float* __restrict__ out, uint64_t ldo, uint32_t stages, uint32_t tmem_cols,
-                 uint32_t* __restrict__ nonfinite) {
+                 uint32_t* __restrict__ nonfinite, uint32_t region_bytes, int vec_out) {
   constexpr int P_A = PREC == SGTK_FP32 ? 3 : 1;  // A planes
   constexpr int P_W = PREC == SGTK_FP32 ? 2 : 1;  // W planes
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -109,7 +111,8 @@ gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const uint32_t a_bytes = kBM * kBK * 4;      // 16 KB
   const uint32_t w_bytes = n_pad * kBK * 4;    // n_pad x 128 B
   const uint32_t stage_bytes = (P_A * a_bytes + P_W * w_bytes + 1023) & ~1023u;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+  // [ring | epilogue tile] region, then the barriers
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + region_bytes);
   uint64_t* conv = full + stages;
   uint64_t* empty = conv + stages;
   uint64_t* tmem_full = empty + stages;
@@ -213,11 +216,16 @@ gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       __syncwarp();
       if (lane == 0) mbar_arrive(conv + s);
     }
-    // ---------------- epilogue: TMEM -> registers -> global ----------------
+    // ---------------- epilogue: TMEM -> registers -> smem -> global ---------
+    // Each warp stages its 32 rows in shared memory (the ring is idle now) and
+    // writes them back row-contiguously: coalesced stores instead of one
+    // 4-byte store per row per instruction.
     mbar_wait(tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t quad = warp & 3u;  // TMEM lanes [32*quad, 32*quad + 32)
-    const uint64_t row = m0 + quad * 32 + lane;
+    const uint32_t tse = n_pad + 4;   // staged row stride (floats): 16-byte aligned, banks spread
+    float* tw = reinterpret_cast<float*>(smem) + quad * 32u * tse;
+    const uint32_t tws = smem_u32(tw);
     bool bad = false;
     for (uint32_t c0 = 0; c0 < n_pad; c0 += 16) {
       uint32_t r[16];
@@ -230,18 +238,35 @@ gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
           : "r"(taddr));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < m) {
-        float* o = out + row * ldo + c0;
+      const bool rv = m0 + quad * 32 + lane < m;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          float v = __uint_as_float(r[j]);
-          if (relu) v = fmaxf(v, 0.0f);
-          if (round_tf32) v = tf32_rne(v);  // consumer: a TF32 SpMM (same RNE it would apply)
-          if (c0 + j < n) {
-            o[j] = v;
-            bad |= !isfinite(v);
-          }
-        }
+      for (int j = 0; j < 16; ++j) {
+        float v = __uint_as_float(r[j]);
+        if (relu) v = fmaxf(v, 0.0f);
+        if (round_tf32) v = tf32_rne(v);  // consumer: a TF32 SpMM (same RNE it would apply)
+        bad |= rv && c0 + j < n && !isfinite(v);
+        r[j] = __float_as_uint(v);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(tws + (lane * tse + c0 + 4 * j) * 4),
+                     "r"(r[4 * j]), "r"(r[4 * j + 1]), "r"(r[4 * j + 2]), "r"(r[4 * j + 3])
+                     : "memory");
+    }
+    __syncwarp();
+    const uint64_t rbase = m0 + quad * 32;
+    if (vec_out) {  // n % 4 == 0, 16-byte aligned rows
+      const uint32_t n4 = n / 4;
+      for (uint32_t i = lane; i < 32 * n4; i += 32) {
+        const uint32_t rr = i / n4, cc = i - rr * n4;
+        if (rbase + rr < m)
+          reinterpret_cast<float4*>(out + (rbase + rr) * ldo)[cc] =
+              *reinterpret_cast<const float4*>(tw + rr * tse + 4 * cc);
+      }
+    } else {
+      for (uint32_t i = lane; i < 32 * n; i += 32) {
+        const uint32_t rr = i / n, cc = i - rr * n;
+        if (rbase + rr < m) out[(rbase + rr) * ldo + cc] = tw[rr * tse + cc];
       }
     }
     if (nonfinite && __any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(nonfinite, 1u);
@@ -346,7 +371,10 @@ bool gemm_tc05_launch(const float* a, uint64_t lda, const float* w, uint64_t m, 
   // a ring deeper than the K loop only costs residency: small K (the GCN
   // hidden layers, K = 64) then fits 4 CTAs per SM instead of 2
   const uint32_t stages = std::max(2u, std::min(std::min(4u, num_kc), (200u * 1024u) / stage_bytes));
-  const size_t smem = size_t(stages) * stage_bytes + 1024 /*align*/ + 256 /*barriers*/;
+  const uint32_t tile_bytes = kBM * (n_pad + 4) * 4;  // staged epilogue tile
+  const uint32_t region = (std::max(stages * stage_bytes, tile_bytes) + 1023) & ~1023u;
+  const size_t smem = size_t(region) + 1024 /*align*/ + 256 /*barriers*/;
+  const int vec_out = n % 4 == 0 && ldo % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
   uint32_t tmem_cols = 32;
   while (tmem_cols < n_pad) tmem_cols <<= 1;
   dim3 grid(unsigned((m + kBM - 1) / kBM));
@@ -361,11 +389,11 @@ bool gemm_tc05_launch(const float* a, uint64_t lda, const float* w, uint64_t m, 
   if (prec == SGTK_FP32) {
     gemm_tc05_kernel<SGTK_FP32><<<grid, kThreads, smem, s>>>(ma, mw, m, uint32_t(n), n_pad, num_kc,
                                                              relu, int(round_tf32), out, ldo, stages,
-                                                             tmem_cols, nonfinite);
+                                                             tmem_cols, nonfinite, region, vec_out);
   } else {
     gemm_tc05_kernel<SGTK_TF32><<<grid, kThreads, smem, s>>>(ma, mw, m, uint32_t(n), n_pad, num_kc,
                                                              relu, int(round_tf32), out, ldo, stages,
-                                                             tmem_cols, nonfinite);
+                                                             tmem_cols, nonfinite, region, vec_out);
   }
   CU_LAUNCH("gemm_tc05_kernel");
   CU(cudaFreeAsync(wt, s));
