@@ -651,14 +651,15 @@ def kernel_breakdown(args, wl, dg, g, h, D, prec, mode, flush, stream, gcn_layer
                 check(L.sgtk_agnn_forward(dg.handle, h.data_ptr(), d, d, 1,
                                           np.ones(1, np.float32).ctypes.data, None, pr, 2,
                                           ws.data_ptr(), ws.numel(), out.data_ptr(), d, None, s))
-            res["agnn_layer_panel(l2norm+prep+dense+rows)"] = ev_time(panel_one)
+            res["agnn_layer_panel(input+dense+rows+final)"] = ev_time(panel_one)
             check(L.sgtk_debug_set(1))  # tensor-core part only
             res["panel_dense_part"] = ev_time(panel_one)
             check(L.sgtk_debug_set(2))  # CUDA-core part only
             res["panel_sparse_part"] = ev_time(panel_one)
             check(L.sgtk_debug_set(0))
-            # one layer inside the 4-layer stack (input normalisation fused into the previous layer)
-            res["agnn_panel_layer"] = res["agnn_layer_panel(l2norm+prep+dense+rows)"] - res["l2norm"]
+            # one layer inside the 4-layer stack (its input normalisation is fused into
+            # the previous layer's final kernel; the l2norm pass stands in for the input kernel)
+            res["agnn_panel_layer"] = res["agnn_layer_panel(input+dense+rows+final)"] - res["l2norm"]
         s_ = 4
         B_fused = 8 * (N + 1) + 4 * E + 4 * N + 2 * s_ * N * d
         B_spmm = 8 * (N + 1) + 4 * E + 4 * E + s_ * N * d + 4 * N * d
