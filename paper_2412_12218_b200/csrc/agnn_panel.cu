@@ -360,11 +360,19 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
     // (K-major SWIZZLE_128B B of S), 32 h rows (MN-major SWIZZLE_128B_BASE32B
     // B of PV), 128 row masks; completion via cp.async.mbarrier.arrive.noinc.
     const uint32_t par = warp - 9;
+    // column ids one chunk ahead: the global load stays off the slot-free ->
+    // gather-issue path
+    uint32_t coln = par < nch ? pv.dcols[uint64_t(c0 + par) * kChunkCols + lane] : 0u;
     for (uint32_t c = par; c < nch; c += 2) {
       const uint32_t ds = c % C::NB;
+#ifdef SGTK_AGNN_GMASK  // timing experiment only: gather a small hot set of rows
+      const uint32_t col = coln == 0xFFFFFFFFu ? coln : (coln & SGTK_AGNN_GMASK);
+#else
+      const uint32_t col = coln;
+#endif
+      coln = c + 2 < nch ? pv.dcols[uint64_t(c0 + c + 2) * kChunkCols + lane] : 0u;
       mbar_wait(bempty + ds, ((c / C::NB) & 1u) ^ 1u);
       if (lane == 0) mark(c, 4);
-      const uint32_t col = pv.dcols[uint64_t(c0 + c) * kChunkCols + lane];
       const uint32_t ht = hr_s + ds * C::T_BYTES;
       constexpr uint32_t LPR = DC / 4, RPI = 32 / LPR;
       const uint32_t j = lane % LPR, jj = j & 7u;
