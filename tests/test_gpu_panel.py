@@ -145,6 +145,44 @@ def test_panel_nonfinite():
         sg.spmm_hybrid(t, x)
 
 
+def test_panel_nonfinite_dense_columns():
+    # the non-finite row is reached through a dense panel column (4 edges in
+    # the panel): flagged by the tensor-core kernel's epilogue check, also for
+    # rows that have no CUDA-core edges at all
+    n = 200
+    cols = [1, 1, 1, 1]
+    npz = np.array([0, 1, 2, 3, 4] + [4] * (n - 4))
+    g = sg.CsrGraph(n, npz, np.array(cols), np.ones(4, np.float32))
+    t = sg.sgt_transform(g)
+    x = np.zeros((n, 32), np.float32)
+    x[1, 7] = np.inf
+    for prec in ("fp32", "tf32"):
+        with pytest.raises(sg.NonFiniteError):
+            sg.spmm_hybrid(t, x, precision=prec)
+    x[1, 7] = 1.0
+    sg.spmm_hybrid(t, x)  # finite: no error
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32"])
+@pytest.mark.parametrize("order", [0, 1])
+def test_gcn_nonfinite_and_tf32_chain(prec, order):
+    # gcn_forward: the GEMM epilogue checks the output and TF32-rounds the next
+    # SpMM's input (reference order); overflow raises NonFiniteError
+    g = sg.gcn_normalize_values(GRAPHS[0][1])
+    t = sg.sgt_transform(g)
+    n = g.num_nodes
+    x = sg.dense_random(n, 24, 5)
+    w1 = sg.dense_random(24, 24, 6) * np.float32(0.2)
+    w2 = sg.dense_random(24, 16, 7) * np.float32(0.2)
+    got = sg.gcn_forward(t, x, [(w1, True), (w2, False)], precision=prec, order=order)
+    want = O.gcn_forward(oracle_csr(g), x, [(w1, True), (w2, False)], tf32=prec == "tf32")
+    assert mre(got, want) <= (1e-5 if prec == "fp32" else 2e-3)
+    big = np.full((24, 24), 1e38, np.float32)
+    xp = np.abs(x) + np.float32(0.5)  # positive rows: every sum overflows fp32
+    with pytest.raises(sg.NonFiniteError):
+        sg.gcn_forward(t, xp, [(big, True), (w2, False)], precision=prec, order=order)
+
+
 # ------------------------------------------------------------ AGNN, mode 2
 # agnn_panel.cu: tensor-core attention over dense panel columns, CUDA-core
 # attention over sparse edges.  Bars: FP32 <= 1e-5 (as test_gpu_parity.py),
