@@ -229,7 +229,7 @@ void agnn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
       agnn_forward_panel(g, x, ldx, d, L, betas, prec, ws, out, ldo, zero_rows_host, s);
       return;
     }
-    mode = 1;  // outside the panel path's envelope: fused 16-row windows
+    mode = d <= 64 ? 1 : 0;  // outside the panel path's envelope: fused 16-row windows, else the chain
   }
   CU(cudaMemsetAsync(zeros, 0, 8, s));
 
