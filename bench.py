@@ -538,6 +538,8 @@ def run_b200(args, wl):
             u["unit"] = "GB/s"
             u["frac"] = round(u["achieved"] / pk["hbm_gbs"], 4)
             line["roofline_unfused_formula"] = u
+        if "roofline_l2_gather" in extra:
+            line["roofline_l2_gather"] = extra["roofline_l2_gather"]
         if "roofline_gemm" in extra:
             rg = extra["roofline_gemm"]
             rg["peak"] = pk["hbm_gbs"]
@@ -697,7 +699,37 @@ def kernel_breakdown(args, wl, dg, g, h, D, prec, mode, flush, stream, gcn_layer
     roof = {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1), "unit": "GB/s",
             "algorithmic_bytes": int(B), "formula": formula, "kernel_ms": round(t, 4),
             "traffic": None}
+    if mode == 2:
+        extra["roofline_l2_gather"] = l2_gather_roofline(dg, wl, t, prec)
     return res, roof
+
+
+def l2_gather_roofline(dg, wl, t_ms, prec):
+    """The panel kernels fetch feature rows at random from an L2-resident
+    table: bytes moved L2 -> SM per layer (tensor-core chunk tiles, CUDA-core
+    rows, streamed entries / masks) against the measured random-row gather
+    rate (tools/gather_peak.cu, profiles/gather_peak.json)."""
+    pi = dg.panel_info()
+    rb = 4 * (32 if wl["hidden"] <= 32 else 64)  # bytes per gathered row (operand stride)
+    planes = 2 if prec == "fp32" else 1           # FP32: hi/lo planes
+    if wl["kind"] == "agnn":  # z and h tiles + row masks per chunk; rows on the CUDA cores
+        b = pi["dense_chunks"] * (32 * 2 * rb * planes + 128 * 4) + pi["sparse_edges"] * rb
+        what = "chunks x (32 z + 32 h rows + 128 masks) + sparse edges x row"
+    else:                     # B tile per chunk + packed entries; rows on the CUDA cores
+        b = pi["dense_chunks"] * 32 * rb + pi["dense_entries"] * 4 * planes + \
+            pi["sparse_edges"] * (rb + 8)
+        what = "chunks x 32 rows + entries + sparse edges x (row + entry)"
+    try:
+        with open(os.path.join(ROOT, "profiles", "gather_peak.json")) as f:
+            gp = json.load(f)["gather_gbs"]
+        peak = gp["row128_table30MB"] if rb == 128 else gp["row256_table34MB"]
+    except Exception:
+        peak = None
+    ach = b / (t_ms * 1e-3) / 1e9
+    return {"bound": "l2-gather", "bytes": int(b), "formula": what, "achieved": round(ach, 1),
+            "unit": "GB/s", "peak": peak, "frac": round(ach / peak, 4) if peak else None,
+            "peak_source": "profiles/gather_peak.json (tools/gather_peak.cu, random rows, "
+                           "L2-resident table)"}
 
 
 def e2e_host(wl, dg, h, prec, mode, L, layers_per_step, gcn_layers, flush, args):
