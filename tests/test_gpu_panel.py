@@ -183,6 +183,19 @@ def test_gcn_nonfinite_and_tf32_chain(prec, order):
         sg.gcn_forward(t, xp, [(big, True), (w2, False)], precision=prec, order=order)
 
 
+def test_agnn_default_mode_fallbacks():
+    # the default (mode 2) falls back to fused 16-row windows for |beta| > 40
+    # and to the kernel chain for d > 64; results stay within the FP32 bar
+    g = GRAPHS[0][1]
+    t = sg.sgt_transform(g)
+    ga = Csr.of(g.num_nodes, g.node_pointer, g.edge_list)
+    for d, betas in ((80, [1.0, 0.5]), (32, [60.0])):
+        x = sg.dense_random(g.num_nodes, d, d)
+        want, _ = O.agnn_forward(ga, x, betas)
+        got = sg.agnn_forward(t, x, betas)
+        assert mre(got, want) <= 1e-5, (d, betas)
+
+
 # ------------------------------------------------------------ AGNN, mode 2
 # agnn_panel.cu: tensor-core attention over dense panel columns, CUDA-core
 # attention over sparse edges.  Bars: FP32 <= 1e-5 (as test_gpu_parity.py),
