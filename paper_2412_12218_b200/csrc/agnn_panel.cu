@@ -65,7 +65,9 @@ struct AgnnCfg {
   static constexpr bool PT = !F32 && DC == 32;
   static constexpr int NSB = PT ? 3 : 2;                   // S buffers (chunk pairs)
   static constexpr int NB = F32 ? (DC == 32 ? 4 : 2) : (PT ? 8 : 6);  // gather ring (even: S pairs)
-  static constexpr int NP = PT ? 4 : 2;  // P slots in smem; PT: pfull barriers only
+  // P slots in smem; PT: pfull barriers only, one per chunk the softmax can
+  // run ahead of the MMA issuer (S can be up to NSB groups ahead)
+  static constexpr int NP = PT ? 8 : 2;
   static constexpr uint32_t O_COL = NSB * 64;
   static constexpr int NF = PT ? 2 : (DC == 32 ? 4 : 2);
   static constexpr uint32_t TMEM_COLS = 256;
