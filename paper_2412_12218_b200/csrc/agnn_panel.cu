@@ -864,8 +864,8 @@ void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, cons
                       const float* hq, const float* hq1, uint64_t ldq, const float* norm,
                       uint64_t d, float beta, int prec, float* opart, float* lpart, float* seg_o,
                       float* seg_l, float* osp, float* lsp, const AgnnNext& nx, cudaStream_t s) {
-  const Panels& pn = *g->panels;
-  PanelView v = panel_view(g);
+  const Panels& pn = panels_for(g, d);
+  PanelView v = panel_view(g, d);
   const uint64_t ro = g->row_offset;
   const int dbg = panel_debug_mode();  // 1: dense part only, 2: sparse part only (timing)
   static const bool serial = std::getenv("SGTK_AGNN_SERIAL") != nullptr;

@@ -127,7 +127,7 @@ uint64_t agnn_workspace_chain(const sgtk_graph* g, uint64_t d) {
 uint64_t agnn_workspace_panel(const sgtk_graph* g, uint64_t d) {
   if (!g->panels || d > 64) return 0;
   const uint64_t ldq = d <= 32 ? 32 : 64;
-  const auto& pn = *g->panels;
+  const auto& pn = panels_for(g, d);
   return 10 * align256(g->n_cols * ldq * 4) + 2 * align256(g->n_cols * 4) +
          align256(g->n_cols * 4) + 2 * align256(g->n_rows * ld4(d) * 4) +
          2 * align256(g->n_rows * ldq * 4) + 2 * align256(g->n_rows * 4) +
@@ -146,7 +146,7 @@ void agnn_forward_panel(const sgtk_graph* g, const float* x, uint64_t ldx, uint6
                         uint64_t* zero_rows_host, cudaStream_t s) {
   const uint64_t N = g->n_rows, NC = g->n_cols;
   const uint64_t ldq = d <= 32 ? 32 : 64, ldb = ld4(d);
-  const auto& pn = *g->panels;
+  const auto& pn = panels_for(g, d);
   char* p = static_cast<char*>(ws);
   auto take = [&](uint64_t bytes) {
     float* r = reinterpret_cast<float*>(p);

@@ -50,7 +50,9 @@ struct Windows {
 // cores.  This is the density-aware hybrid split of SURVEY §8f rank 3.
 constexpr int kPanelRows = 128;
 constexpr int kChunkCols = 32;
-constexpr uint32_t kDenseMin = 2;
+constexpr uint32_t kDenseMin = 2;     // panels: tensor-core columns have >= 2 edges
+constexpr uint32_t kDenseMin32 = 3;   // panels32: the d <= 32 kernels' cheaper CUDA-core edge
+                                      // makes 2-edge columns cheaper there
 constexpr uint32_t kSegEdges = 512;       // sparse edges per CUDA-core work item
 
 struct Panels {
@@ -125,7 +127,8 @@ struct sgtk_graph {
   uint64_t T8 = 0, T16 = 0;
   std::shared_ptr<sgtkcu::DevBuf> toff8, bm8, toff16, bm16;
   sgtkcu::UnitPlan plan8, plan16;
-  std::shared_ptr<sgtkcu::Panels> panels;  // 128-row panel format (panel.cu)
+  std::shared_ptr<sgtkcu::Panels> panels;    // 128-row panel format (panel.cu), kDenseMin
+  std::shared_ptr<sgtkcu::Panels> panels32;  // same at kDenseMin32: operations with d <= 32
 
   // workspace for host-buffer entry points and forwards (mutable scratch)
   mutable std::shared_ptr<sgtkcu::DevBuf> scratch;

@@ -70,7 +70,9 @@ void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, cons
 void agnn_input_launch(const float* x, uint64_t ldx, uint64_t rows, uint64_t d, uint64_t ldq, int prec,
                        float* z, float* zq, float* zq1, float* hq, float* hq1, float* norm,
                        uint64_t* zeros, cudaStream_t s);
-PanelView panel_view(const sgtk_graph* g);
+// The panel format an operation of width d runs on (panels32 for d <= 32).
+const Panels& panels_for(const sgtk_graph* g, uint64_t d);
+PanelView panel_view(const sgtk_graph* g, uint64_t d);
 void panel_debug_set(int mode);
 int panel_debug_mode();
 bool panel_enabled();

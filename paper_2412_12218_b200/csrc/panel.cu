@@ -68,10 +68,10 @@ __global__ void panel_count_kernel(const uint32_t* __restrict__ e2r, const uint3
     atomicAdd(cnt + wo[e2r[e] / kPanelRows] + e2c[e], 1u);
 }
 
-__global__ void dense_flag_kernel(uint32_t* __restrict__ cnt, uint64_t U) {
+__global__ void dense_flag_kernel(uint32_t* __restrict__ cnt, uint64_t U, uint32_t dense_min) {
   for (uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; u <= U;
        u += uint64_t(gridDim.x) * blockDim.x)
-    cnt[u] = (u < U && cnt[u] >= kDenseMin) ? 1u : 0u;
+    cnt[u] = (u < U && cnt[u] >= dense_min) ? 1u : 0u;
 }
 
 __global__ void panel_dcount_kernel(const uint64_t* __restrict__ wo, const uint32_t* __restrict__ grank,
@@ -927,7 +927,8 @@ void launch_sparse(const Panels& pn, const uint2* sent, const float* x, uint64_t
 }  // namespace
 
 // ---------------------------------------------------------------- builder
-void build_panels(sgtk_graph& g, cudaStream_t s) {
+namespace {
+std::shared_ptr<Panels> build_panel_format(sgtk_graph& g, uint32_t dense_min, cudaStream_t s) {
   auto pn = std::make_shared<Panels>();
   const uint64_t n = g.n_rows, E = g.nnz;
   const uint64_t P = (n + kPanelRows - 1) / kPanelRows;
@@ -942,7 +943,7 @@ void build_panels(sgtk_graph& g, cudaStream_t s) {
   CU(cudaMemsetAsync(flag.p, 0, (U + 1) * 4, s));
   if (E) panel_count_kernel<<<grid_for(E, 256), 256, 0, s>>>(e2r, e2c, wo, E, flag.as<uint32_t>());
   CU_LAUNCH("panel_count_kernel");
-  dense_flag_kernel<<<grid_for(U + 1, 256), 256, 0, s>>>(flag.as<uint32_t>(), U);
+  dense_flag_kernel<<<grid_for(U + 1, 256), 256, 0, s>>>(flag.as<uint32_t>(), U, dense_min);
   CU_LAUNCH("dense_flag_kernel");
   exclusive_scan_u32(flag.as<uint32_t>(), grank.as<uint32_t>(), U + 1, s);
 
@@ -1056,14 +1057,27 @@ void build_panels(sgtk_graph& g, cudaStream_t s) {
   pn->items = ul(items.data(), items.size(), s);
   pn->lrows = ul(lrows.data(), lrows.size(), s);
   CU(cudaStreamSynchronize(s));
-  g.panels = pn;
+  return pn;
+}
+}  // namespace
+
+// Two panel formats per graph, differing only in the dense-column threshold:
+// measured, 2-edge columns are cheaper on the CUDA cores for d <= 32 (AGNN
+// C4 -2%, SpMM d = 32 -2%) and on the tensor cores for d = 64 (+3% otherwise).
+void build_panels(sgtk_graph& g, cudaStream_t s) {
+  g.panels = build_panel_format(g, kDenseMin, s);
+  g.panels32 = build_panel_format(g, kDenseMin32, s);
+}
+
+const Panels& panels_for(const sgtk_graph* g, uint64_t d) {
+  return d <= 32 && g->panels32 ? *g->panels32 : *g->panels;
 }
 
 void panel_debug_set(int mode) { g_panel_debug.store(mode, std::memory_order_relaxed); }
 int panel_debug_mode() { return panel_debug(); }
 
-PanelView panel_view(const sgtk_graph* g) {
-  const Panels& pn = *g->panels;
+PanelView panel_view(const sgtk_graph* g, uint64_t d) {
+  const Panels& pn = panels_for(g, d);
   PanelView v{};
   v.n_rows = g->n_rows;
   v.P = pn.P;
@@ -1094,8 +1108,8 @@ bool spmm_panel_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64
   if (!g->panels || !panel_enabled()) return false;
   if (ldx % 4 != 0 || reinterpret_cast<uintptr_t>(x) % 16 != 0) return false;
   if (g->n_rows == 0 || d == 0) return true;
-  PanelView v = panel_view(g);
-  const Panels& pn = *g->panels;
+  PanelView v = panel_view(g, d);
+  const Panels& pn = panels_for(g, d);
   {
     PanelSmem L;
     const bool fits = (d <= 32 ? (prec == SGTK_FP32 ? panel_smem<32, SGTK_FP32>(pn.max_chunk_entries, L)
