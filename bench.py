@@ -407,7 +407,7 @@ def run_b200(args, wl):
             return D.gemm(agnn_stack(hh), w_out, relu=False, precision=prec)
 
         if mode == 2:
-            pi = dg.panel_info()
+            pi = dg.panel_info(d)
             # input kernel, then per layer: dense + rows + final (+ hub rows)
             launches_per_step = 1 + L * (3 + (1 if pi["long_rows"] else 0))
         else:
@@ -527,7 +527,7 @@ def run_b200(args, wl):
                 if wl["kind"] == "agnn" else f"gcn_forward({L} layers); value = step/{L}",
                 "tiles16x8": int(bs[0]), "tile_density16x8": round(bs[3], 4),
                 "translate_ms": round(translate_ms, 2),
-                "panel_format": dg.panel_info() if mode == 2 else None}),
+                "panel_format": dg.panel_info(wl["hidden"]) if mode == 2 else None}),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
             "model_forward_ms": round(model_ms, 4), "kernels_ms": kern,
@@ -709,7 +709,7 @@ def l2_gather_roofline(dg, wl, t_ms, prec):
     table: bytes moved L2 -> SM per layer (tensor-core chunk tiles, CUDA-core
     rows, streamed entries / masks) against the measured random-row gather
     rate (tools/gather_peak.cu, profiles/gather_peak.json)."""
-    pi = dg.panel_info()
+    pi = dg.panel_info(wl["hidden"])
     rb = 4 * (32 if wl["hidden"] <= 32 else 64)  # bytes per gathered row (operand stride)
     planes = 2 if prec == "fp32" else 1           # FP32: hi/lo planes
     if wl["kind"] == "agnn":  # z and h tiles + row masks per chunk; rows on the CUDA cores

@@ -134,6 +134,10 @@ int sgtk_graph_download(const sgtk_graph* g, uint32_t* edge_to_row,
  * info = {panels, dense_chunks, dense_entries (padded), sparse_edges,
  *         max_chunk_entries, dense_columns (padded), hub_rows, hub_segments} */
 int sgtk_panel_info(const sgtk_graph* g, uint64_t info[8]);
+/* The same for the format an operation of feature width d runs on: d <= 32
+ * uses a second format whose tensor-core columns need >= 3 edges in the
+ * panel (sgtk_panel_info / sgtk_panel_download describe the >= 2 one). */
+int sgtk_panel_info_for(const sgtk_graph* g, uint64_t d, uint64_t info[8]);
 
 /* Timing experiments only: 0 = normal; 1 = tensor-core (dense) part of the
  * panel kernels only; 2 = CUDA-core (sparse) part only (partial results). */

@@ -84,6 +84,7 @@ _SIGS = {
     "sgtk_graph_info": [vp, vp],
     "sgtk_graph_device_ptrs": [vp, vp],
     "sgtk_panel_info": [vp, vp],
+    "sgtk_panel_info_for": [vp, u64, vp],
     "sgtk_debug_set": [C.c_int],
     "sgtk_panel_download": [vp, vp, vp, vp, vp, vp, vp],
     "sgtk_graph_download": [vp, vp, vp, vp, vp, vp],

@@ -147,6 +147,16 @@ int sgtk_graph_info(const sgtk_graph* g, uint64_t info[11]) {
   });
 }
 
+int sgtk_panel_info_for(const sgtk_graph* g, uint64_t d, uint64_t info[8]) {
+  return guard([&] {
+    check_graph(g);
+    const auto& p = sgtkcu::panels_for(g, d);
+    const uint64_t v[8] = {p.P, p.n_chunks, p.n_dent, p.n_sparse, p.max_chunk_entries,
+                           p.n_chunks * 32, p.n_long, p.n_segs};
+    std::memcpy(info, v, sizeof v);
+  });
+}
+
 int sgtk_panel_info(const sgtk_graph* g, uint64_t info[8]) {
   return guard([&] {
     check_graph(g);

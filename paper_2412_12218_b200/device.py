@@ -154,10 +154,14 @@ class DeviceGraph:
         out["block_counter"] = np.array(i.block_counter, np.uint64)
         return out
 
-    def panel_info(self) -> dict:
-        """128-row panel format sizes (sgtk_panel_info)."""
+    def panel_info(self, d: int | None = None) -> dict:
+        """128-row panel format sizes (sgtk_panel_info); with d, of the format
+        an operation of width d runs on (sgtk_panel_info_for)."""
         a = np.zeros(8, np.uint64)
-        check(lib().sgtk_panel_info(self._h, a.ctypes.data))
+        if d is None:
+            check(lib().sgtk_panel_info(self._h, a.ctypes.data))
+        else:
+            check(lib().sgtk_panel_info_for(self._h, u64(d), a.ctypes.data))
         return dict(zip(("panels", "dense_chunks", "dense_entries", "sparse_edges",
                          "max_chunk_entries", "dense_columns", "long_rows", "segments"),
                         (int(v) for v in a)))
