@@ -328,11 +328,14 @@ def run_b200(args, wl):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     prec = args.precision
-    mode = {"panel": 2, "fused": 1, "chain": 0}[args.mode]
+    mode = {"panel": 2, "fused": 1, "chain": 0, "auto": -1}[args.mode]
 
     t0 = time.perf_counter()
     g, gen = make_graph(wl, args.locality)
     N = g.num_nodes
+    if mode < 0:  # the library's AGNN auto mode (forward.cu): panels from 2M edges, else fused
+        mode = 2 if (wl["kind"] == "gcn" or g.num_edges >= (2 << 20) or wl["hidden"] > 64) else 1
+        args.mode = {2: "panel", 1: "fused"}[mode] + " (auto)"
     log(f"[bench] graph {N} nodes {g.num_edges} edges in {time.perf_counter() - t0:.1f}s")
     # row partition in whole 128-row panels (balanced by edges)
     Q = 128
@@ -786,7 +789,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="reddit-agnn", choices=sorted(WORKLOADS))
     ap.add_argument("--precision", default="tf32", choices=["fp32", "tf32"])
-    ap.add_argument("--mode", default="panel", choices=["panel", "fused", "chain"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "panel", "fused", "chain"])
     ap.add_argument("--locality", default="calibrated", choices=sorted(LOCALITY))
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     args = ap.parse_args()

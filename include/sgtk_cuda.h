@@ -249,8 +249,9 @@ uint64_t sgtk_gcn_workspace(const sgtk_graph* g, uint32_t num_layers,
  * mode 2 = 128-row panels: tensor-core attention over each panel's dense
  * columns + CUDA-core attention over its singleton columns, concurrently,
  * next layer's l2 norm fused (falls back to mode 1 for |beta| > 40 or an
- * explicit partial plan, to mode 0 for d > 64).  The Python API and the C++
- * drop-in default to mode 2.
+ * explicit partial plan, to mode 0 for d > 64); mode 3 = auto: mode 2 for
+ * graphs with >= 2M edges, else mode 1 (one launch per layer wins on small
+ * graphs).  The Python API and the C++ drop-in default to mode 3.
  * zero_rows_host (may be NULL) receives the zero-norm row count (syncs). */
 int sgtk_agnn_forward(const sgtk_graph* g, const float* x_dev, uint64_t ldx,
                       uint64_t d, uint32_t num_layers, const float* betas_host,

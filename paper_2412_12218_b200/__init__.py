@@ -258,7 +258,7 @@ def gcn_forward(t: TransformedGraph, x, layers, plan: HybridSplitPlan | None = N
 
 
 def agnn_forward(t: TransformedGraph, x, betas, plan: HybridSplitPlan | None = None,
-                 precision="fp32", threads: int = 0, mode: int = 2, return_zeros=False):
+                 precision="fp32", threads: int = 0, mode: int = 3, return_zeros=False):
     x = _mat(x)
     if x.shape[0] != t.csr.num_nodes:
         raise ShapeError("agnn_forward: x.rows != num_nodes")

@@ -386,7 +386,7 @@ SGTK_EXPORT DenseMatrix agnn_forward(const TransformedGraph& t, const DenseMatri
     auto cut = upload_cut(t, plan);
     // panel mode (tcgen05 + CUDA cores, agnn_panel.cu); outside its envelope
     // (|beta| > 40, d > 64, partial plans) it falls back to the fused 16-row mode
-    const int mode = x.cols <= 64 ? 2 : 0;
+    const int mode = 3;  // auto: panels, fused windows for small graphs, the chain for d > 64
     ck(sgtk_agnn_forward(dg, xd.p, x.cols, x.cols, uint32_t(layers.size()), betas.data(),
                          cut ? cut->p : nullptr, prec_of(prec), mode, ws.p, wsb, od.p, x.cols,
                          &zeros, nullptr));

@@ -273,7 +273,7 @@ class DeviceGraph:
                                      u64(out.stride(0)), _stream()))
         return out
 
-    def agnn_forward(self, x, betas, cut=None, precision="fp32", mode=2, return_zeros=False):
+    def agnn_forward(self, x, betas, cut=None, precision="fp32", mode=3, return_zeros=False):
         _f32_2d(x, "x")
         if x.shape[0] != self.num_cols:  # == num_nodes unless a row slice (full replica in)
             raise ShapeError("agnn_forward: x.rows != num_nodes")

@@ -184,7 +184,7 @@ def test_gcn_nonfinite_and_tf32_chain(prec, order):
 
 
 def test_agnn_default_mode_fallbacks():
-    # the default (mode 2) falls back to fused 16-row windows for |beta| > 40
+    # mode 2 (and the auto default) falls back to fused 16-row windows for |beta| > 40
     # and to the kernel chain for d > 64; results stay within the FP32 bar
     g = GRAPHS[0][1]
     t = sg.sgt_transform(g)
@@ -192,8 +192,9 @@ def test_agnn_default_mode_fallbacks():
     for d, betas in ((80, [1.0, 0.5]), (32, [60.0])):
         x = sg.dense_random(g.num_nodes, d, d)
         want, _ = O.agnn_forward(ga, x, betas)
-        got = sg.agnn_forward(t, x, betas)
-        assert mre(got, want) <= 1e-5, (d, betas)
+        for mode in (2, 3):
+            got = sg.agnn_forward(t, x, betas, mode=mode)
+            assert mre(got, want) <= 1e-5, (d, betas, mode)
 
 
 # ------------------------------------------------------------ AGNN, mode 2
