@@ -52,6 +52,8 @@ WORKLOADS = {
                         d_out=3, layers=4, cfg="C2"),
     "proteins-gcn": dict(n=132534, e=39_561_252, alpha=0.0, kind="gcn", d_in=64, hidden=64,
                          d_out=64, layers=2, cfg="C3"),
+    "proteins16-gcn": dict(n=132534, e=39_561_252, alpha=0.0, kind="gcn", d_in=16, hidden=16,
+                           d_out=16, layers=2, cfg="C3 (d=16)"),
     "cora-gcn": dict(n=2708, e=10556 + 2708, alpha=0.0, kind="gcn", d_in=1433, hidden=16,
                      d_out=7, layers=2, cfg="C1"),
     "powerlaw-gcn": dict(n=10_000_000, e=1_000_000_000, alpha=2.0, kind="gcn", d_in=128,

@@ -87,7 +87,9 @@ struct AgnnCfg {
   static_assert(SMEM <= 227u * 1024u, "agnn panel smem");
 };
 
-__device__ __align__(16) float g_agnn_zero[64];
+// Zero rows for the padding columns of a panel's last chunk, one 16-byte
+// piece per (chunk row, lane piece): distinct addresses, no hot spot.
+__device__ __align__(16) float g_agnn_zero[32 * 64];
 
 // K-major SWIZZLE_128B offset of element (row, k) in a tile with `rows` rows:
 // 128-byte K blocks of 32 fp32, rows*128 bytes apart.
@@ -382,7 +384,9 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       for (uint32_t t = 0; t < 32 / RPI; ++t) {
         const uint32_t k = t * RPI + lane / LPR;  // chunk row (B row / K row)
         const uint32_t ck = __shfl_sync(0xFFFFFFFFu, col, k);
-        const bool real = ck != 0xFFFFFFFFu && int(4 * j) < dvalid;
+        // operand rows are ldq wide with zero padding features in memory, so
+        // only padding chunk columns take the zero source (distinct pieces)
+        const bool real = ck != 0xFFFFFFFFu;
         const uint64_t gofs = uint64_t(ck) * ld + 4 * j;
         // z: K-major SWIZZLE_128B, row k, 16-byte piece j; K block j>>3 of slot ds
         const uint32_t zo = ((j >> 3) * C::NB + ds) * 4096u + (k >> 3) * 1024u + (k & 7u) * 128u +
@@ -390,11 +394,11 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
         // h: MN-major SWIZZLE_128B_BASE32B (tc05.cuh desc_mn32)
         const uint32_t ho = (j >> 3) * 4096u + (k >> 2) * 512u + (k & 3u) * 128u +
                             ((((jj >> 1) ^ (k & 3u)) << 5) | ((jj & 1u) << 4));
-        cp_async16(zr_s + zo, real ? z + gofs : g_agnn_zero);
-        cp_async16(ht + ho, real ? h + gofs : g_agnn_zero);
+        cp_async16(zr_s + zo, real ? z + gofs : g_agnn_zero + (k * LPR + j) * 4);
+        cp_async16(ht + ho, real ? h + gofs : g_agnn_zero + (k * LPR + j) * 4);
         if constexpr (C::F32) {  // lo planes (pre-split once per layer)
-          cp_async16(zr_s + C::KB * C::NB * 4096u + zo, real ? z1 + gofs : g_agnn_zero);
-          cp_async16(ht + C::NB * C::T_BYTES + ho, real ? h1 + gofs : g_agnn_zero);
+          cp_async16(zr_s + C::KB * C::NB * 4096u + zo, real ? z1 + gofs : g_agnn_zero + (k * LPR + j) * 4);
+          cp_async16(ht + C::NB * C::T_BYTES + ho, real ? h1 + gofs : g_agnn_zero + (k * LPR + j) * 4);
         }
       }
       cp_async16(mr_s + ds * C::M_BYTES + lane * 16, pv.dmask + (uint64_t(c0 + c) * kPanelRows) + lane * 4);

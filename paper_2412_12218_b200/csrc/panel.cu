@@ -343,9 +343,6 @@ struct PanelSmem {
   uint32_t bring_off, dring_off, total;
 };
 
-// Source of the zero rows that pad a panel's last chunk (cp.async needs a
-// global address; 256 B covers a 64-feature slice).
-__device__ __align__(16) float g_zero_row[64];
 // Zeros for an A stage (up to 2 planes x 16 KB), copied in by the TMA engine.
 __device__ __align__(128) uint32_t g_zero_tile[2 * kPanelRows * kChunkCols];
 
@@ -534,7 +531,11 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
         // XOR (k % 4)
         const uint32_t dst = bst + (j >> 3) * 4096u + (k >> 2) * 512u + (k & 3u) * 128u +
                              ((((jj >> 1) ^ (k & 3u)) << 5) | ((jj & 1u) << 4));
-        cp_async16(dst, real ? x + uint64_t(ck) * ldx + fbase + 4 * j : g_zero_row);
+        // zeros (padding columns / features) from distinct 16-byte pieces: a
+        // single zero source would serialise every CTA's padding copies on
+        // one address (d = 16: 6x slower)
+        cp_async16(dst, real ? x + uint64_t(ck) * ldx + fbase + 4 * j
+                             : reinterpret_cast<const float*>(g_zero_tile) + (k * LPR + j) * 4);
       }
       cp_async_arrive_noinc(bfull + ds);
     };
