@@ -368,7 +368,11 @@ __device__ __align__(128) uint32_t g_zero_tile[2 * kPanelRows * kChunkCols];
 //               into fp32 registers in group order (IEEE adds keep every
 //               tensor-core accumulation chain <= FOLD chunks), store.
 // ---------------------------------------------------------------------------
-template <int DC, int PREC>
+// PAD: the feature slice is narrower than DC (d % DC != 0): the B ring's
+// padding features are zeroed once and never copied (copying zeros for them
+// from one source keeps a few L2 lines hot across all CTAs: d = 16 0.27 ms
+// against 0.23 ms this way; used for DC = 32 only, see launch_dense)
+template <int DC, int PREC, bool PAD>
 __global__ void __launch_bounds__(kPanelThreads, PanelCfg<DC, PREC>::CTAS)
 spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict__ x, uint64_t ldx,
                   uint64_t d, float* __restrict__ out, uint64_t ldo, int vec_out,
@@ -423,6 +427,12 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
     mbar_init_fence();
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if constexpr (PAD) {
+    const uint32_t rb = smem_u32(bring);
+    for (uint32_t i = threadIdx.x; i < ND * C::B_STAGE / 16; i += blockDim.x)
+      st_shared_v4(rb + i * 16, 0u, 0u, 0u, 0u);
+    fence_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -534,8 +544,9 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
         // zeros (padding columns / features) from distinct 16-byte pieces: a
         // single zero source would serialise every CTA's padding copies on
         // one address (d = 16: 6x slower)
-        cp_async16(dst, real ? x + uint64_t(ck) * ldx + fbase + 4 * j
-                             : reinterpret_cast<const float*>(g_zero_tile) + (k * LPR + j) * 4);
+        if (!PAD || int(4 * j) < dvalid)
+          cp_async16(dst, real ? x + uint64_t(ck) * ldx + fbase + 4 * j
+                               : reinterpret_cast<const float*>(g_zero_tile) + (k * LPR + j) * 4);
       }
       cp_async_arrive_noinc(bfull + ds);
     };
@@ -854,7 +865,9 @@ bool launch_dense(const PanelView& v, uint64_t P, uint32_t max_entries, const fl
   if (!panel_smem<DC, PREC>(max_entries, L)) return false;
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(spmm_panel_kernel<DC, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(spmm_panel_kernel<DC, PREC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kSmemCap));
+    cudaFuncSetAttribute(spmm_panel_kernel<DC, PREC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(kSmemCap));
   });
   dim3 grid(unsigned(P), unsigned((d + DC - 1) / DC));
@@ -868,8 +881,14 @@ bool launch_dense(const PanelView& v, uint64_t P, uint32_t max_entries, const fl
     }
     return t;
   }();
-  spmm_panel_kernel<DC, PREC><<<grid, kPanelThreads, L.total, s>>>(v, L, x, ldx, d, out, ldo,
-                                                                   vec_out, nonfinite, trace);
+  // PAD measured: d = 8/16/24 0.28/0.27/0.25 -> 0.22/0.23/0.23 ms; at d = 48
+  // (DC = 64) copying the zero features stays faster (0.34 vs 0.38 ms)
+  if (DC == 32 && d % DC)
+    spmm_panel_kernel<DC, PREC, true><<<grid, kPanelThreads, L.total, s>>>(v, L, x, ldx, d, out, ldo,
+                                                                         vec_out, nonfinite, trace);
+  else
+    spmm_panel_kernel<DC, PREC, false><<<grid, kPanelThreads, L.total, s>>>(v, L, x, ldx, d, out, ldo,
+                                                                          vec_out, nonfinite, trace);
   if (trace) {
     std::vector<long long> h(4 * 256 * 8);
     cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost);

@@ -10,12 +10,13 @@ ap.add_argument("--precision", default="tf32")
 ap.add_argument("--mode", type=int, default=2)
 ap.add_argument("--layers", type=int, default=4)
 ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--d", type=int, default=0, help="feature width (default: the workload's)")
 a = ap.parse_args()
 wl = bench.WORKLOADS[a.workload]
 g, _ = bench.make_graph(wl, "calibrated")
 dg = DeviceGraph.from_csr(g.node_pointer, g.edge_list)
 print(dg.panel_info(), flush=True)
-x = torch.from_numpy(sg.dense_random(g.num_nodes, wl["hidden"], 3)).cuda()
+x = torch.from_numpy(sg.dense_random(g.num_nodes, a.d or wl["hidden"], 3)).cuda()
 betas = np.ones(a.layers, np.float32)
 for _ in range(a.iters):
     dg.agnn_forward(x, betas, precision=a.precision, mode=a.mode)
