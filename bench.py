@@ -563,7 +563,9 @@ def profiled_traffic(kernel_field):
 
     names = [k.strip() for k in kernel_field.split("(")[-1].rstrip(")").split("+")] \
         if "(" in kernel_field else [kernel_field]
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_launches.csv")), key=os.path.getmtime)
+    # newest round last: tags r1_, r1b, ..., r1h sort by name (mtimes do not
+    # survive the copy to the GPU box)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_launches.csv")))
     for path in reversed(files):
         try:
             with open(path, newline="") as f:
