@@ -514,7 +514,7 @@ def run_b200(args, wl):
 
     pk, pk_src = peaks()
     if roof:
-        roof["traffic"] = profiled_traffic(roof["kernel"])
+        roof["traffic"] = profiled_traffic(roof["kernel"], gcn=wl["kind"] == "gcn")
         roof["peak"] = pk["hbm_gbs"]
         roof["frac"] = round(roof["achieved"] / pk["hbm_gbs"], 4)
         roof["peak_source"] = f"MEASURED_PEAKS.json hbm_gbs ({pk_src})"
@@ -555,7 +555,7 @@ def run_b200(args, wl):
         dist.destroy_process_group()
 
 
-def profiled_traffic(kernel_field):
+def profiled_traffic(kernel_field, gcn=False):
     """DRAM bytes (read + write) per launch of the roofline kernel(s), from the
     committed ncu launch list of this code (profiles/*_launches.csv, written by
     tools/profile_round.sh + tools/ncu_summary.py); None if not profiled."""
@@ -566,6 +566,8 @@ def profiled_traffic(kernel_field):
     # newest round last: tags r1_, r1b, ..., r1h sort by name (mtimes do not
     # survive the copy to the GPU box)
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_launches.csv")))
+    # the GCN workload's launch list is *_gcn_launches.csv (tools/profile_round.sh)
+    files = [f for f in files if f.endswith("_gcn_launches.csv") == gcn]
     for path in reversed(files):
         try:
             with open(path, newline="") as f:

@@ -6,6 +6,9 @@ tag=${1:-r1}
 mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launches_${tag}.csv python bench.py --steps 2 --warmup 3 --no-cpu > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file gpurun_out/launches_${tag}_gcn.csv python bench.py --steps 2 --warmup 3 --no-cpu \
+    --workload proteins-gcn > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on \
     -k regex:"agnn_dense_kernel|agnn_rows_kernel|spmm_panel_kernel|sparse_rows_kernel|gemm_tc05_kernel" -c 6 \
     -o gpurun_out/prof_${tag} python bench.py --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1
