@@ -1,0 +1,87 @@
+"""Parity at the bench's full sizes (BASELINE.json C4 and C3): the GPU result
+for a random sample of rows against an exact float64 evaluation of those rows
+(the oracle path is too slow at 114M edges; these rows' neighbourhoods are
+not).  Same bars as test_gpu_parity.py: FP32 <= 1e-5 max_rel_err, TF32
+<= 2e-3 for AGNN and the componentwise TF32 bound for SpMM."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _graph(name):
+    import bench
+
+    g, _ = bench.make_graph(bench.WORKLOADS[name], "calibrated")
+    return g
+
+
+def _sample(n, k=96, seed=0):
+    rng = np.random.default_rng(seed)
+    return np.unique(np.concatenate([rng.integers(0, n, k), [0, n - 1]]))
+
+
+@pytest.mark.parametrize("prec,bar", [("fp32", 1e-5), ("tf32", 2e-3)])
+def test_agnn_c4_sampled_rows(prec, bar):
+    import paper_2412_12218_b200 as sg
+    from paper_2412_12218_b200.device import DeviceGraph
+
+    g = _graph("reddit-agnn")
+    n = g.num_nodes
+    npz = g.node_pointer.astype(np.int64)
+    el = g.edge_list.astype(np.int64)
+    x = sg.dense_random(n, 32, 11)
+    dg = DeviceGraph.from_csr(g.node_pointer, g.edge_list)
+    beta = 0.8
+    out = dg.agnn_forward(torch.from_numpy(x).cuda(), [beta], precision=prec, mode=2).cpu().numpy()
+    h = x.astype(np.float64)
+    nrm = np.linalg.norm(h, axis=1, keepdims=True)
+    z = np.where(nrm > 0, h / np.where(nrm > 0, nrm, 1), 0.0)
+    rows = _sample(n)
+    ref = np.empty((len(rows), 32))
+    for t, i in enumerate(rows):
+        nb = el[npz[i]:npz[i + 1]]
+        lg = beta * (z[nb] @ z[i])
+        a = np.exp(lg - lg.max())
+        ref[t] = (a / a.sum()) @ h[nb]
+    err = np.abs(out[rows] - ref).max() / np.abs(ref).max()
+    assert err <= bar, f"AGNN C4 {prec} sampled max_rel_err {err:.2e}"
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32"])
+def test_spmm_c3_sampled_rows(prec):
+    import paper_2412_12218_b200 as sg
+    from paper_2412_12218_b200.device import DeviceGraph
+
+    g = sg.gcn_normalize_values(_graph("proteins-gcn"))
+    n = g.num_nodes
+    npz = g.node_pointer.astype(np.int64)
+    el = g.edge_list.astype(np.int64)
+    vals = g.values
+    x = sg.dense_random(n, 64, 12)
+    dg = DeviceGraph.from_csr(g.node_pointer, g.edge_list, vals)
+    out = dg.spmm(torch.from_numpy(x).cuda(), precision=prec).cpu().numpy()
+    rows = _sample(n)
+    xd = x.astype(np.float64)
+    ref = np.empty((len(rows), 64))
+    bound = np.empty((len(rows), 64))
+    for t, i in enumerate(rows):
+        a = vals[npz[i]:npz[i + 1]].astype(np.float64)
+        nb = el[npz[i]:npz[i + 1]]
+        ref[t] = a @ xd[nb]
+        bound[t] = np.abs(a) @ np.abs(xd[nb])
+    got = out[rows]
+    if prec == "fp32":
+        err = np.abs(got - ref).max() / np.abs(ref).max()
+        assert err <= 1e-5, f"SpMM C3 fp32 sampled max_rel_err {err:.2e}"
+    else:  # componentwise TF32 bound, both operands rounded
+        lim = 2.0 ** -10 * bound + 1e-6 * np.abs(ref).max()
+        assert np.all(np.abs(got - ref) <= lim), "SpMM C3 tf32 outside the componentwise bound"
