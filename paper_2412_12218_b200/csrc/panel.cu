@@ -701,9 +701,8 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
 // Sparse part on the CUDA cores: one warp per work item (a row's sparse
 // edges, or a <= kSegEdges segment of a hub row), lanes over features
 // (FPL = 1 or 2 consecutive floats per lane: 128- or 256-byte coalesced
-// rows), BATCH / EPI edge rows in flight per lane (small batches keep
-// registers low enough for 4 blocks per SM), edges of a batch broadcast by
-// shuffle.  Direct items continue the row's sum from the dense result in
+// rows), BATCH / EPI = 6 edge rows in flight per lane (measured best
+// against 2..8), edges of a batch broadcast by shuffle.  Direct items continue the row's sum from the dense result in
 // `out` (out = dense + e0 + e1 + ...); segments write partials that
 // long_rows_kernel adds in segment order.  Deterministic throughout.
 // ---------------------------------------------------------------------------
@@ -718,10 +717,10 @@ sparse_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint
   // lane = feature; the EPI partial sums merge by a fixed shuffle tree
   constexpr uint32_t DC = 32 * FPL, LPE = DC / 4, EPI = 32 / LPE;
 #ifndef SGTK_SPARSE_BATCH1
-#define SGTK_SPARSE_BATCH1 16
+#define SGTK_SPARSE_BATCH1 24
 #endif
 #ifndef SGTK_SPARSE_BATCH2
-#define SGTK_SPARSE_BATCH2 8
+#define SGTK_SPARSE_BATCH2 12
 #endif
   // edges per batch (loads in flight per warp: BATCH / EPI float4 per lane)
   constexpr uint32_t BATCH = FPL == 1 ? uint32_t(SGTK_SPARSE_BATCH1) : uint32_t(SGTK_SPARSE_BATCH2);
