@@ -919,7 +919,10 @@ void launch_sparse(const Panels& pn, const uint2* sent, const float* x, uint64_t
   const uint64_t dc = d <= 32 ? 32 : 64;  // features per warp pass
   float* part = nullptr;
   if (pn.n_segs) CU(cudaMallocAsync(reinterpret_cast<void**>(&part), pn.n_segs * dc * 4, s));
-  const unsigned blocks = unsigned(std::min<uint64_t>((pn.n_items + 7) / 8, 148ull * 8));
+#ifndef SGTK_SPARSE_GRID
+#define SGTK_SPARSE_GRID 4
+#endif
+  const unsigned blocks = unsigned(std::min<uint64_t>((pn.n_items + 7) / 8, 148ull * SGTK_SPARSE_GRID));
   for (uint64_t fb = 0; fb < d; fb += dc) {
     const uint4* it = pn.items->as<uint4>();
     if (dc == 32) {
