@@ -318,7 +318,10 @@ struct PanelCfg {
   static constexpr uint32_t B_BYTES = kChunkCols * DC * 4;          // MN-major
   static constexpr uint32_t A_STAGE = PA * A_BYTES;                 // multiple of 1024
   static constexpr uint32_t B_STAGE = PB * B_BYTES;                 // multiple of 1024
-  static constexpr int NS = (PREC == SGTK_FP32 || DC == 64) ? 2 : 4;  // A ring depth
+#ifndef SGTK_NS32
+#define SGTK_NS32 4
+#endif
+  static constexpr int NS = (PREC == SGTK_FP32 || DC == 64) ? 2 : SGTK_NS32;  // A ring depth
   static constexpr int GW = 4 / NS;                                 // builder warps per chunk
   static constexpr int NV = PREC == SGTK_FP32 ? 2 : 1;              // entry (+ value) slots
   // DC = 32 TF32 fits two CTAs per SM (256 TMEM columns, <= 113 KB smem,
@@ -329,7 +332,10 @@ struct PanelCfg {
   // 16 columns at a time: few registers) + NF accumulation buffers
   static constexpr int NF = (TMEM_COLS - DC) / DC;
   static constexpr uint32_t BUF0 = DC;                              // first buffer column
-  static constexpr uint32_t FOLD = 4;                               // chunks per accumulator
+#ifndef SGTK_FOLD
+#define SGTK_FOLD 4
+#endif
+  static constexpr uint32_t FOLD = SGTK_FOLD;                       // chunks per accumulator
 };
 
 constexpr int kPanelThreads = 320;
