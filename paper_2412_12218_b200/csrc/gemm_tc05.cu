@@ -370,7 +370,13 @@ bool gemm_tc05_launch(const float* a, uint64_t lda, const float* w, uint64_t m, 
   const uint32_t num_kc = uint32_t(k_pad / kBK);
   // a ring deeper than the K loop only costs residency: small K (the GCN
   // hidden layers, K = 64) then fits 4 CTAs per SM instead of 2
-  const uint32_t stages = std::max(2u, std::min(std::min(4u, num_kc), (200u * 1024u) / stage_bytes));
+// 3 stages: more CTAs per SM beat a deeper ring (in-proj 602->32: 2-3 stages
+// 0.130 ms, 4 0.134, 6-8 0.16)
+#ifndef SGTK_GEMM_STAGES
+#define SGTK_GEMM_STAGES 3
+#endif
+  const uint32_t stages =
+      std::max(2u, std::min(std::min(uint32_t(SGTK_GEMM_STAGES), num_kc), (200u * 1024u) / stage_bytes));
   const uint32_t tile_bytes = kBM * (n_pad + 4) * 4;  // staged epilogue tile
   const uint32_t region = (std::max(stages * stage_bytes, tile_bytes) + 1023) & ~1023u;
   const size_t smem = size_t(region) + 1024 /*align*/ + 256 /*barriers*/;
