@@ -293,6 +293,37 @@ def run_reference_arm(args, wl):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    if args.csv:
+        blocks = cap = dens = ""
+        try:  # the reference's own transform statistics (block_stats, sgt_transform.cpp:93-100)
+            from oracle.oracle import Csr, RefLib
+
+            R = RefLib()
+            t = R.transform_fields(R.transform_handle(Csr.of(g.num_nodes, g.node_pointer, g.edge_list), 16, 8))
+            blocks = int(t.block_counter)
+            cap = blocks * 16 * 8
+            dens = g.num_edges / cap if cap else 0.0
+        except Exception:
+            pass
+        write_report_csv(args.csv, [dict(dataset=args.workload, kernel=wl["kind"], path="reference-cpu",
+                                         median_ms=round(ms, 4), blocks=blocks, capacity=cap,
+                                         nnz=g.num_edges, density=dens)])
+
+
+CSV_HEADER = "dataset,kernel,path,median_ms,blocks,capacity,nnz,density,max_rel_err"
+
+
+def write_report_csv(path, rows):
+    """The reference bench's report schema (bench.hpp:53-55, bench.cpp:216-227):
+    dataset,kernel,path,median_ms,blocks,capacity,nnz,density,max_rel_err, so
+    the CPU and GPU rows of a run sit side by side.  Appends (header once)."""
+    new = not os.path.exists(path) or os.path.getsize(path) == 0
+    with open(path, "a", newline="") as f:
+        w = csv.writer(f, lineterminator="\n")
+        if new:
+            f.write(CSV_HEADER + "\n")
+        for r in rows:
+            w.writerow([r.get(k, "") for k in CSV_HEADER.split(",")])
 
 
 def metric_name(wl):
@@ -551,6 +582,12 @@ def run_b200(args, wl):
             rg["frac"] = round(rg["achieved"] / pk["hbm_gbs"], 4)
             line["roofline_gemm"] = rg
         print(json.dumps(line), flush=True)
+        if args.csv:  # per layer, like the reference arm's row
+            write_report_csv(args.csv, [dict(dataset=args.workload, kernel=wl["kind"],
+                                             path=f"b200-{args.mode.split()[0]}",
+                                             median_ms=round(statistics.median(step_ts) / layers_per_step, 4),
+                                             blocks=bs[0], capacity=bs[1], nnz=bs[2],
+                                             density=round(bs[3], 6))])
     if world > 1:
         dist.destroy_process_group()
 
@@ -798,6 +835,8 @@ def main():
     ap.add_argument("--mode", default="auto", choices=["auto", "panel", "fused", "chain"])
     ap.add_argument("--locality", default="calibrated", choices=sorted(LOCALITY))
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--csv", default="", help="also append a row in the reference bench's CSV "
+                                               "schema (bench.hpp:53-55) to this file")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
