@@ -776,6 +776,13 @@ inline unsigned rows_grid(uint64_t items, unsigned bs) {
   const uint64_t b = (items * 32 + bs - 1) / bs;
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(b, 148ull * SGTK_ROWS_GRID)));
 }
+#ifndef SGTK_FINAL_GRID
+#define SGTK_FINAL_GRID 16
+#endif
+inline unsigned final_grid(uint64_t items) {  // 4 rows per warp instruction
+  const uint64_t b = (items * 8 + 255) / 256;
+  return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(b, 148ull * SGTK_FINAL_GRID)));
+}
 inline unsigned blocks_for(uint64_t n, unsigned bs = 256) {
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + bs - 1) / bs, 148ull * 16)));
 }
@@ -851,7 +858,7 @@ void launch_agnn_rows(const Panels& pn, const float* zown, const float* z, uint6
     CU(cudaEventRecord(ev, s));
     CU(cudaStreamWaitEvent(s_final, ev, 0));
     if (pn.n_aitems) {
-      agnn_final_kernel<FPL, PREC><<<blocks_for(pn.n_aitems * 32), 256, 0, s_final>>>(
+      agnn_final_kernel<FPL, PREC><<<final_grid(pn.n_aitems), 256, 0, s_final>>>(
           pn.aitems->as<uint4>(), pn.n_aitems, d, opart, lpart, osp, lsp, nx);
       CU_LAUNCH("agnn_final_kernel");
     }
