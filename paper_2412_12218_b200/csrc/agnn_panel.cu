@@ -85,6 +85,7 @@ struct AgnnCfg {
   static constexpr uint32_t P_OFF = (M_OFF + NB * M_BYTES + 1023) / 1024 * 1024;
   static constexpr uint32_t SMEM = P_OFF + (PT ? 0 : NP * PP * P_BYTES) + 1024;
   static_assert(NB % 2 == 0, "S pairs need an even gather ring");
+  static_assert(M_OFF - Z_OFF >= 4u * 32u * (DC + 4) * 4u, "epilogue staging fits the gather rings");
   // S of a chunk pair needs both chunks' gathers while PV still lags: a ring
   // of >= 4 slots; shallower rings compute S chunk by chunk (N = 32)
   static constexpr bool PAIR = NB >= 4;
@@ -279,12 +280,24 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       if (lane == 0) mbar_arrive(accempty + buf);
     }
     named_bar(1, 256);
-    if (grow < pv.n_rows) {
-      float* o = opart + grow * DC;
+    {  // rows staged in shared memory (the gather rings are idle now: every
+       // MMA retired), then written back row-contiguously (coalesced)
+      constexpr uint32_t TSW = DC + 4;  // staged row stride (floats): spreads banks
+      const uint32_t sb = smem_u32(smem + C::Z_OFF) + q * 32u * TSW * 4u;
 #pragma unroll
       for (int j = 0; j < DC / 4; ++j)
-        reinterpret_cast<float4*>(o)[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
-      lpart[grow] = lbuf[r];
+        st_shared_v4(sb + (lane * TSW + 4 * j) * 4, __float_as_uint(acc[4 * j]), __float_as_uint(acc[4 * j + 1]),
+                     __float_as_uint(acc[4 * j + 2]), __float_as_uint(acc[4 * j + 3]));
+      __syncwarp();
+      constexpr uint32_t LPR = DC / 4, RPI = 32 / LPR;
+      const uint64_t row0 = p * kPanelRows + q * 32;
+#pragma unroll
+      for (uint32_t t = 0; t < 32 / RPI; ++t) {
+        const uint32_t rr = t * RPI + lane / LPR, cc = lane % LPR;
+        if (row0 + rr < pv.n_rows)
+          reinterpret_cast<float4*>(opart + (row0 + rr) * DC)[cc] = ld_shared_f4(sb + (rr * TSW + 4 * cc) * 4);
+      }
+      if (grow < pv.n_rows) lpart[grow] = lbuf[r];
     }
   } else if (warp == 8) {
     // ------------------------------------------------------------ MMA issuer
