@@ -210,15 +210,26 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       tmem_ld_wait();
       if (warp == 0 && lane == 0) mark(c, 6);
       tc_fence_before();
-      float pr[32], lq[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      // Blackwell's paired fp32 instructions (FFMA2 / FADD2) take two elements
+      // per issue; same roundings and the same 4 partial sums (j % 4) as the
+      // scalar form, so the results are bit-identical to it
+      float pr[32];
+      float2 lq01 = make_float2(0.0f, 0.0f), lq23 = make_float2(0.0f, 0.0f);
+      const float2 bl2v = make_float2(bl2, bl2), offv = make_float2(-off, -off);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float e = ex2_approx(fmaf(__uint_as_float(sv[j]), bl2, -off));
-        pr[j] = (mask & (1u << j)) ? e : 0.0f;
-        if constexpr (!C::F32) pr[j] = __uint_as_float(tf32_op(pr[j]));  // finite, >= 0
-        lq[j & 3] += pr[j];
+      for (int j = 0; j < 32; j += 2) {
+        const float2 xe = __ffma2_rn(make_float2(__uint_as_float(sv[j]), __uint_as_float(sv[j + 1])), bl2v, offv);
+        const float e0 = ex2_approx(xe.x), e1 = ex2_approx(xe.y);
+        pr[j] = (mask & (1u << j)) ? e0 : 0.0f;
+        pr[j + 1] = (mask & (1u << (j + 1))) ? e1 : 0.0f;
+        if constexpr (!C::F32) {  // finite, >= 0
+          pr[j] = __uint_as_float(tf32_op(pr[j]));
+          pr[j + 1] = __uint_as_float(tf32_op(pr[j + 1]));
+        }
+        if ((j & 3) == 0) lq01 = __fadd2_rn(lq01, make_float2(pr[j], pr[j + 1]));
+        else lq23 = __fadd2_rn(lq23, make_float2(pr[j], pr[j + 1]));
       }
-      l += (lq[0] + lq[1]) + (lq[2] + lq[3]);
+      l += (lq01.x + lq01.y) + (lq23.x + lq23.y);
       if (warp == 0 && lane == 0) mark(c, 5);
       if constexpr (C::PT) {  // P over this chunk's S columns (already read)
         tmem_st32(tmem + ((warp * 32u) << 16) + s_col + sb * 64 + shalf, *reinterpret_cast<uint32_t(*)[32]>(pr));
