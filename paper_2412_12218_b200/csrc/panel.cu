@@ -769,11 +769,14 @@ sparse_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint
         if (u >= cnt) av[k] = 0.0f;
       }
 #pragma unroll
-      for (uint32_t k = 0; k < BATCH / EPI; ++k) {
-        acc[0] = fmaf(av[k], xv[k].x, acc[0]);
-        acc[1] = fmaf(av[k], xv[k].y, acc[1]);
-        acc[2] = fmaf(av[k], xv[k].z, acc[2]);
-        acc[3] = fmaf(av[k], xv[k].w, acc[3]);
+      for (uint32_t k = 0; k < BATCH / EPI; ++k) {  // paired FFMA2: same per-element FMAs
+        const float2 a2 = make_float2(av[k], av[k]);
+        const float2 lo = __ffma2_rn(a2, make_float2(xv[k].x, xv[k].y), make_float2(acc[0], acc[1]));
+        const float2 hi = __ffma2_rn(a2, make_float2(xv[k].z, xv[k].w), make_float2(acc[2], acc[3]));
+        acc[0] = lo.x;
+        acc[1] = lo.y;
+        acc[2] = hi.x;
+        acc[3] = hi.y;
       }
     }
 #pragma unroll
