@@ -3,21 +3,33 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
                     [--workload reddit-agnn|proteins-gcn|pubmed-agnn|cora-gcn|powerlaw-gcn]
-                    [--precision fp32|tf32] [--mode panel|fused|chain] [--locality calibrated|uniform]
+                    [--precision fp32|tf32] [--mode auto|panel|fused|chain]
+                    [--locality calibrated|uniform] [--csv FILE] [--no-cpu] [--no-verify]
 
 Default workload (config C4 of BASELINE.json): AGNN forward on a synthetic
-Reddit-shaped graph (232,965 nodes, ~114.6M edges incl. self-loops; in-proj
-602->32, 4 AGNN layers at d=32, beta=1, out-proj 32->41).  The metric is the
-AGNN *layer-forward* time per graph: one step = the reference API call
-agnn_forward(t, h0, 4 layers) on the whole graph, value = step ms / 4.
-Inputs are resident in HBM; L2 is flushed (256 MB write) between timed steps;
-per-step CUDA events on the launch stream, max over ranks.
+Reddit-shaped graph (232,965 nodes, ~114.6M edges incl. self-loops), 4 AGNN
+layers at d=32, beta=1.  The metric is the AGNN *layer-forward* time per
+graph: one step = the reference API call agnn_forward(t, h0, 4 layers) on the
+whole graph, value = step ms / 4.  h0 = DenseMatrix::random(N, 32, seed+7)
+exactly as the reference's own bench builds its AGNN input
+(/root/reference/proj/src/bench.cpp:128,134-135).  Inputs are resident in HBM;
+L2 is flushed (256 MB write) between timed steps; per-step CUDA events on the
+launch stream, max over ranks.
+
+N GPUs: `--gpus N` without torchrun re-launches itself under
+torch.distributed.run (one process per GPU).  Rows are partitioned by whole
+128-row panels (distributed.RowSlice); each layer ends with one in-place NCCL
+all-gather of the padded embedding replica.  When more ranks than devices are
+visible (a 1-GPU lease exercising the N>1 path) ranks share the devices and
+exchange over gloo.
 
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref/libsgtk_ref.so, compiled unmodified from /root/reference; the
-oracle restatement if that .so is absent) on this host's cores: one step =
-one AGNN layer through the reference's public functions (l2_normalize_rows,
-sddmm_hybrid on reblock(t,16), edge_softmax, spmm_hybrid; gnn.cpp:107-116).
+generator of the synthetic graph is linked into that library too, so this arm
+never loads the product library) on this host's cores, same workload, same
+precision, same inputs: one step = one full-size layer through the reference's
+public functions (l2_normalize_rows, sddmm_hybrid on reblock(t,16),
+edge_softmax, spmm_hybrid; gnn.cpp:107-116), or gcn_forward / L for GCN.
 """
 
 from __future__ import annotations
@@ -27,6 +39,7 @@ import csv
 import ctypes as C
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -60,26 +73,54 @@ WORKLOADS = {
                          hidden=128, d_out=128, layers=2, cfg="C5"),
 }
 
+INPUT_SEED = 8   # DenseMatrix::random(n, dims, seed + 7) with the bench's seed 1 (bench.cpp:128)
+LAYER_SEED = 1   # random_gcn_layers(..., seed) with the bench's seed 1 (bench.cpp:131-132)
+
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
 # ------------------------------------------------------------------ inputs
-def make_graph(wl, locality, seed=1):
-    """Synthetic symmetric graph of the workload's shape (deterministic)."""
-    import paper_2412_12218_b200 as sg
+def make_graph(wl, locality, seed=1, synth=None):
+    """Synthetic symmetric graph of the workload's shape (deterministic).
+    `synth(n, picks, alpha, p_local, band, seed)` -> graph with num_nodes /
+    num_edges / node_pointer / edge_list; default: the product library's
+    generator (the reference arm passes the copy linked into libsgtk_ref.so —
+    same source, same output, tests/test_bench_cpu.py)."""
+    if synth is None:
+        import paper_2412_12218_b200 as sg
 
+        synth = sg.synth_graph
     n, e = wl["n"], wl["e"]
     loc = LOCALITY[locality]
     picks = max((e - n) / (2.0 * n), 0.5)
     # duplicate picks (local ones collide) shrink E: calibrate on a 50k sample
     ns = min(n, 50_000)
-    s = sg.synth_graph(ns, picks, wl["alpha"], loc["p_local"], loc["band"], seed)
+    s = synth(ns, picks, wl["alpha"], loc["p_local"], loc["band"], seed)
     ratio = (s.num_edges - ns) / (2.0 * ns * picks)
     picks = picks / max(ratio, 0.3)
-    g = sg.synth_graph(n, picks, wl["alpha"], loc["p_local"], loc["band"], seed)
+    g = synth(n, picks, wl["alpha"], loc["p_local"], loc["band"], seed)
     return g, dict(avg_picks=round(picks, 3), **loc, alpha=wl["alpha"])
+
+
+def host_info():
+    """Host cores this process may use, CPU model, OMP_NUM_THREADS."""
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count()
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cores_available": cores, "cpu_model": model,
+            "omp_num_threads": os.environ.get("OMP_NUM_THREADS", "unset (OpenMP default)")}
 
 
 class _NvmlSampler:
@@ -192,131 +233,214 @@ def peaks():
 
 
 # ------------------------------------------------------- reference CPU arm
-def reference_layer_sample(g, h0, beta=1.0, threads=0):
-    """One AGNN layer on the full graph through the reference's public API.
-    Returns (ms per layer, kind, cores, sample description)."""
-    from oracle.oracle import Csr
-
-    c = Csr.of(g.num_nodes, g.node_pointer, g.edge_list)
-    cores = threads or os.cpu_count()
-    try:
-        from oracle.oracle import RefLib
-
-        R = RefLib()
-        th = R.transform_handle(c, 16, 8, threads)
-        th16 = R.reblock_handle(th, 16)
-        hc = R.csr(c)
-        kind = "reference"
-
-        def layer():
-            z, _ = R.l2_normalize_rows(h0)
-            logits = R.sddmm(th16, c.num_edges, z, z, 1.0, False, threads,
-                             values=np.ones(c.num_edges, np.float32))
-            logits *= np.float32(beta)
-            out = np.zeros(c.num_edges, np.float32)
-            R._ok(R.L.ref_edge_softmax(hc.ptr, C.c_void_p(logits.ctypes.data),
-                                       C.c_uint64(c.num_edges), C.c_void_p(out.ctypes.data)))
-            return R.spmm(th, c.num_nodes, h0, 1.0, False, threads, values=out)
-    except FileNotFoundError:
-        from oracle.oracle import Oracle
-
-        O = Oracle()
-        kind = "port"
-
-        def layer():
-            z, _ = O.l2_normalize_rows(h0)
-            logits = O.sddmm(c, z, z, values=np.ones(c.num_edges, np.float32)) * np.float32(beta)
-            return O.spmm(c, h0, values=O.edge_softmax(c, logits))
-    return layer, kind, cores
+def sample_rows(n, k=96, seed=0):
+    rng = np.random.default_rng(seed)
+    return np.unique(np.concatenate([rng.integers(0, n, k), [0, n - 1]]))
 
 
-def reference_gcn_sample(g, x, dims, threads=0):
-    """The GCN layers through the reference's public API (gcn_normalize_values,
-    then gcn_forward on its transform); returns (run, kind, cores)."""
-    from oracle.oracle import Csr
+def rows_agnn_f64(node_pointer, edge_list, x, rows, beta=1.0):
+    """One AGNN layer (gnn.cpp:107-116) for the given rows, exactly in float64."""
+    npz = node_pointer.astype(np.int64)
+    h = x.astype(np.float64)
+    ref = np.zeros((len(rows), x.shape[1]))
+    for t, i in enumerate(rows):
+        nb = edge_list[npz[i]:npz[i + 1]].astype(np.int64)
+        if nb.size == 0:
+            continue
+        hn = h[nb]
+        nn = np.linalg.norm(hn, axis=1)
+        zn = np.where(nn[:, None] > 0, hn / np.where(nn > 0, nn, 1)[:, None], 0.0)
+        nrm_i = np.linalg.norm(h[i])
+        zi = h[i] / nrm_i if nrm_i > 0 else np.zeros_like(h[i])
+        lg = beta * (zn @ zi)
+        a = np.exp(lg - lg.max())
+        ref[t] = (a / a.sum()) @ hn
+    return ref
 
-    c = Csr.of(g.num_nodes, g.node_pointer, g.edge_list)
-    cores = threads or os.cpu_count()
-    rng = np.random.default_rng(5)
-    layers = [((rng.standard_normal((a, b)) / np.sqrt(a)).astype(np.float32), i + 1 < len(dims) - 1)
-              for i, (a, b) in enumerate(zip(dims[:-1], dims[1:]))]
-    try:
-        from oracle.oracle import RefLib
 
-        R = RefLib()
-        th = R.transform_handle(R.gcn_normalize_values(c), 16, 8, threads)
-        return (lambda: R.gcn_forward(th, g.num_nodes, x, layers, threads=threads)), "reference", cores
-    except FileNotFoundError:
-        from oracle.oracle import Oracle
+def rows_spmm_f64(node_pointer, edge_list, values, x, rows):
+    """out = A x for the given rows, exactly in float64 (tile_exec.cpp:200-314)."""
+    npz = node_pointer.astype(np.int64)
+    xd = x.astype(np.float64)
+    ref = np.zeros((len(rows), x.shape[1]))
+    for t, i in enumerate(rows):
+        nb = edge_list[npz[i]:npz[i + 1]].astype(np.int64)
+        a = np.ones(nb.size) if values is None else values[npz[i]:npz[i + 1]].astype(np.float64)
+        ref[t] = a @ xd[nb]
+    return ref
 
-        O = Oracle()
-        cn = O.gcn_normalize_values(c)
-        return (lambda: O.gcn_forward(cn, x, layers)), "port", cores
+
+def max_rel_err(got, ref):
+    """dense_matrix.hpp:68-85: max|got - ref| / max|ref|."""
+    den = float(np.abs(ref).max()) if ref.size else 0.0
+    num = float(np.abs(np.asarray(got, np.float64) - ref).max()) if ref.size else 0.0
+    return num / den if den > 0 else num
+
+
+class RefWorkload:
+    """The reference's own CPU implementation (oracle/_ref/libsgtk_ref.so, the
+    unmodified reference sources) on the bench inputs, through its public
+    functions.  AGNN: one layer as agnn_forward runs it (gnn.cpp:107-116), on
+    reblock(t, 16) built once here (the reference's agnn_forward rebuilds it
+    on every call, gnn.cpp:101 — hoisting it only favours the reference).
+    GCN: gcn_normalize_values + gcn_forward (gnn.cpp:33-52) with the reference
+    bench's own inputs (bench.cpp:114-132)."""
+
+    def __init__(self, wl, g, tf32, R):
+        from oracle.oracle import Csr
+
+        self.R, self.wl, self.tf32 = R, wl, bool(tf32)
+        self.n = g.num_nodes
+        self.c = Csr.of(g.num_nodes, g.node_pointer, g.edge_list)
+        self.threads = R.threads()
+        if wl["kind"] == "agnn":
+            self.x = R.dense_random(self.n, wl["hidden"], INPUT_SEED)
+            self.th = R.transform_handle(self.c, 16, 8)
+            self.th16 = R.reblock_handle(self.th, 16)
+            self.hc = R.csr(self.c)
+            self.unit = np.ones(self.c.num_edges, np.float32)
+            self.per = 1
+        else:
+            L = wl["layers"]
+            self.gn = R.gcn_normalize_values(self.c)
+            self.th = R.transform_handle(self.gn, 16, 8)
+            self.x = R.dense_random(self.n, wl["d_in"], INPUT_SEED)
+            self.layers = R.random_gcn_layers(wl["d_in"], wl["hidden"], wl["d_out"], L, LAYER_SEED)
+            self.per = L
+
+    def run(self, ratio=1.0):
+        """One step; ratio 1 = the reference's default tile path, 0 = its scalar path."""
+        R, tf = self.R, self.tf32
+        if self.wl["kind"] == "agnn":
+            z, _ = R.l2_normalize_rows(self.x)
+            logits = R.sddmm(self.th16, self.c.num_edges, z, z, ratio, tf, 0, values=self.unit)
+            logits *= np.float32(1.0)  # beta (bench.cpp:135)
+            attn = np.zeros_like(logits)
+            R._ok(R.L.ref_edge_softmax(self.hc.ptr, C.c_void_p(logits.ctypes.data),
+                                       C.c_uint64(logits.shape[0]), C.c_void_p(attn.ctypes.data)))
+            return R.spmm(self.th, self.n, self.x, ratio, tf, 0, values=attn)
+        return R.gcn_forward(self.th, self.n, self.x, self.layers, ratio, tf)
+
+    def oracle_spmm_ms(self):
+        """The reference's single-threaded oracle_spmm (oracle.cpp:7-20) on the
+        layer's aggregation input (unit values for AGNN)."""
+        g = self.c if self.wl["kind"] == "agnn" else self.gn
+        t0 = time.perf_counter()
+        self.R.oracle_spmm(g, self.x)
+        return (time.perf_counter() - t0) * 1e3
+
+    def check_rows(self, out):
+        """Sampled-row max_rel_err of a step's output: AGNN layer / GCN first
+        layer's aggregation vs float64 (GCN: checked on the SpMM, run apart)."""
+        rows = sample_rows(self.n)
+        if self.wl["kind"] == "agnn":
+            ref = rows_agnn_f64(self.c.node_pointer, self.c.edge_list, self.x, rows)
+            return max_rel_err(out[rows], ref)
+        agg = self.R.spmm(self.th, self.n, self.x, 1.0, self.tf32)
+        ref = rows_spmm_f64(self.gn.node_pointer, self.gn.edge_list, self.gn.values, self.x, rows)
+        return max_rel_err(agg[rows], ref)
+
+
+def ref_lib():
+    from oracle.oracle import RefLib
+
+    return RefLib()
+
+
+def timed_cpu(fn, warmup, steps):
+    for _ in range(warmup):
+        fn()
+    ts = []
+    out = None
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        out = fn()
+        ts.append((time.perf_counter() - t0) * 1e3)
+    return ts, out
+
+
+def cpu_baseline_leg(wl, g, prec, R):
+    """The GPU arm's cpu_baseline (rank 0, N=1): the reference on this host's
+    cores, warmed, median of 3 — tile path (ratio 1, the reference default),
+    scalar path (ratio 0), and the single-threaded oracle_spmm."""
+    W = RefWorkload(wl, g, prec == "tf32", R)
+    tile, out = timed_cpu(W.run, 1, 3)
+    scalar, _ = timed_cpu(lambda: W.run(0.0), 1, 3)
+    orc = W.oracle_spmm_ms()
+    per = W.per
+    info = host_info()
+    what = (f"one full-size AGNN layer (d={wl['hidden']}, {g.num_edges} edges)" if wl["kind"] == "agnn"
+            else f"one full-size gcn_forward ({wl['layers']} layers) / {wl['layers']}")
+    return {"value": round(statistics.median(tile) / per, 2), "unit": "ms", "cores": W.threads,
+            "kind": "reference", "precision": prec,
+            "sample": f"{what} through the reference's public functions, tile path (ratio 1, the "
+                      f"reference default), 1 warm-up + median of 3, reference threads = "
+                      f"resolve_thread_count(0) = {W.threads}",
+            "scalar_path_ms": round(statistics.median(scalar) / per, 2),
+            "oracle_spmm_1thread_ms": round(orc, 2),
+            "cpu_model": info["cpu_model"], "omp_num_threads": info["omp_num_threads"],
+            "cores_available": info["cores_available"],
+            "max_rel_err_sampled": W.check_rows(out)}
 
 
 def run_reference_arm(args, wl):
+    """`--impl reference`: the reference's CPU path alone (rank 0; other ranks
+    of a torchrun launch exit without work).  Loads only oracle/_ref."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_2412_12218_b200 as sg
-
-    g, gen = make_graph(wl, args.locality)
-    if wl["kind"] == "agnn":
-        h0 = sg.dense_random(g.num_nodes, wl["hidden"], 17, -1.0, 1.0)
-        layer, kind, cores = reference_layer_sample(g, h0)
-        per, what = 1, f"one full-size AGNN layer (d={wl['hidden']})"
-    else:  # GCN: the whole gcn_forward per step, reported per layer
-        L = wl["layers"]
-        dims = [wl["d_in"]] + [wl["hidden"]] * (L - 1) + [wl["d_out"]]
-        x0 = sg.dense_random(g.num_nodes, dims[0], 17, -1.0, 1.0)
-        layer, kind, cores = reference_gcn_sample(g, x0, dims)
-        per, what = L, f"gcn_forward ({L} layers, {dims}) / {L}"
-    steps = max(1, min(args.steps, 5))
-    for _ in range(min(args.warmup, 1)):
-        layer()
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        layer()
-        times.append((time.perf_counter() - t0) * 1e3 / per)
-    ms = statistics.median(times)
+    R = ref_lib()
+    g, gen = make_graph(wl, args.locality, synth=R.synth_graph)
+    W = RefWorkload(wl, g, args.precision == "tf32", R)
+    ts, out = timed_cpu(W.run, args.warmup, args.steps)
+    per_layer = [t / W.per for t in ts]
+    ms = float(np.mean(per_layer))
+    info = host_info()
+    err = W.check_rows(out)
+    what = (f"one full-size AGNN layer (d={wl['hidden']}) per step" if wl["kind"] == "agnn"
+            else f"one full-size gcn_forward ({wl['layers']} layers) per step, reported / {W.per}")
     line = {
         "impl": "reference", "metric": metric_name(wl), "value": round(ms, 3), "unit": "ms",
-        "n_gpus": args.gpus, "steps": steps, "warmup": min(args.warmup, 1),
-        "ms_per_step": round(ms * per, 3), "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms * W.per, 3), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": dtype_name(args.precision), "data": DATA,
         "config": config_of(args, wl, g, gen),
-        "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": cores, "kind": kind,
-                         "sample": f"{what} per step, median "
-                                   f"of {steps}; reference threads = all {cores} host cores"},
+        "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": W.threads,
+                         "kind": "reference",
+                         "sample": f"{what}, tile path (ratio 1, the reference default), mean of "
+                                   f"{args.steps} after {args.warmup} warm-up; reference threads = "
+                                   f"resolve_thread_count(0) = {W.threads}",
+                         "median_ms": round(statistics.median(per_layer), 3),
+                         "cpu_model": info["cpu_model"], "omp_num_threads": info["omp_num_threads"],
+                         "cores_available": info["cores_available"]},
         "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "max_rel_err_sampled": err,
     }
     print(json.dumps(line), flush=True)
     if args.csv:
-        blocks = cap = dens = ""
-        try:  # the reference's own transform statistics (block_stats, sgt_transform.cpp:93-100)
-            from oracle.oracle import Csr, RefLib
-
-            R = RefLib()
-            t = R.transform_fields(R.transform_handle(Csr.of(g.num_nodes, g.node_pointer, g.edge_list), 16, 8))
-            blocks = int(t.block_counter)
-            cap = blocks * 16 * 8
-            dens = g.num_edges / cap if cap else 0.0
-        except Exception:
-            pass
-        write_report_csv(args.csv, [dict(dataset=args.workload, kernel=wl["kind"], path="reference-cpu",
-                                         median_ms=round(ms, 4), blocks=blocks, capacity=cap,
-                                         nnz=g.num_edges, density=dens)])
+        t = R.transform_fields(W.th)
+        blocks = int(t.block_counter)
+        cap = blocks * 16 * 8
+        write_report_csv(args.csv, [dict(
+            dataset=args.workload, kernel=wl["kind"], path="reference-cpu-tile",
+            median_ms=round(statistics.median(per_layer), 4), blocks=blocks, capacity=cap,
+            nnz=g.num_edges, density=round(g.num_edges / cap, 6) if cap else 0.0,
+            max_rel_err=f"{err:.3e}", gpus=0, cpu_ms=round(ms, 3), cpu_cores=W.threads)])
 
 
-CSV_HEADER = "dataset,kernel,path,median_ms,blocks,capacity,nnz,density,max_rel_err"
+CSV_HEADER = ("dataset,kernel,path,median_ms,blocks,capacity,nnz,density,max_rel_err,"
+              "gpus,achieved_GBps,roofline_frac,tc_pipe_pct,cpu_ms,cpu_cores")
 
 
 def write_report_csv(path, rows):
     """The reference bench's report schema (bench.hpp:53-55, bench.cpp:216-227):
-    dataset,kernel,path,median_ms,blocks,capacity,nnz,density,max_rel_err, so
-    the CPU and GPU rows of a run sit side by side.  Appends (header once)."""
+    dataset,kernel,path,median_ms,blocks,capacity,nnz,density,max_rel_err —
+    then the SURVEY §5 columns gpus,achieved_GBps,roofline_frac,tc_pipe_pct,
+    cpu_ms,cpu_cores — so the CPU and GPU rows of a run sit side by side.
+    max_rel_err: sampled rows of one layer (AGNN) / the SpMM (GCN) against a
+    float64 evaluation (the reference bench's dense oracles stop at 2,048
+    nodes, bench.cpp:194-209).  Appends (header once)."""
     new = not os.path.exists(path) or os.path.getsize(path) == 0
     with open(path, "a", newline="") as f:
         w = csv.writer(f, lineterminator="\n")
@@ -326,159 +450,147 @@ def write_report_csv(path, rows):
             w.writerow([r.get(k, "") for k in CSV_HEADER.split(",")])
 
 
+DATA = "synthetic (deterministic generator; inputs = the reference bench's seeded streams)"
+
+
+def dtype_name(prec):
+    return "f32 (split-TF32 on tensor cores)" if prec == "fp32" else "tf32"
+
+
 def metric_name(wl):
     k = "AGNN" if wl["kind"] == "agnn" else "GCN"
     return f"{k} layer-forward ms per graph"
 
 
-def config_of(args, wl, g, gen, extra=None):
-    c = {"workload": f"{args.workload} ({wl['cfg']}): {wl['kind'].upper()} on synthetic "
-                     f"{args.workload.split('-')[0]}-shaped graph",
-         "nodes": g.num_nodes, "edges": g.num_edges,
-         "model": f"{wl['d_in']}->{wl['hidden']}->{wl['d_out']}, {wl['layers']} layers",
-         "global_batch": 1, "seq_len": 0, "parallelism": f"rowwindow{args.gpus}",
-         "precision": args.precision, "mode": args.mode, "locality": args.locality,
-         "generator": gen, "l2": "flushed between timed steps (256 MB write)"}
-    if extra:
-        c.update(extra)
-    return c
+def config_of(args, wl, g, gen):
+    """Identical in both arms (the driver compares them)."""
+    return {"workload": f"{args.workload} ({wl['cfg']}): {wl['kind'].upper()} on synthetic "
+                        f"{args.workload.split('-')[0]}-shaped graph",
+            "nodes": g.num_nodes, "edges": g.num_edges,
+            "model": f"{wl['d_in']}->{wl['hidden']}->{wl['d_out']}, {wl['layers']} layers",
+            "step": (f"agnn_forward({wl['layers']} layers, d={wl['hidden']}, beta=1) on the whole "
+                     f"graph; value = ms per layer" if wl["kind"] == "agnn" else
+                     f"gcn_forward({wl['layers']} layers); value = ms per layer"),
+            "global_batch": 1, "seq_len": 0, "parallelism": f"rowwindow{args.gpus}",
+            "precision": args.precision, "mode": args.mode, "locality": args.locality,
+            "generator": gen, "l2": "flushed between timed steps (256 MB write)"}
 
 
 # ------------------------------------------------------------- B200 arm
+def dist_setup():
+    """One process per GPU (torchrun env).  More ranks than visible devices
+    (the N>1 path exercised on a 1-GPU lease): ranks share devices, gloo."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    ndev = torch.cuda.device_count()
+    if ndev == 0:
+        raise RuntimeError("bench.py (b200 arm) needs a CUDA device; there is no CPU fallback")
+    devi = local % ndev
+    torch.cuda.set_device(devi)
+    backend = None
+    if world > 1:
+        backend = "nccl" if world <= ndev else "gloo"
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", devi))
+        else:
+            dist.init_process_group("gloo")
+    return world, rank, devi, backend
+
+
 def run_b200(args, wl):
     import torch
     import torch.distributed as dist
 
     import paper_2412_12218_b200 as sg
     from paper_2412_12218_b200 import device as D
-    from paper_2412_12218_b200._lib import check, lib
+    from paper_2412_12218_b200.distributed import RowSlice, allgather_rows
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
+    world, rank, devi, backend = dist_setup()
+    dev = torch.device("cuda", devi)
     prec = args.precision
-    mode = {"panel": 2, "fused": 1, "chain": 0, "auto": -1}[args.mode]
+    L, d = wl["layers"], wl["hidden"]
 
     t0 = time.perf_counter()
     g, gen = make_graph(wl, args.locality)
-    N = g.num_nodes
-    if mode < 0:  # the library's AGNN auto mode (forward.cu): panels from 2M edges, else fused
-        mode = 2 if (wl["kind"] == "gcn" or g.num_edges >= (2 << 20) or wl["hidden"] > 64) else 1
-        args.mode = {2: "panel", 1: "fused"}[mode] + " (auto)"
-    log(f"[bench] graph {N} nodes {g.num_edges} edges in {time.perf_counter() - t0:.1f}s")
-    # row partition in whole 128-row panels (balanced by edges)
-    Q = 128
-    bounds = np.zeros(world + 1, np.uint64)
-    check(lib().sgtk_partition_windows(g.node_pointer.ctypes.data, N, Q, world, bounds.ctypes.data))
-    r0, r1 = min(N, int(bounds[rank]) * Q), min(N, int(bounds[rank + 1]) * Q)
-    e0, e1 = int(g.node_pointer[r0]), int(g.node_pointer[r1])
-    np_loc = (g.node_pointer[r0:r1 + 1] - np.uint64(e0)).astype(np.uint64)
-    el_loc = g.edge_list[e0:e1]
-    vals_loc = None
-    if wl["kind"] == "gcn":
-        vals_loc = sg.gcn_normalize_values(g).values[e0:e1]
+    N, E = g.num_nodes, g.num_edges
+    log(f"[bench] rank {rank}: graph {N} nodes {E} edges in {time.perf_counter() - t0:.1f}s")
+    # the library's AGNN auto mode (forward.cu): panels from 2M edges or d > 64, else the fused
+    # kernel — resolved on the WHOLE graph so every partition runs the same kernels
+    mode = {"panel": 2, "fused": 1, "chain": 0, "auto": -1}[args.mode]
+    if mode < 0:
+        mode = 2 if (wl["kind"] == "gcn" or E >= (2 << 20) or d > 64) else 1
+    mode_name = {2: "panel", 1: "fused", 0: "chain"}[mode] + (" (auto)" if args.mode == "auto" else "")
+    vals = sg.gcn_normalize_values(g).values if wl["kind"] == "gcn" else None
 
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    if world == 1:
-        dg = D.DeviceGraph.from_csr(np_loc, el_loc, vals_loc, r1 - r0)
-    else:
-        dg = D.DeviceGraph.from_csr(np_loc, el_loc, vals_loc, r1 - r0, num_cols=N, row_offset=r0)
+    sl = RowSlice(g.node_pointer, g.edge_list, vals, N, rank, world)
     torch.cuda.synchronize()
     translate_ms = (time.perf_counter() - t0) * 1e3
+    dg = sl.graph
     info = dg.info
     bs = dg.block_stats()
-    log(f"[bench] rank {rank}: rows [{r0},{r1}) translate {translate_ms:.1f} ms, tiles8 {info.tiles8} "
-        f"tiles16 {info.tiles16} units {info.work_units8} density16x8 {bs[3]:.4f}")
+    log(f"[bench] rank {rank}: rows [{sl.r0},{sl.r1}) translate {translate_ms:.1f} ms, "
+        f"tiles8 {info.tiles8} tiles16 {info.tiles16} units {info.work_units8} "
+        f"density16x8 {bs[3]:.4f}")
 
-    x_host = sg.dense_random(N, wl["d_in"], 8)
-    w_in = torch.from_numpy(sg.dense_random(wl["d_in"], wl["hidden"], 1, -0.1, 0.1)).to(dev)
-    w_out = torch.from_numpy(sg.dense_random(wl["hidden"], wl["d_out"], 2, -0.1, 0.1)).to(dev)
-    # features resident with a 16-byte-multiple row pitch (TMA-eligible rows)
-    ldx = (wl["d_in"] + 3) // 4 * 4
-    x = torch.zeros((N, ldx), dtype=torch.float32, device=dev)[:, :wl["d_in"]]
-    x.copy_(torch.from_numpy(x_host))
-    L = wl["layers"]
-    d = wl["hidden"]
-    betas = np.ones(L, np.float32)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-
-    # ---------------- step definitions --------------------------------------
-    def allgather_rows(local_rows: torch.Tensor) -> torch.Tensor:
-        if world == 1:
-            return local_rows
-        maxr = int(max(min(N, int(bounds[p + 1]) * Q) - min(N, int(bounds[p]) * Q)
-                       for p in range(world)))
-        pad = torch.zeros((maxr, local_rows.shape[1]), dtype=local_rows.dtype, device=dev)
-        pad[:local_rows.shape[0]] = local_rows
-        full = torch.empty((world * maxr, local_rows.shape[1]), dtype=local_rows.dtype, device=dev)
-        dist.all_gather_into_tensor(full, pad)
-        parts = [full[p * maxr: p * maxr + (min(N, int(bounds[p + 1]) * Q) -
-                                            min(N, int(bounds[p]) * Q))] for p in range(world)]
-        return torch.cat(parts)
-
+    betas = np.ones(L, np.float32)
     if wl["kind"] == "agnn":
-        h0_loc = D.gemm(x[r0:r1], w_in, relu=True, precision=prec)
-        h0 = allgather_rows(h0_loc) if world > 1 else h0_loc
-
-        def agnn_stack(h):
-            if world == 1:
-                return dg.agnn_forward(h, betas, precision=prec, mode=mode)
-            cur = h
-            for l in range(L):
-                loc = dg.agnn_forward(cur, betas[l:l + 1], precision=prec, mode=mode)
-                cur = allgather_rows(loc) if l + 1 < L else loc
-            return cur
+        h0_host = sg.dense_random(N, d, INPUT_SEED)
+        h0_full = torch.from_numpy(h0_host).to(dev)
+        h_rep = h0_full if world == 1 else sl.scatter_full(h0_full, sl.replica(d, dev))
+        scratch = None if world == 1 else (sl.replica(d, dev), sl.replica(d, dev))
+        out_buf = torch.empty((sl.rows, d), dtype=torch.float32, device=dev)
 
         def step():
-            return agnn_stack(h0)
-
-        def model_forward():
-            hh = allgather_rows(D.gemm(x[r0:r1], w_in, relu=True, precision=prec))
-            return D.gemm(agnn_stack(hh), w_out, relu=False, precision=prec)
+            return sl.agnn_forward(h_rep, betas, precision=prec, mode=mode, scratch=scratch,
+                                   out=out_buf)
 
         if mode == 2:
             pi = dg.panel_info(d)
-            # input kernel, then per layer: dense + rows + final (+ hub rows)
-            launches_per_step = 1 + L * (3 + (1 if pi["long_rows"] else 0))
+            per_call = 3 + (1 if pi["long_rows"] else 0)  # dense + rows + final (+ hub rows)
+            # one input kernel per call: once per step on 1 GPU, once per layer on N
+            launches_per_step = (1 + L * per_call) if world == 1 else L * (1 + per_call)
         else:
-            launches_per_step = L * (2 if mode == 1 else 4) + (
-                L if (mode == 1 and dg_has_splits(dg, 16)) or (mode == 0 and dg_has_splits(dg, 8)) else 0)
-        layers_per_step = L
+            split = dg_has_splits(dg, 16 if mode == 1 else 8)
+            launches_per_step = L * ((2 if mode == 1 else 4) + (1 if split else 0))
+        x_in = h0_full
     else:
+        x_full = torch.from_numpy(sg.dense_random(N, wl["d_in"], INPUT_SEED)).to(dev)
+        x_loc = x_full[sl.r0:sl.r1]
         layers = [(torch.from_numpy(w).to(dev), r) for w, r in
-                  sg.random_gcn_layers(wl["d_in"], wl["hidden"], wl["d_out"], L, 1)]
-        xs = torch.from_numpy(sg.dense_random(N, wl["d_in"], 8)).to(dev) if wl["d_in"] != x.shape[1] else x
+                  sg.random_gcn_layers(wl["d_in"], wl["hidden"], wl["d_out"], L, LAYER_SEED)]
+        reps = {}
 
         def step():
-            if world == 1:
-                return dg.gcn_forward(xs, layers, precision=prec, order=2)
-            h = xs
-            for l, (w, r) in enumerate(layers):
-                hw = D.gemm(h[r0:r1] if h.shape[0] == N else h, w, relu=False, precision=prec)
-                full = allgather_rows(hw)
-                loc = dg.spmm(full, precision=prec)
-                if r:
-                    loc = torch.relu_(loc)
-                h = allgather_rows(loc) if l + 1 < L else loc
-            return h
+            return sl.gcn_forward(x_loc, layers, precision=prec, reps=reps)
 
-        model_forward = step
         launches_per_step = L * 3 + (L if dg_has_splits(dg, 8) else 0)
-        layers_per_step = L
+        if world > 1:
+            launches_per_step += sum(1 for w, r in layers if r and w.shape[1] < w.shape[0])
+        x_in = x_full
 
     # ---------------- timing --------------------------------------------------
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     def timed(fn, steps, warmup):
         for _ in range(warmup):
             fn()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        torch.cuda.synchronize()
         ts = []
         for _ in range(steps):
             flush.fill_(1)
@@ -490,12 +602,9 @@ def run_b200(args, wl):
             b.synchronize()
             ts.append(a.elapsed_time(b))
         torch.cuda.synchronize()
-        ms = float(np.mean(ts))
         if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms, ts
+            dist.barrier()
+        return max_over_ranks(float(np.mean(ts))), ts
 
     warm = max(3, args.warmup)
     sampler, rows = clocks_sampler()
@@ -503,45 +612,86 @@ def run_b200(args, wl):
     if sampler:
         sampler.terminate()
     clocks = summarize_clocks(rows)
-    value = step_ms / layers_per_step
-    model_ms, _ = timed(model_forward, max(2, args.steps // 2), 2)
+    value = step_ms / L
 
-    # ---------------- dominant-kernel roofline (CUDA events on our stream) ----
+    details = {"mode_resolved": mode_name, "translate_ms": round(translate_ms, 2),
+               "tiles16x8": int(bs[0]), "tile_density16x8": round(bs[3], 4),
+               "rows_this_rank": [sl.r0, sl.r1],
+               "panel_format": dg.panel_info(d) if mode == 2 else None}
+    if world > 1:
+        details.update(backend=backend, devices=torch.cuda.device_count(),
+                       exchange="one in-place all_gather_into_tensor per layer over the padded "
+                                "replica" if backend == "nccl" else
+                                "gloo all-gather via host copies (ranks share a device)")
+
+    # ---------------- N>1: bit-identical against one device ------------------
+    verify = None
+    if world > 1 and args.verify:
+        out_loc = step()
+        torch.cuda.synchronize()
+        loc = out_loc if backend == "nccl" else out_loc.cpu()
+        full = allgather_rows(loc, sl.ranges).cpu()
+        if rank == 0:
+            whole = D.DeviceGraph.from_csr(g.node_pointer, g.edge_list, vals, N)
+            if wl["kind"] == "agnn":
+                want = whole.agnn_forward(x_in, betas, precision=prec, mode=mode)
+            else:
+                want = whole.gcn_forward(x_in, layers, precision=prec, order=2)
+            verify = {"bit_identical": bool(torch.equal(want.cpu(), full)),
+                      "against": "single-device forward of the whole graph (rank 0)"}
+            del whole
+        if world > 1:
+            dist.barrier()
+
+    # ---------------- N=1 extras: model forward, kernel breakdown, roofline ---
     roof = None
     kern = {}
     extra = {}
+    model_ms = None
+    err = None
     if world == 1:
-        kern, roof = kernel_breakdown(args, wl, dg, g, h0 if wl["kind"] == "agnn" else xs, D, prec,
-                                      mode, flush, stream, layers if wl["kind"] == "gcn" else None,
-                                      extra, (x, w_in) if wl["kind"] == "agnn" else None)
+        if wl["kind"] == "agnn":
+            x_host = sg.dense_random(N, wl["d_in"], INPUT_SEED + 1)
+            w_in = torch.from_numpy(sg.dense_random(wl["d_in"], d, 1, -0.1, 0.1)).to(dev)
+            w_out = torch.from_numpy(sg.dense_random(d, wl["d_out"], 2, -0.1, 0.1)).to(dev)
+            ldx = (wl["d_in"] + 3) // 4 * 4  # 16-byte row pitch (TMA-eligible rows)
+            xp = torch.zeros((N, ldx), dtype=torch.float32, device=dev)[:, :wl["d_in"]]
+            xp.copy_(torch.from_numpy(x_host))
 
-    # ---------------- e2e through the host-buffer C ABI ----------------------
-    e2e = None
+            def model_forward():
+                hh = D.gemm(xp, w_in, relu=True, precision=prec)
+                return D.gemm(dg.agnn_forward(hh, betas, precision=prec, mode=mode), w_out,
+                              relu=False, precision=prec)
+
+            model_ms, _ = timed(model_forward, max(2, args.steps // 2), 2)
+            proj = (xp, w_in)
+            rows_s = sample_rows(N)
+            one = dg.agnn_forward(h0_full, betas[:1], precision=prec, mode=mode).cpu().numpy()
+            err = max_rel_err(one[rows_s], rows_agnn_f64(g.node_pointer, g.edge_list, h0_host, rows_s))
+        else:
+            proj = None
+            rows_s = sample_rows(N)
+            agg = dg.spmm(x_full, precision=prec).cpu().numpy()
+            err = max_rel_err(agg[rows_s], rows_spmm_f64(g.node_pointer, g.edge_list, vals,
+                                                         x_full.cpu().numpy(), rows_s))
+        kern, roof = kernel_breakdown(args, wl, dg, g, x_in, D, prec, mode, flush, stream,
+                                      layers if wl["kind"] == "gcn" else None, extra, proj)
+
+    # ---------------- e2e: host buffers in, host buffers out ------------------
     if world == 1:
-        e2e = e2e_host(wl, dg, h0 if wl["kind"] == "agnn" else xs, prec, mode, L, layers_per_step,
-                       layers if wl["kind"] == "gcn" else None, flush, args)
+        e2e = e2e_host(wl, dg, x_in, prec, mode, L, L, layers if wl["kind"] == "gcn" else None,
+                       flush, args)
+    else:
+        e2e = e2e_multi(wl, sl, step, x_in, h_rep if wl["kind"] == "agnn" else None,
+                        None if wl["kind"] == "agnn" else x_loc, L, args, max_over_ranks, flush)
 
     # ---------------- CPU baseline (rank 0, N=1) ------------------------------
     cpu = None
-    if rank == 0 and world == 1 and wl["kind"] == "agnn" and not args.no_cpu:
-        h0_host = h0.cpu().numpy()
-        layer, kind, cores = reference_layer_sample(g, h0_host)
-        t0 = time.perf_counter()
-        layer()
-        cpu_ms = (time.perf_counter() - t0) * 1e3
-        cpu = {"value": round(cpu_ms, 1), "unit": "ms", "cores": cores, "kind": kind,
-               "sample": f"one full-size AGNN layer (d={d}, {g.num_edges} edges) through the "
-                         "reference's public functions, single run, all host cores"}
-    elif rank == 0 and world == 1 and not args.no_cpu:  # GCN: gcn_forward / layers
-        dims = [wl["d_in"]] + [wl["hidden"]] * (L - 1) + [wl["d_out"]]
-        run, kind, cores = reference_gcn_sample(g, xs.cpu().numpy(), dims)
-        t0 = time.perf_counter()
-        run()
-        cpu_ms = (time.perf_counter() - t0) * 1e3 / L
-        cpu = {"value": round(cpu_ms, 1), "unit": "ms", "cores": cores, "kind": kind,
-               "sample": f"one full-size gcn_forward ({L} layers, dims {dims}, {g.num_edges} "
-                         "edges) through the reference's public API, per layer, single run, "
-                         "all host cores"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline_leg(wl, g, prec, ref_lib())
+        except FileNotFoundError as e:
+            cpu = {"value": None, "unavailable": str(e)}
 
     pk, pk_src = peaks()
     if roof:
@@ -549,24 +699,20 @@ def run_b200(args, wl):
         roof["peak"] = pk["hbm_gbs"]
         roof["frac"] = round(roof["achieved"] / pk["hbm_gbs"], 4)
         roof["peak_source"] = f"MEASURED_PEAKS.json hbm_gbs ({pk_src})"
+        roof["tc_pipe_pct"] = profiled_tc_pipe(gcn=wl["kind"] == "gcn")
 
     if rank == 0:
         line = {
             "metric": metric_name(wl), "value": round(value, 4), "unit": "ms",
             "n_gpus": world, "steps": args.steps, "warmup": warm,
             "ms_per_step": round(step_ms, 4), "higher_is_better": False,
-            "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32 (split-TF32 on tensor cores)" if prec == "fp32" else "tf32",
-            "data": "synthetic (deterministic generator; random-init weights)",
-            "config": config_of(args, wl, g, gen, {
-                "step": f"agnn_forward({L} layers) on the whole graph; value = step/{L}"
-                if wl["kind"] == "agnn" else f"gcn_forward({L} layers); value = step/{L}",
-                "tiles16x8": int(bs[0]), "tile_density16x8": round(bs[3], 4),
-                "translate_ms": round(translate_ms, 2),
-                "panel_format": dg.panel_info(wl["hidden"]) if mode == 2 else None}),
+            "scaling": "strong", "vs_baseline": None, "dtype": dtype_name(prec), "data": DATA,
+            "config": config_of(args, wl, g, gen),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
-            "model_forward_ms": round(model_ms, 4), "kernels_ms": kern,
+            "max_rel_err_sampled": err, "verify": verify,
+            "model_forward_ms": None if model_ms is None else round(model_ms, 4),
+            "kernels_ms": kern, "details": details,
         }
         if "roofline_unfused_formula" in extra and roof:
             u = extra["roofline_unfused_formula"]
@@ -582,14 +728,80 @@ def run_b200(args, wl):
             rg["frac"] = round(rg["achieved"] / pk["hbm_gbs"], 4)
             line["roofline_gemm"] = rg
         print(json.dumps(line), flush=True)
-        if args.csv:  # per layer, like the reference arm's row
-            write_report_csv(args.csv, [dict(dataset=args.workload, kernel=wl["kind"],
-                                             path=f"b200-{args.mode.split()[0]}",
-                                             median_ms=round(statistics.median(step_ts) / layers_per_step, 4),
-                                             blocks=bs[0], capacity=bs[1], nnz=bs[2],
-                                             density=round(bs[3], 6))])
+        if args.csv:
+            write_report_csv(args.csv, [dict(
+                dataset=args.workload, kernel=wl["kind"], path=f"b200-{mode_name.split()[0]}",
+                median_ms=round(statistics.median(step_ts) / L, 4), blocks=bs[0], capacity=bs[1],
+                nnz=bs[2], density=round(bs[3], 6),
+                max_rel_err="" if err is None else f"{err:.3e}", gpus=world,
+                achieved_GBps=roof["achieved"] if roof else "",
+                roofline_frac=roof["frac"] if roof else "",
+                tc_pipe_pct=((roof or {}).get("tc_pipe_pct") or {}).get("pct", ""),
+                cpu_ms=cpu.get("value") if cpu else "", cpu_cores=cpu.get("cores") if cpu else "")])
     if world > 1:
         dist.destroy_process_group()
+
+
+def e2e_multi(wl, sl, step, x_full, h_rep, x_loc, L, args, max_over_ranks, flush):
+    """N>1 end to end: every step copies this rank's input rows from pinned
+    host memory (AGNN: into its block of the replica, then the exchange), runs
+    the layers, and reads its output rows back; max over ranks."""
+    import torch
+
+    d_in = x_full.shape[1]
+    pin_in = x_full[sl.r0:sl.r1].cpu().pin_memory()
+    out0 = step()
+    pin_out = torch.empty(tuple(out0.shape), dtype=torch.float32).pin_memory()
+    dst = sl.mine(h_rep) if h_rep is not None else x_loc
+
+    def call():
+        dst.copy_(pin_in, non_blocking=True)
+        if h_rep is not None:
+            sl.exchange(h_rep)
+        pin_out.copy_(step(), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(2):
+        call()
+    ts = []
+    for _ in range(max(3, args.steps)):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        call()
+        ts.append((time.perf_counter() - t0) * 1e3)
+    ms = max_over_ranks(float(np.mean(ts)))
+    d_out = int(out0.shape[1])
+    return {"value": round(ms / L, 4), "unit": "ms",
+            "h2d_bytes_per_step": int(sl.n * d_in * 4), "d2h_bytes_per_step": int(sl.n * d_out * 4),
+            "path": "distributed.RowSlice (pinned H2D of each rank's rows -> layers with in-place "
+                    "all-gathers -> D2H of each rank's rows); bytes summed over ranks"}
+
+
+def profiled_tc_pipe(gcn=False):
+    """Tensor-pipe utilisation of the dominant tcgen05 kernel from the newest
+    committed ncu summary (profiles/*_ncu_full.md, tools/ncu_summary.py)."""
+    import glob
+    import re
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_full.md")))
+    files = [f for f in files if f.endswith("_gcn_ncu_full.md") == gcn]
+    kern = "spmm_panel_kernel" if gcn else "agnn_dense_kernel"
+    for path in reversed(files):
+        try:
+            text = open(path).read()
+        except OSError:
+            continue
+        sec = text.split(f"`{kern}")
+        if len(sec) < 2:
+            continue
+        m = re.search(r"\| sm__pipe_tensor_cycles_active\.avg\.pct_of_peak_sustained_active \| "
+                      r"([0-9.]+)", sec[1].split("## ")[0])
+        if m:
+            return {"kernel": kern, "pct": float(m.group(1)),
+                    "metric": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+                    "source": os.path.relpath(path, ROOT)}
+    return None
 
 
 def profiled_traffic(kernel_field, gcn=False):
@@ -824,6 +1036,14 @@ def e2e_host(wl, dg, h, prec, mode, L, layers_per_step, gcn_layers, flush, args)
             "path": "sgtk_agnn_forward_host" if wl["kind"] == "agnn" else "sgtk_gcn_forward_host"}
 
 
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -835,14 +1055,30 @@ def main():
     ap.add_argument("--mode", default="auto", choices=["auto", "panel", "fused", "chain"])
     ap.add_argument("--locality", default="calibrated", choices=sorted(LOCALITY))
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-verify", dest="verify", action="store_false",
+                    help="N>1: skip the bit-identity check against a one-device forward")
     ap.add_argument("--csv", default="", help="also append a row in the reference bench's CSV "
                                                "schema (bench.hpp:53-55) to this file")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         run_reference_arm(args, wl)
-    else:
-        run_b200(args, wl)
+        if os.environ.get("SGTK_BENCH_PRINT_MAPS"):  # tests: which native libraries loaded
+            with open("/proc/self/maps") as f:
+                libs = sorted({ln.split()[-1] for ln in f if ln.rstrip().endswith(".so")})
+            log("[bench] loaded: " + " ".join(libs))
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (the driver's own launch form)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        log(f"[bench] WORLD_SIZE={world} overrides --gpus {args.gpus}")
+        args.gpus = world
+    run_b200(args, wl)
 
 
 if __name__ == "__main__":

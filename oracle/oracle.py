@@ -413,6 +413,62 @@ class RefLib:
     def tf32_round_value(self, v):
         return self.L.ref_tf32_round_value(C.c_float(v))
 
+    def random_gcn_layers(self, in_dim, hidden, out_dim, num_layers, seed):
+        """The reference's seeded layer stack (gnn.cpp:121-137): [(W, relu)]."""
+        dims = [in_dim] + [hidden] * (num_layers - 1) + [out_dim]
+        w = np.zeros(sum(a * b for a, b in zip(dims[:-1], dims[1:])), np.float32)
+        relu = np.zeros(num_layers, np.int32)
+        self._ok(self.L.ref_random_gcn_layers(C.c_uint64(in_dim), C.c_uint64(hidden),
+                                              C.c_uint64(out_dim), C.c_uint32(num_layers),
+                                              C.c_uint64(seed), _vp(w), _vp(relu)))
+        out, o = [], 0
+        for l, (a, b) in enumerate(zip(dims[:-1], dims[1:])):
+            out.append((w[o:o + a * b].reshape(a, b).copy(), bool(relu[l])))
+            o += a * b
+        return out
+
+    def synth_graph(self, n, avg_picks, alpha=0.0, p_local=0.0, band=4.0, seed=1) -> Csr:
+        """The bench's synthetic generator (paper_2412_12218_b200/csrc/synth.cpp,
+        linked into this library so the reference arm never loads the product
+        library); identical output to sgtk.synth_graph."""
+        h = C.c_void_p()
+        L = self.L
+        L.sgtk_synth_create.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_double,
+                                        C.c_double, C.c_uint64, C.POINTER(C.c_void_p)]
+        L.sgtk_synth_destroy.argtypes = [C.c_void_p]
+        rc = L.sgtk_synth_create(n, avg_picks, alpha, p_local, band, seed, C.byref(h))
+        if rc:
+            raise OracleError(rc, "sgtk_synth_create failed")
+        try:
+            nn, nnz = C.c_uint64(), C.c_uint64()
+            L.sgtk_synth_info(h, C.byref(nn), C.byref(nnz))
+            np_ = np.zeros(nn.value + 1, np.uint64)
+            el = np.zeros(nnz.value, np.uint32)
+            L.sgtk_synth_copy(h, _vp(np_), _vp(el))
+        finally:
+            L.sgtk_synth_destroy(h)
+        return Csr(int(nn.value), np_, el, None)
+
+    def threads(self, requested: int = 0) -> int:
+        """resolve_thread_count (threading.cpp:9-22): the default worker count."""
+        return int(self.L.ref_resolve_threads(int(requested)))
+
+    def save_sgt(self, th, path: str):
+        self._ok(self.L.ref_save_sgt(th.ptr, path.encode()))
+
+    def load_sgt(self, path: str):
+        h = C.c_void_p()
+        self._ok(self.L.ref_load_sgt(path.encode(), C.byref(h)))
+        return self._Handle(self, h, self.L.ref_graph_free)
+
+    def oracle_spmm(self, g: Csr, x):
+        """The reference's single-threaded oracle_spmm (oracle.cpp:7-20)."""
+        hc = self.csr(g)
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.zeros((g.num_nodes, x.shape[1]), np.float32)
+        self._ok(self.L.ref_oracle_spmm(hc.ptr, _vp(x), C.c_uint64(x.shape[1]), _vp(out)))
+        return out
+
     def dense_random(self, r, c, seed, lo=-1.0, hi=1.0):
         out = np.zeros((r, c), np.float32)
         self.L.ref_dense_random(C.c_uint64(r), C.c_uint64(c), C.c_uint64(seed),

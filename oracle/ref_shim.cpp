@@ -21,6 +21,8 @@
 #include "sgtk/gnn.hpp"
 #include "sgtk/graph_io.hpp"
 #include "sgtk/oracle.hpp"
+#include "sgtk/sgt_file.hpp"
+#include "sgtk/threading.hpp"
 #include "sgtk/sgt_transform.hpp"
 #include "sgtk/tile_exec.hpp"
 
@@ -289,6 +291,33 @@ float ref_tf32_round_value(float v) { return tf32_round_value(v); }
 void ref_dense_random(uint64_t r, uint64_t c, uint64_t seed, float lo,
                       float hi, float* out) {
   put(DenseMatrix::random(r, c, seed, lo, hi), out);
+}
+
+// random_gcn_layers(in, hidden, out, L, seed) (gnn.cpp:121-137): weights
+// concatenated row-major, relu flags.
+int ref_random_gcn_layers(uint64_t in_dim, uint64_t hidden, uint64_t out_dim,
+                          uint32_t nlayers, uint64_t seed, float* weights,
+                          int* relu) {
+  return guard([&] {
+    auto layers = random_gcn_layers(in_dim, hidden, out_dim, nlayers, seed);
+    float* w = weights;
+    for (uint32_t l = 0; l < layers.size(); ++l) {
+      put(layers[l].weight, w);
+      w += layers[l].weight.data.size();
+      relu[l] = layers[l].apply_relu ? 1 : 0;
+    }
+  });
+}
+// resolve_thread_count(0) (threading.cpp:9-22): the worker count the
+// reference's kernels use by default (SGTK_THREADS, else OpenMP's max).
+int ref_resolve_threads(int requested) { return resolve_thread_count(requested); }
+// save_sgt / load_sgt (sgt_file.cpp:47-107): the reference's SGT1 writer and
+// reader, for byte-compatibility fixtures.
+int ref_save_sgt(void* h, const char* path) {
+  return guard([&] { save_sgt(*static_cast<TransformedGraph*>(h), path); });
+}
+int ref_load_sgt(const char* path, void** out) {
+  return guard([&] { *out = new TransformedGraph(load_sgt(path)); });
 }
 
 }  // extern "C"

@@ -273,7 +273,8 @@ class DeviceGraph:
                                      u64(out.stride(0)), _stream()))
         return out
 
-    def agnn_forward(self, x, betas, cut=None, precision="fp32", mode=3, return_zeros=False):
+    def agnn_forward(self, x, betas, cut=None, precision="fp32", mode=3, return_zeros=False,
+                     out=None):
         _f32_2d(x, "x")
         if x.shape[0] != self.num_cols:  # == num_nodes unless a row slice (full replica in)
             raise ShapeError("agnn_forward: x.rows != num_nodes")
@@ -281,7 +282,12 @@ class DeviceGraph:
         b = np.ascontiguousarray(betas, np.float32)
         ws_bytes = lib().sgtk_agnn_workspace(self._h, u64(d))
         ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=x.device)
-        out = torch.empty((self.info.num_nodes, d), dtype=torch.float32, device=x.device)
+        if out is None:
+            out = torch.empty((self.info.num_nodes, d), dtype=torch.float32, device=x.device)
+        elif tuple(out.shape) != (self.info.num_nodes, d):
+            raise ShapeError("agnn_forward: out shape != (num_nodes, d)")
+        else:
+            _f32_2d(out, "out")
         z = u64(0)
         cut = self._cut(cut)
         check(lib().sgtk_agnn_forward(self._h, _ptr(x), u64(x.stride(0)), u64(d), len(b),
@@ -303,12 +309,17 @@ def l2_normalize_rows(h: torch.Tensor, want_z=True):
     return z, inv, int(zeros.item())
 
 
-def gemm(a: torch.Tensor, w: torch.Tensor, relu=False, precision="fp32") -> torch.Tensor:
+def gemm(a: torch.Tensor, w: torch.Tensor, relu=False, precision="fp32", out=None) -> torch.Tensor:
     _f32_2d(a, "a")
     w = w.contiguous()
     if w.shape[0] != a.shape[1]:
         raise ShapeError("matmul: inner dimensions differ")
-    out = torch.empty((a.shape[0], w.shape[1]), dtype=torch.float32, device=a.device)
+    if out is None:
+        out = torch.empty((a.shape[0], w.shape[1]), dtype=torch.float32, device=a.device)
+    elif tuple(out.shape) != (a.shape[0], w.shape[1]):
+        raise ShapeError("matmul: out shape != (rows, cols)")
+    else:
+        _f32_2d(out, "out")
     check(lib().sgtk_gemm(_ptr(a), u64(a.stride(0)), _ptr(w), u64(a.shape[0]), u64(a.shape[1]),
                           u64(w.shape[1]), int(relu), _prec(precision), _ptr(out),
                           u64(out.stride(0)), _stream()))

@@ -9,9 +9,22 @@ splitting depends on a window alone, each rank's transform of its slice equals
 the global transform restricted to it, and every output row is bit-identical
 for 1/2/4/8 GPUs.
 
-Per layer the only exchange is the node-embedding all-gather:
-  AGNN: h_full -> (l2norm, fused attention on local rows) -> all-gather
-  GCN : h_local W (local rows) -> all-gather -> SpMM on local rows
+Replica layout (no copies around the collective).  Every rank keeps the node
+embeddings in a *padded* replica of `world * stride` rows: rank p's rows live
+at [p*stride, p*stride + n_p), `stride` = the largest slice rounded up to a
+whole panel.  Each rank's column ids are renumbered into that space once, when
+its slice is built (c -> owner(c)*stride + c - r0(owner); monotone, so the
+slice stays sorted-unique and its SGT structure — window uniques, ranks, tile
+maps — is the same as with global ids).  A layer writes its output rows
+straight into its own block of the next replica, and the exchange is ONE
+in-place `all_gather_into_tensor` over the replica (NCCL's in-place form:
+send buffer = the rank's block of the receive buffer).  Padding rows are never
+referenced by an edge.
+
+Per layer the only exchange is that all-gather:
+  AGNN: replica(h) -> layer on local rows (norms computed from the replica) -> all-gather
+  GCN : d_out < d_in: local h W into the replica -> all-gather -> SpMM (+ReLU)
+        otherwise   : h in the replica -> all-gather -> SpMM -> local GEMM (+ReLU)
 There is no other collective on the data path.
 """
 
@@ -52,77 +65,184 @@ def local_csr(node_pointer, edge_list, values, r0: int, r1: int):
     return np_loc, edge_list[e0:e1], None if values is None else values[e0:e1]
 
 
+def replica_stride(ranges: list[tuple[int, int]], quantum: int = ROW_QUANTUM) -> int:
+    """Rows per rank block in the padded replica (a whole number of panels,
+    so every block starts on a 16-row window boundary)."""
+    m = max(r1 - r0 for r0, r1 in ranges)
+    return max(quantum, (m + quantum - 1) // quantum * quantum)
+
+
+def remap_columns(edge_list, ranges: list[tuple[int, int]], stride: int):
+    """Global node ids -> padded-replica ids (monotone).  numpy or torch in,
+    same kind out (torch: computed on the tensor's device)."""
+    starts = [r0 for r0, _ in ranges]
+    if isinstance(edge_list, torch.Tensor):
+        el = edge_list.to(torch.int64)
+        st = torch.tensor(starts, dtype=torch.int64, device=el.device)
+        owner = torch.searchsorted(st, el, right=True) - 1
+        return (el + owner * stride - st[owner]).to(torch.int32)
+    el = np.asarray(edge_list, np.int64)
+    st = np.asarray(starts, np.int64)
+    owner = np.searchsorted(st, el, side="right") - 1
+    return (el + owner * stride - st[owner]).astype(np.uint32)
+
+
 def allgather_rows(local: torch.Tensor, ranges: list[tuple[int, int]], group=None) -> torch.Tensor:
-    """Concatenate every rank's row slice (uneven slices: padded collective)."""
+    """Concatenate every rank's row slice into an N-row matrix (uneven slices).
+    Assembly helper for checks and final outputs; the layer loop uses the
+    in-place padded replica (RowSlice.exchange) instead."""
     world = len(ranges)
     if world == 1:
         return local
-    maxr = max(r1 - r0 for r0, r1 in ranges)
-    pad = torch.zeros((maxr,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    stride = replica_stride(ranges, 1)
+    pad = torch.zeros((stride,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     pad[:local.shape[0]] = local
-    if dist.get_backend(group) == "nccl":
-        full = torch.empty((world * maxr,) + tuple(local.shape[1:]), dtype=local.dtype,
-                           device=local.device)
-        dist.all_gather_into_tensor(full, pad, group=group)
-        parts = [full[p * maxr: p * maxr + (r1 - r0)] for p, (r0, r1) in enumerate(ranges)]
-    else:
-        bufs = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(bufs, pad, group=group)
-        parts = [bufs[p][: r1 - r0] for p, (r0, r1) in enumerate(ranges)]
-    return torch.cat(parts)
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    return torch.cat([bufs[p][: r1 - r0] for p, (r0, r1) in enumerate(ranges)])
+
+
+def exchange_inplace(buf: torch.Tensor, rank: int, world: int, group=None) -> None:
+    """All-gather rank blocks of a padded replica in place.  NCCL: one
+    all_gather_into_tensor whose input is this rank's block of `buf`.  Other
+    backends (gloo: CPU tests, several ranks sharing one device) gather through
+    host copies of the blocks."""
+    if world == 1:
+        return
+    stride = buf.shape[0] // world
+    mine = buf[rank * stride:(rank + 1) * stride]
+    if buf.is_cuda and dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(buf, mine, group=group)
+        return
+    host = buf.cpu() if buf.is_cuda else buf
+    blocks = list(host.view(world, stride, *buf.shape[1:]).unbind(0))
+    dist.all_gather(blocks, host[rank * stride:(rank + 1) * stride].clone(), group=group)
+    if buf.is_cuda:
+        buf.copy_(host)
 
 
 class RowSlice:
-    """One rank's share of a graph: its row slice resident on this GPU."""
+    """One rank's share of a graph: its row slice resident on this GPU, with
+    column ids in the padded-replica space (see module docstring)."""
 
     def __init__(self, node_pointer, edge_list, values, num_nodes: int, rank: int, world: int,
-                 group=None, blk_h: int = 16, blk_w: int = 8):
-        from .device import DeviceGraph
-
+                 group=None, blk_h: int = 16, blk_w: int = 8, build_graph: bool = True):
         self.n = num_nodes
         self.rank, self.world, self.group = rank, world, group
         self.bounds = partition(node_pointer, num_nodes, world)  # whole 128-row panels
         self.ranges = row_ranges(self.bounds, num_nodes)
         self.r0, self.r1 = self.ranges[rank]
+        self.rows = self.r1 - self.r0
+        self.stride = replica_stride(self.ranges) if world > 1 else num_nodes
+        self.padded_rows = self.stride * world if world > 1 else num_nodes
+        self.offset = rank * self.stride if world > 1 else 0
         np_loc, el_loc, v_loc = local_csr(node_pointer, edge_list, values, self.r0, self.r1)
-        if world == 1:
-            self.graph = DeviceGraph.from_csr(np_loc, el_loc, v_loc, self.r1 - self.r0,
-                                              blk_h=blk_h, blk_w=blk_w)
-        else:
-            self.graph = DeviceGraph.from_csr(np_loc, el_loc, v_loc, self.r1 - self.r0, blk_h,
-                                              blk_w, num_cols=num_nodes, row_offset=self.r0)
+        if world > 1:
+            el_loc = remap_columns(el_loc, self.ranges, self.stride)
+        self.csr = (np_loc, el_loc, v_loc)
+        self.graph = None
+        if build_graph:
+            from .device import DeviceGraph
 
-    def allgather(self, local: torch.Tensor) -> torch.Tensor:
-        return allgather_rows(local, self.ranges, self.group)
+            if world == 1:
+                self.graph = DeviceGraph.from_csr(np_loc, el_loc, v_loc, self.rows,
+                                                  blk_h=blk_h, blk_w=blk_w)
+            else:
+                self.graph = DeviceGraph.from_csr(np_loc, el_loc, v_loc, self.rows, blk_h,
+                                                  blk_w, num_cols=self.padded_rows,
+                                                  row_offset=self.offset)
 
-    def agnn_forward(self, h_full: torch.Tensor, betas, precision="tf32", mode=1) -> torch.Tensor:
-        """All layers; returns this rank's rows of the last layer."""
+    # ---- replica management -------------------------------------------------
+    def replica(self, d: int, device=None, dtype=torch.float32) -> torch.Tensor:
+        """A zeroed padded replica [padded_rows, d] (padding rows stay zero)."""
+        return torch.zeros((self.padded_rows, d), dtype=dtype, device=device)
+
+    def mine(self, buf: torch.Tensor) -> torch.Tensor:
+        """This rank's rows inside a replica (a view: writes land in place)."""
+        return buf[self.offset:self.offset + self.rows]
+
+    def exchange(self, buf: torch.Tensor) -> None:
+        exchange_inplace(buf, self.rank, self.world, self.group)
+
+    def scatter_full(self, full: torch.Tensor, buf: torch.Tensor) -> torch.Tensor:
+        """Write an N-row matrix into the replica layout (inputs, tests)."""
         if self.world == 1:
-            return self.graph.agnn_forward(h_full, betas, precision=precision, mode=mode)
-        cur = h_full
-        for l in range(len(betas)):
-            loc = self.graph.agnn_forward(cur, np.asarray(betas[l:l + 1], np.float32),
-                                          precision=precision, mode=mode)
-            cur = self.allgather(loc) if l + 1 < len(betas) else loc
-        return cur
+            buf.copy_(full)
+            return buf
+        for p, (r0, r1) in enumerate(self.ranges):
+            buf[p * self.stride:p * self.stride + (r1 - r0)] = full[r0:r1]
+        return buf
 
-    def gcn_forward(self, x_local: torch.Tensor, layers, precision="tf32") -> torch.Tensor:
+    def gather_full(self, buf: torch.Tensor) -> torch.Tensor:
+        """Replica -> N-row matrix (outside any timed region)."""
+        if self.world == 1:
+            return buf
+        return torch.cat([buf[p * self.stride:p * self.stride + (r1 - r0)]
+                          for p, (r0, r1) in enumerate(self.ranges)])
+
+    # ---- layers -------------------------------------------------------------
+    def agnn_forward(self, h_rep: torch.Tensor, betas, precision="tf32", mode=3,
+                     scratch=None, out=None) -> torch.Tensor:
+        """All layers.  h_rep: the input replica (already exchanged; left
+        intact).  Every layer but the last writes its rows into a scratch
+        replica (two, used in turn) and exchanges it in place; returns this
+        rank's rows of the last layer."""
+        b = np.asarray(betas, np.float32)
+        if self.world == 1:
+            return self.graph.agnn_forward(h_rep, b, precision=precision, mode=mode, out=out)
+        if scratch is None:
+            scratch = (torch.zeros_like(h_rep), torch.zeros_like(h_rep))
+        src = h_rep
+        for l in range(len(b)):
+            if l + 1 == len(b):
+                return self.graph.agnn_forward(src, b[l:l + 1], precision=precision, mode=mode,
+                                               out=out)
+            dst = scratch[l % 2]
+            self.graph.agnn_forward(src, b[l:l + 1], precision=precision, mode=mode,
+                                    out=self.mine(dst))
+            self.exchange(dst)
+            src = dst
+        return self.mine(h_rep).clone() if out is None else out.copy_(self.mine(h_rep))
+
+    def gcn_forward(self, x_local: torch.Tensor, layers, precision="tf32",
+                    reps: dict | None = None) -> torch.Tensor:
         """Per layer, the same operand order as single-GPU gcn_forward(order=2):
-        d_out < d_in: local h W, all-gather(h W), SpMM, ReLU;
-        otherwise   : all-gather(h), SpMM, local GEMM with the ReLU epilogue.
-        Every row is computed exactly as on one GPU (bit-identical)."""
+        d_out < d_in: local h W (into the replica), all-gather, SpMM, ReLU;
+        otherwise   : h into the replica, all-gather, SpMM, local GEMM + ReLU.
+        Every row is computed exactly as on one GPU (bit-identical).  `reps`
+        caches replicas by width across calls."""
         from .device import gemm, relu_
 
         if self.world == 1:
             return self.graph.gcn_forward(x_local, layers, precision=precision, order=2)
+        reps = {} if reps is None else reps
+
+        def rep(d):
+            if d not in reps:
+                reps[d] = self.replica(d, device=x_local.device)
+            return reps[d]
+
+        def narrows(w):  # A (h W) order: all-gather the narrower h W
+            return w.shape[1] < w.shape[0]
+
         h = x_local
-        for w, relu in layers:
-            if w.shape[1] < w.shape[0]:
-                hw = gemm(h, w, relu=False, precision=precision)
-                h = self.graph.spmm(self.allgather(hw), precision=precision)
+        for l, (w, relu) in enumerate(layers):
+            nxt = layers[l + 1][0] if l + 1 < len(layers) else None
+            # a GEMM whose output the next layer all-gathers writes it in place
+            dst = self.mine(rep(w.shape[1])) if nxt is not None and not narrows(nxt) else None
+            if narrows(w):
+                r = rep(w.shape[1])
+                gemm(h, w, relu=False, precision=precision, out=self.mine(r))
+                self.exchange(r)
+                h = self.graph.spmm(r, precision=precision, out=dst)
                 if relu:
                     relu_(h)
             else:
-                agg = self.graph.spmm(self.allgather(h), precision=precision)
-                h = gemm(agg, w, relu=relu, precision=precision)
+                r = rep(w.shape[0])
+                m = self.mine(r)
+                if m.data_ptr() != h.data_ptr():
+                    m.copy_(h)  # layer-0 input (later layers land here already)
+                self.exchange(r)
+                h = gemm(self.graph.spmm(r, precision=precision), w, relu=relu,
+                         precision=precision, out=dst)
         return h

@@ -14,7 +14,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import paper_2412_12218_b200 as sg
-from paper_2412_12218_b200.distributed import allgather_rows, local_csr, partition, row_ranges
+from paper_2412_12218_b200.distributed import (RowSlice, allgather_rows, exchange_inplace,
+                                               local_csr, partition, remap_columns, row_ranges)
 from oracle.oracle import Csr, Oracle
 
 
@@ -84,11 +85,51 @@ def worker(rank, world, port, q):
         out_loc = O.spmm(sv, full_hw)
         out = allgather_rows(torch.from_numpy(out_loc), ranges).numpy()
         assert np.array_equal(out, O.spmm(gn, O.matmul(x, w)))
+        # the padded replica the GPU path uses: remapped column ids, rows
+        # written straight into this rank's block, one in-place all-gather
+        # per layer (distributed.RowSlice / exchange_inplace)
+        rs = RowSlice(g.node_pointer, g.edge_list, None, n, rank, world, build_graph=False)
+        assert rs.stride % 128 == 0 and rs.padded_rows == world * rs.stride
+        np_p, el_p, _ = rs.csr
+        for r in range(rs.rows):
+            row = el_p[int(np_p[r]):int(np_p[r + 1])].astype(np.int64)
+            assert np.all(np.diff(row) > 0)  # monotone remap keeps rows sorted-unique
+        sp = Csr.of(rs.rows, np_p, el_p)
+        rep = rs.replica(16)
+        rs.scatter_full(torch.from_numpy(x), rep)
+        h_rep = rep.numpy()
+        for l, b in enumerate(betas):
+            z, _ = O.l2_normalize_rows(h_rep)
+            logits = O.sddmm(sp, z[rs.offset:rs.offset + rs.rows], z,
+                             values=np.ones(sp.num_edges, np.float32)) * np.float32(b)
+            h_loc = O.spmm(sp, h_rep, values=O.edge_softmax(sp, logits))
+            nxt = rs.replica(16)
+            rs.mine(nxt).copy_(torch.from_numpy(h_loc))
+            rs.exchange(nxt)
+            h_rep = nxt.numpy()
+        assert np.array_equal(rs.gather_full(torch.from_numpy(h_rep)).numpy(), want)
+        # exchange_inplace leaves padding rows untouched and fills every block
+        buf = torch.full((world * 4, 2), -1.0)
+        buf[rank * 4:rank * 4 + 3] = float(rank)
+        exchange_inplace(buf, rank, world)
+        for p in range(world):
+            assert torch.all(buf[p * 4:p * 4 + 3] == p)
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e)))
     finally:
         dist.destroy_process_group()
+
+
+def test_remap_columns_monotone():
+    ranges = [(0, 300), (300, 520), (520, 1000)]
+    stride = 512
+    el = np.arange(1000, dtype=np.uint32)
+    m = remap_columns(el, ranges, stride)
+    assert np.all(np.diff(m.astype(np.int64)) > 0)
+    assert m[0] == 0 and m[300] == 512 and m[519] == 512 + 219 and m[520] == 1024
+    mt = remap_columns(torch.from_numpy(el.astype(np.int32)), ranges, stride)
+    assert np.array_equal(mt.numpy().astype(np.uint32), m)
 
 
 @pytest.mark.parametrize("world", [2, 3])

@@ -17,8 +17,12 @@ keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__throughput.avg.pct_of_peak_sustained_active",
         "sm__warps_active.avg.pct_of_peak_sustained_active",
         "smsp__issue_active.avg.pct_of_peak_sustained_active",
-        "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
-        "sm__pipe_tensor_subpipe_utcmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__ops_path_tensor_op_utchmma_src_tf32_dst_fp32.sum",
+        "sm__inst_executed_pipe_tc_scope_1cta.sum",
+        "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
         "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__grid_size",
         "launch__shared_mem_per_block_dynamic"]
 out = [f"# ncu --set full summary ({tag})\n",
