@@ -792,7 +792,7 @@ def profiled_tc_pipe(gcn=False):
             text = open(path).read()
         except OSError:
             continue
-        sec = text.split(f"`{kern}")
+        sec = text.split(f"{kern}<")
         if len(sec) < 2:
             continue
         m = re.search(r"\| sm__pipe_tensor_cycles_active\.avg\.pct_of_peak_sustained_active \| "

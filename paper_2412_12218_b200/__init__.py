@@ -272,6 +272,31 @@ def agnn_forward(t: TransformedGraph, x, betas, plan: HybridSplitPlan | None = N
 # --------------------------------------------------------------------------
 # Preprocessing and inputs
 # --------------------------------------------------------------------------
+def normalize_graph(g: CsrGraph, symmetrize: bool = False, add_self_loops: bool = False,
+                    dedupe: bool = True) -> CsrGraph:
+    """graph_io.cpp:195-259 on the GPU (bit-exact; bindings.cpp:209-216 defaults)."""
+    h = C.c_void_p()
+    np_ = np.ascontiguousarray(g.node_pointer, np.uint64)
+    el = np.ascontiguousarray(g.edge_list, np.uint32)
+    vals = None if g.values is None else np.ascontiguousarray(g.values, np.float32)
+    check(lib().sgtk_normalize_graph(np_.ctypes.data, el.ctypes.data,
+                                     None if vals is None else vals.ctypes.data,
+                                     g.num_nodes, el.shape[0], int(symmetrize),
+                                     int(add_self_loops), int(dedupe), 0, None, C.byref(h)))
+    try:
+        info = np.zeros(3, np.uint64)
+        check(lib().sgtk_csr_info(h, info.ctypes.data))
+        n, e, hv = (int(v) for v in info)
+        out_np = np.empty(n + 1, np.uint64)
+        out_el = np.empty(e, np.uint32)
+        out_v = np.empty(e, np.float32) if hv else None
+        check(lib().sgtk_csr_download(h, out_np.ctypes.data, out_el.ctypes.data,
+                                      None if out_v is None else out_v.ctypes.data))
+    finally:
+        lib().sgtk_csr_destroy(h)
+    return CsrGraph(n, out_np, out_el, out_v)
+
+
 def gcn_normalize_values(g: CsrGraph) -> CsrGraph:
     """graph_io.cpp:261-277 on the GPU (bit-exact: fp64 inv-sqrt-degrees)."""
     from .device import gcn_normalize_values as dev_norm
@@ -336,6 +361,6 @@ __all__ = [
     "NonFiniteError", "RangeError", "SgtkError", "ShapeError", "TileGeometry", "TileIndexError",
     "TransformedGraph", "agnn_forward", "block_stats", "csr_from_coo", "dense_random",
     "edge_softmax", "exported_symbols", "gather_tile", "gcn_forward", "gcn_normalize_values",
-    "l2_normalize_rows", "lib", "make_split_plan", "random_gcn_layers", "reblock", "sddmm_hybrid",
+    "l2_normalize_rows", "lib", "make_split_plan", "normalize_graph", "random_gcn_layers", "reblock", "sddmm_hybrid",
     "sgt_transform", "spmm_hybrid", "synth_graph", "tf32_round", "tf32_round_value",
 ]

@@ -133,13 +133,24 @@ __device__ __forceinline__ void fetch_tile(TileRegs<NB>& R, const DevGraph& G,
 #define SGTK_AGNN_MINB 1
 #endif
 
+// Any non-finite value among a lane's stored outputs -> *flag = 1 (warp vote,
+// one atomic per warp).  All lanes of the warp reach the epilogue together.
+template <int N>
+__device__ __forceinline__ void flag_nonfinite(const float (&a)[N], const float (&b)[N], bool va,
+                                               bool vb, int valid, uint32_t* flag) {
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < N; ++j) bad |= j < valid && ((va && !isfinite(a[j])) || (vb && !isfinite(b[j])));
+  if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
 template <int NB, int PREC, bool FULL>
 __global__ void __launch_bounds__(kWarps * 32, SGTK_AGNN_MINB)
 agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t n_units,
                   const uint32_t* __restrict__ thr, const float* __restrict__ h,
                   const float* __restrict__ z, uint64_t ldh, uint64_t ldz, uint64_t d, float beta,
                   float* __restrict__ out, uint64_t ldo, float* __restrict__ partial,
-                  uint64_t pstride) {
+                  uint64_t pstride, uint32_t* __restrict__ nonfinite) {
   const uint32_t wid = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (wid >= n_units) return;
   const WorkUnit u = units[wid];
@@ -330,7 +341,8 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
   const int64_t rem = int64_t(d) - int64_t(sf);
   const int svalid = rem <= 0 ? 0 : (rem > 2 * NB ? 2 * NB : int(rem));
   if (u.slot == kNoSlot) {
-    const float la = sa.l > 0.0f ? 1.0f / sa.l : 0.0f, lb = sb.l > 0.0f ? 1.0f / sb.l : 0.0f;
+    // l == 0: no edges; a NaN l (non-finite input) propagates
+    const float la = sa.l != 0.0f ? 1.0f / sa.l : 0.0f, lb = sb.l != 0.0f ? 1.0f / sb.l : 0.0f;
     float va_[2 * NB], vb_[2 * NB];
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
@@ -339,6 +351,7 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
     }
     if (va) store_seg<2 * NB, FULL>(out + ra * ldo + sf, va_, svalid);
     if (vb) store_seg<2 * NB, FULL>(out + rb * ldo + sf, vb_, svalid);
+    if (nonfinite) flag_nonfinite<2 * NB>(va_, vb_, va, vb, svalid, nonfinite);
   } else {
     // partial state: O[16][8*NB], then m[16] (log2 domain), l[16]
     float* P = partial + uint64_t(u.slot) * pstride;
@@ -363,7 +376,8 @@ agnn_fused_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t
 template <int NB>
 __global__ void agnn_merge_kernel(const ReduceItem* __restrict__ items, uint64_t n_rows,
                                   const float* __restrict__ partial, uint64_t pstride, uint64_t d,
-                                  float* __restrict__ out, uint64_t ldo) {
+                                  float* __restrict__ out, uint64_t ldo,
+                                  uint32_t* __restrict__ nonfinite) {
   const ReduceItem it = items[blockIdx.x];
   for (uint32_t i = threadIdx.x; i < 16u * 8u * NB; i += blockDim.x) {
     const uint32_t rr = i / (8 * NB), f = i % (8 * NB);
@@ -381,7 +395,9 @@ __global__ void agnn_merge_kernel(const ReduceItem* __restrict__ items, uint64_t
       L += P[16 * 8 * NB + 16 + rr] * sc;
       O += P[rr * 8 * NB + f] * sc;
     }
-    out[r * ldo + f] = L > 0.0f ? O * (1.0f / L) : 0.0f;
+    const float v = L != 0.0f ? O * (1.0f / L) : 0.0f;
+    out[r * ldo + f] = v;
+    if (nonfinite && !isfinite(v)) atomicOr(nonfinite, 1u);
   }
 }
 
@@ -427,7 +443,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
 agnn_fused_v3_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint32_t n_units,
                      const float* __restrict__ h, uint64_t ldh, const float* __restrict__ inv,
                      float beta, float* __restrict__ out, uint64_t ldo,
-                     float* __restrict__ partial, uint64_t pstride) {
+                     float* __restrict__ partial, uint64_t pstride, uint32_t* __restrict__ nonfinite) {
   constexpr int NB = 4;
   extern __shared__ __align__(16) uint8_t smem_v3[];
   const uint32_t wib = threadIdx.x >> 5;
@@ -596,7 +612,7 @@ agnn_fused_v3_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint3
   const uint64_t sf = 2u * t * NB;
   float va_[2 * NB], vb_[2 * NB];
   if (u.slot == kNoSlot) {
-    const float la = sa.l > 0.0f ? 1.0f / sa.l : 0.0f, lb = sb.l > 0.0f ? 1.0f / sb.l : 0.0f;
+    const float la = sa.l != 0.0f ? 1.0f / sa.l : 0.0f, lb = sb.l != 0.0f ? 1.0f / sb.l : 0.0f;
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
       va_[j] = o[j][0] * la; va_[NB + j] = o[j][1] * la;
@@ -604,6 +620,7 @@ agnn_fused_v3_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint3
     }
     if (va) store_seg<2 * NB, true>(out + ra * ldo + sf, va_, 2 * NB);
     if (vb) store_seg<2 * NB, true>(out + rb * ldo + sf, vb_, 2 * NB);
+    if (nonfinite) flag_nonfinite<2 * NB>(va_, vb_, va, vb, 2 * NB, nonfinite);
   } else {
     float* P = partial + uint64_t(u.slot) * pstride;
 #pragma unroll
@@ -624,7 +641,7 @@ agnn_fused_v3_kernel(const DevGraph G, const WorkUnit* __restrict__ units, uint3
 
 template <int PREC>
 void launch_v3(const sgtk_graph* g, const float* h, uint64_t ldh, const float* inv, float beta,
-               float* out, uint64_t ldo, cudaStream_t s) {
+               float* out, uint64_t ldo, uint32_t* nonfinite, cudaStream_t s) {
   const auto& P = g->plan16;
   const uint64_t pstride = 16 * 8 * 4 + 32;
   float* partial = nullptr;
@@ -632,11 +649,12 @@ void launch_v3(const sgtk_graph* g, const float* h, uint64_t ldh, const float* i
     CU(cudaMallocAsync(reinterpret_cast<void**>(&partial), uint64_t(P.n_slots) * pstride * 4, s));
   const size_t smem = size_t(kWarps) * kStages * sizeof(V3Slot);
   agnn_fused_v3_kernel<PREC><<<(P.n_units + kWarps - 1) / kWarps, kWarps * 32, smem, s>>>(
-      g->view(), P.units->as<WorkUnit>(), P.n_units, h, ldh, inv, beta, out, ldo, partial, pstride);
+      g->view(), P.units->as<WorkUnit>(), P.n_units, h, ldh, inv, beta, out, ldo, partial, pstride,
+      nonfinite);
   CU_LAUNCH("agnn_fused_v3_kernel");
   if (P.n_reduce) {
     agnn_merge_kernel<4><<<P.n_reduce, 256, 0, s>>>(P.reduce->as<ReduceItem>(), g->n_rows, partial,
-                                                    pstride, 32, out, ldo);
+                                                    pstride, 32, out, ldo, nonfinite);
     CU_LAUNCH("agnn_merge_kernel");
   }
   if (partial) CU(cudaFreeAsync(partial, s));
@@ -644,7 +662,8 @@ void launch_v3(const sgtk_graph* g, const float* h, uint64_t ldh, const float* i
 
 template <int NB, int PREC, bool FULL>
 void launch(const sgtk_graph* g, const uint32_t* thr, const float* h, uint64_t ldh, const float* z,
-            uint64_t ldz, uint64_t d, float beta, float* out, uint64_t ldo, cudaStream_t s) {
+            uint64_t ldz, uint64_t d, float beta, float* out, uint64_t ldo, uint32_t* nonfinite,
+            cudaStream_t s) {
   const auto& P = g->plan16;
   const uint64_t pstride = 16 * 8 * NB + 32;
   float* partial = nullptr;
@@ -652,11 +671,11 @@ void launch(const sgtk_graph* g, const uint32_t* thr, const float* h, uint64_t l
     CU(cudaMallocAsync(reinterpret_cast<void**>(&partial), uint64_t(P.n_slots) * pstride * 4, s));
   agnn_fused_kernel<NB, PREC, FULL><<<(P.n_units + kWarps - 1) / kWarps, kWarps * 32, 0, s>>>(
       g->view(), P.units->as<WorkUnit>(), P.n_units, thr, h, z, ldh, ldz, d, beta, out, ldo,
-      partial, pstride);
+      partial, pstride, nonfinite);
   CU_LAUNCH("agnn_fused_kernel");
   if (P.n_reduce) {
     agnn_merge_kernel<NB><<<P.n_reduce, 256, 0, s>>>(P.reduce->as<ReduceItem>(), g->n_rows,
-                                                     partial, pstride, d, out, ldo);
+                                                     partial, pstride, d, out, ldo, nonfinite);
     CU_LAUNCH("agnn_merge_kernel");
   }
   if (partial) CU(cudaFreeAsync(partial, s));
@@ -665,13 +684,13 @@ void launch(const sgtk_graph* g, const uint32_t* thr, const float* h, uint64_t l
 template <int NB>
 void dispatch(int prec, bool full, const sgtk_graph* g, const uint32_t* thr, const float* h,
               uint64_t ldh, const float* z, uint64_t ldz, uint64_t d, float beta, float* out,
-              uint64_t ldo, cudaStream_t s) {
+              uint64_t ldo, uint32_t* nf, cudaStream_t s) {
   if (prec == SGTK_FP32) {
-    if (full) launch<NB, SGTK_FP32, true>(g, thr, h, ldh, z, ldz, d, beta, out, ldo, s);
-    else launch<NB, SGTK_FP32, false>(g, thr, h, ldh, z, ldz, d, beta, out, ldo, s);
+    if (full) launch<NB, SGTK_FP32, true>(g, thr, h, ldh, z, ldz, d, beta, out, ldo, nf, s);
+    else launch<NB, SGTK_FP32, false>(g, thr, h, ldh, z, ldz, d, beta, out, ldo, nf, s);
   } else {
-    if (full) launch<NB, SGTK_TF32, true>(g, thr, h, ldh, z, ldz, d, beta, out, ldo, s);
-    else launch<NB, SGTK_TF32, false>(g, thr, h, ldh, z, ldz, d, beta, out, ldo, s);
+    if (full) launch<NB, SGTK_TF32, true>(g, thr, h, ldh, z, ldz, d, beta, out, ldo, nf, s);
+    else launch<NB, SGTK_TF32, false>(g, thr, h, ldh, z, ldz, d, beta, out, ldo, nf, s);
   }
 }
 
@@ -679,7 +698,8 @@ void dispatch(int prec, bool full, const sgtk_graph* g, const uint32_t* thr, con
 
 void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, const float* z,
                        uint64_t ldz, const float* inv, uint64_t d, float beta, int prec,
-                       const uint32_t* cut_dev, float* out, uint64_t ldo, cudaStream_t s) {
+                       const uint32_t* cut_dev, float* out, uint64_t ldo, cudaStream_t s,
+                       uint32_t* nonfinite) {
   if (prec != SGTK_FP32 && prec != SGTK_TF32)
     raise(SGTK_ERR_RANGE, "agnn_forward: precision must be FP32 or TF32");
   if (d > 64) raise(SGTK_ERR_SHAPE, "agnn_forward: fused mode supports d <= 64 (use mode 0)");
@@ -689,8 +709,8 @@ void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, const 
   // d == 32 with every tile on the tensor cores: the smem-staged v3 kernel
   if (d == 32 && !thr && !getenv("SGTK_AGNN_V2") && ldh % 4 == 0 && ldo % 4 == 0 &&
       reinterpret_cast<uintptr_t>(h) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0) {
-    if (prec == SGTK_FP32) launch_v3<SGTK_FP32>(g, h, ldh, inv, beta, out, ldo, s);
-    else launch_v3<SGTK_TF32>(g, h, ldh, inv, beta, out, ldo, s);
+    if (prec == SGTK_FP32) launch_v3<SGTK_FP32>(g, h, ldh, inv, beta, out, ldo, nonfinite, s);
+    else launch_v3<SGTK_TF32>(g, h, ldh, inv, beta, out, ldo, nonfinite, s);
     return;
   }
   const int nb = d <= 16 ? 2 : d <= 32 ? 4 : 8;
@@ -698,9 +718,9 @@ void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, const 
                     reinterpret_cast<uintptr_t>(h) % 16 == 0 &&
                     reinterpret_cast<uintptr_t>(z) % 16 == 0 &&
                     reinterpret_cast<uintptr_t>(out) % 16 == 0;
-  if (nb == 2) dispatch<2>(prec, full, g, thr, h, ldh, z, ldz, d, beta, out, ldo, s);
-  else if (nb == 4) dispatch<4>(prec, full, g, thr, h, ldh, z, ldz, d, beta, out, ldo, s);
-  else dispatch<8>(prec, full, g, thr, h, ldh, z, ldz, d, beta, out, ldo, s);
+  if (nb == 2) dispatch<2>(prec, full, g, thr, h, ldh, z, ldz, d, beta, out, ldo, nonfinite, s);
+  else if (nb == 4) dispatch<4>(prec, full, g, thr, h, ldh, z, ldz, d, beta, out, ldo, nonfinite, s);
+  else dispatch<8>(prec, full, g, thr, h, ldh, z, ldz, d, beta, out, ldo, nonfinite, s);
 }
 
 }  // namespace sgtkcu

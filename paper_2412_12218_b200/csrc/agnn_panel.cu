@@ -461,9 +461,16 @@ template <int FPL, int PREC>
 __device__ __forceinline__ void agnn_finalize(uint64_t r, const float (&o)[FPL], float l, uint32_t lane,
                                               int fv, const AgnnNext& nx, unsigned long long& nz) {
   float v[FPL];
-  const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;
+  // l == 0 only for a row without edges (every exp term is > 0); a NaN l
+  // (non-finite input) must propagate like the reference's softmax does
+  const float inv_l = l != 0.0f ? 1.0f / l : 0.0f;
+  bool bad = false;
 #pragma unroll
-  for (int i = 0; i < FPL; ++i) v[i] = l > 0.0f ? o[i] * inv_l : 0.0f;
+  for (int i = 0; i < FPL; ++i) {
+    v[i] = l != 0.0f ? o[i] * inv_l : 0.0f;
+    bad |= i < fv && !isfinite(v[i]);
+  }
+  if (nx.nonfinite && __any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(nx.nonfinite, 1u);
   const uint64_t f = uint64_t(lane) * FPL;
   if (nx.out) {
 #pragma unroll
@@ -662,18 +669,26 @@ __global__ void agnn_final_kernel(const uint4* __restrict__ items, uint64_t n_it
     float v[4] = {0.f, 0.f, 0.f, 0.f};
     float l = 0.0f;
     if (ok) {
-      const float4 a = *reinterpret_cast<const float4*>(opart + r * DC + f);
-      const float4 b = *reinterpret_cast<const float4*>(osp + r * DC + f);
+      // padding features [d, DC) of the partials are never written: skip them
+      const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 a = fv ? *reinterpret_cast<const float4*>(opart + r * DC + f) : z4;
+      const float4 b = fv ? *reinterpret_cast<const float4*>(osp + r * DC + f) : z4;
       l = lpart[r] + lsp[r];
-      const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;
+      const float inv_l = l != 0.0f ? 1.0f / l : 0.0f;  // NaN propagates (agnn_finalize)
       const float o[4] = {a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] = (l > 0.0f && i < fv) ? o[i] * inv_l : 0.0f;
+      for (int i = 0; i < 4; ++i) v[i] = (l != 0.0f && i < fv) ? o[i] * inv_l : 0.0f;
       if (nx.out) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           if (i < fv) nx.out[r * nx.ldo + f + i] = v[i];
       }
+    }
+    if (nx.nonfinite) {
+      bool bad = false;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) bad |= !isfinite(v[i]);
+      if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(nx.nonfinite, 1u);
     }
     if (!nx.zq) continue;  // last layer
     double sq = 0.0;
@@ -824,16 +839,34 @@ inline unsigned blocks_for(uint64_t n, unsigned bs = 256) {
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + bs - 1) / bs, 148ull * 16)));
 }
 
+// The CUDA-core half of a layer runs on an auxiliary stream.  One stream and
+// its two events per (host thread, device): concurrent callers never share an
+// event (no record/wait interleaving across threads) and every device gets
+// its own stream.  Created on first use, kept for the thread's lifetime.
+struct AuxStreams {
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ready = nullptr, join = nullptr;
+};
+
+const AuxStreams& aux_streams() {
+  thread_local std::vector<std::pair<int, AuxStreams>> per_dev;
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  for (auto& e : per_dev)
+    if (e.first == dev) return e.second;
+  AuxStreams a;
+  CU(cudaStreamCreateWithFlags(&a.aux, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&a.ready, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming));
+  per_dev.emplace_back(dev, a);
+  return per_dev.back().second;
+}
+
 template <int DC, int PREC>
 void launch_agnn_dense(const PanelView& v, uint64_t P, const float* zraw, const float* zq, const float* zq1,
                        const float* hq, const float* hq1, uint64_t ldq, uint64_t d,
                        uint64_t row_offset, float beta, float* opart, float* lpart, cudaStream_t s) {
   using C = AgnnCfg<DC, PREC>;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(agnn_dense_kernel<DC, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(C::SMEM));
-  });
   // SGTK_AGNN_DENSE_SMEM (bytes): pad the dense kernel's shared memory, e.g.
   // to hold one CTA per SM and leave room for the concurrent CUDA-core kernel
   static const uint32_t pad = [] {
@@ -841,8 +874,7 @@ void launch_agnn_dense(const PanelView& v, uint64_t P, const float* zraw, const 
     return e ? uint32_t(std::atoi(e)) : 0u;
   }();
   const uint32_t smem = std::max<uint32_t>(C::SMEM, std::min<uint32_t>(pad, 227u * 1024u));
-  static std::once_flag once2;
-  std::call_once(once2, [smem] {
+  once_per_device(reinterpret_cast<const void*>(&agnn_dense_kernel<DC, PREC>), [] {
     cudaFuncSetAttribute(agnn_dense_kernel<DC, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(227u * 1024u));
   });
@@ -887,13 +919,8 @@ void launch_agnn_rows(const Panels& pn, const float* zown, const float* z, uint6
     CU_LAUNCH("agnn_rows_kernel");
   }
   if (osp) {  // concurrent mode: join, then finalise on the main stream
-    static cudaEvent_t ev = [] {
-      cudaEvent_t e;
-      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-      return e;
-    }();
-    CU(cudaEventRecord(ev, s));
-    CU(cudaStreamWaitEvent(s_final, ev, 0));
+    CU(cudaEventRecord(aux_streams().join, s));
+    CU(cudaStreamWaitEvent(s_final, aux_streams().join, 0));
     if (pn.n_aitems) {
       agnn_final_kernel<FPL, PREC><<<final_grid(pn.n_aitems), 256, 0, s_final>>>(
           pn.aitems->as<uint4>(), pn.n_aitems, d, opart, lpart, osp, lsp, nx);
@@ -965,20 +992,11 @@ void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, cons
     rows(s, nullptr, nullptr, s);
     return;
   }
-  static cudaStream_t aux = [] {
-    cudaStream_t a;
-    cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking);
-    return a;
-  }();
-  static cudaEvent_t ready = [] {
-    cudaEvent_t e;
-    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    return e;
-  }();
-  CU(cudaEventRecord(ready, s));  // inputs of the layer are on s
-  CU(cudaStreamWaitEvent(aux, ready, 0));
+  const AuxStreams& ax = aux_streams();
+  CU(cudaEventRecord(ax.ready, s));  // inputs of the layer are on s
+  CU(cudaStreamWaitEvent(ax.aux, ax.ready, 0));
   dense(s);
-  rows(aux, osp, lsp, s);  // sparse partials on aux; final + hub rows join on s
+  rows(ax.aux, osp, lsp, s);  // sparse partials on aux; final + hub rows join on s
 }
 
 void agnn_input_launch(const float* x, uint64_t ldx, uint64_t rows, uint64_t d, uint64_t ldq, int prec,

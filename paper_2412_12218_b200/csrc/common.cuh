@@ -4,8 +4,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
+#include <mutex>
+#include <set>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "sgtk_cuda.h"
 
@@ -32,6 +36,19 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define CU_LAUNCH(what) ::sgtkcu::cuda_check(cudaGetLastError(), what)
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Runs fn once per (current device, key) — kernel attributes such as the
+// dynamic shared-memory ceiling are per device, so a process driving several
+// GPUs must set them on each.  fn runs under the lock: no launch on that
+// device can pass this point before the attribute is in place.
+inline void once_per_device(const void* key, const std::function<void()>& fn) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.insert({dev, key}).second) fn();
+}
 
 constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
 constexpr int kWinRows = 16;  // internal row-window height (MMA M)

@@ -6,6 +6,7 @@
 // O(windows) arithmetic, tf32_round_value on one float, file I/O) stay on the
 // host like the reference's.
 
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -44,13 +45,35 @@ inline void cuck(cudaError_t e) {
   if (e != cudaSuccess) throw Error(std::string("CUDA: ") + cudaGetErrorString(e));
 }
 
-// RAII device array
+// Device scratch for one drop-in call.  Stream-ordered allocations from the
+// device's default pool with its release threshold raised (the same pool the
+// C ABI's *_host entry points use, capi.cpp prepare_device), so a call's
+// inputs, outputs and workspace are recycled memory, not a fresh cudaMalloc /
+// cudaFree pair per call.  All drop-in work runs on the legacy default stream,
+// which orders these allocations with the synchronous copies around them.
+void keep_pool_cached() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  cuck(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  for (int d : done)
+    if (d == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~uint64_t(0);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.push_back(dev);
+}
+
 template <class T>
 struct Dev {
   T* p = nullptr;
   size_t n = 0;
   explicit Dev(size_t count) : n(count) {
-    if (count) cuck(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+    keep_pool_cached();
+    if (count) cuck(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), cudaStreamLegacy));
   }
   Dev(const T* host, size_t count) : Dev(count) {
     if (count) cuck(cudaMemcpy(p, host, count * sizeof(T), cudaMemcpyHostToDevice));
@@ -58,12 +81,26 @@ struct Dev {
   Dev(const Dev&) = delete;
   Dev& operator=(const Dev&) = delete;
   ~Dev() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, cudaStreamLegacy);
   }
   void get(T* host) const {
     if (n) cuck(cudaMemcpy(host, p, n * sizeof(T), cudaMemcpyDeviceToHost));
   }
 };
+
+// 64-bit content hash of a float array (4 words per step, order dependent):
+// the device cache must notice values edited in place.
+uint64_t content_hash(const std::vector<float>& v) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(v.data());
+  const size_t n = v.size();
+  uint64_t h[4] = {0x9E3779B97F4A7C15ull, 0xC2B2AE3D27D4EB4Full, 0x165667B19E3779F9ull,
+                   0x27D4EB2F165667C5ull};
+  size_t i = 0;
+  for (; i + 4 <= n; i += 4)
+    for (int k = 0; k < 4; ++k) h[k] = (h[k] ^ w[i + k]) * 0x100000001B3ull;
+  for (; i < n; ++i) h[0] = (h[0] ^ w[i]) * 0x100000001B3ull;
+  return h[0] ^ (h[1] * 31) ^ (h[2] * 131) ^ (h[3] * 1313) ^ n;
+}
 
 // Device graph cached on a TransformedGraph (its `device` member), tagged
 // with a fingerprint of the host fields it was built from.
@@ -73,17 +110,32 @@ struct DeviceCache {
   size_t nnz;
   uint64_t block_counter;
   uint32_t blk_w;
+  const void* val_data;  // csr.values: pointer, length and content
+  size_t n_vals;
+  uint64_t val_hash;
 };
 
 std::shared_ptr<sgtk_graph> own(sgtk_graph* g) {
   return std::shared_ptr<sgtk_graph>(g, [](sgtk_graph* p) { sgtk_graph_destroy(p); });
 }
 
+DeviceCache fingerprint(const TransformedGraph& t, std::shared_ptr<sgtk_graph> g) {
+  const auto& c = t.csr;
+  return DeviceCache{std::move(g),          c.edge_list.data(), c.num_edges(),
+                     t.block_counter,       t.geometry.blk_w,   c.values.data(),
+                     c.values.size(),       c.values.empty() ? 0 : content_hash(c.values)};
+}
+
+// The device copy is reused only while the host fields it was built from are
+// unchanged — including csr.values (pointer, length, content), which callers
+// may reassign or edit in place (the reference reads them on every call).
 sgtk_graph* device_of(const TransformedGraph& t) {
   if (t.device) {
     auto* c = static_cast<DeviceCache*>(t.device.get());
-    if (c->el_data == t.csr.edge_list.data() && c->nnz == t.csr.num_edges() &&
-        c->block_counter == t.block_counter && c->blk_w == t.geometry.blk_w)
+    const DeviceCache now = fingerprint(t, nullptr);
+    if (c->el_data == now.el_data && c->nnz == now.nnz && c->block_counter == now.block_counter &&
+        c->blk_w == now.blk_w && c->val_data == now.val_data && c->n_vals == now.n_vals &&
+        c->val_hash == now.val_hash)
       return c->g.get();
   }
   sgtk_graph* h = nullptr;
@@ -92,16 +144,12 @@ sgtk_graph* device_of(const TransformedGraph& t) {
                        g.has_values() ? g.values.data() : nullptr, g.num_nodes, g.num_edges(),
                        t.geometry.blk_h, t.geometry.blk_w, t.edge_to_column.data(),
                        t.window_offsets.data(), t.window_unique_cols.data(), nullptr, &h));
-  auto cache = std::make_shared<DeviceCache>(
-      DeviceCache{own(h), g.edge_list.data(), g.num_edges(), t.block_counter, t.geometry.blk_w});
-  t.device = cache;
+  t.device = std::make_shared<DeviceCache>(fingerprint(t, own(h)));
   return h;
 }
 
 void attach(TransformedGraph& t, std::shared_ptr<sgtk_graph> g) {
-  t.device = std::make_shared<DeviceCache>(DeviceCache{std::move(g), t.csr.edge_list.data(),
-                                                       t.csr.num_edges(), t.block_counter,
-                                                       t.geometry.blk_w});
+  t.device = std::make_shared<DeviceCache>(fingerprint(t, std::move(g)));
 }
 
 // tile_exec.cpp:35-42
@@ -393,6 +441,8 @@ SGTK_EXPORT DenseMatrix agnn_forward(const TransformedGraph& t, const DenseMatri
     od.get(out.data.data());
   } else {
     out = x;
+    // gnn.cpp:74-91: with no columns every row has a zero norm, in every layer
+    if (!x.cols) zeros = uint64_t(x.rows) * layers.size();
   }
   if (zero_norm_rows) *zero_norm_rows = zeros;
   return out;

@@ -100,7 +100,11 @@ void gcn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint32_t L,
       h_tf32 = tf && !last;
     } else {      // A (h W), ReLU after the aggregation
       gemm_launch(h, ldh, w, N, din, dout, 0, prec, tmp, ld4(dout), s, tf);
-      spmm_launch(g, tmp, ld4(dout), dout, cut, nullptr, prec, dst, ldd, flag, s, tf);
+      // A (h W) is not the reference's checked quantity A h: a hidden layer's
+      // -inf that its ReLU zeroes must not raise, so those layers are checked
+      // after the ReLU only (relu_nonfinite_launch)
+      spmm_launch(g, tmp, ld4(dout), dout, cut, nullptr, prec, dst, ldd,
+                  relu[l] && !last ? nullptr : flag, s, tf);
       if (relu[l] || last) relu_nonfinite_launch(dst, N, dout, ldd, relu[l], flag, s);
       h_tf32 = false;
     }
@@ -140,6 +144,19 @@ uint64_t agnn_workspace(const sgtk_graph* g, uint64_t d) {
 }
 
 namespace {
+// End of an AGNN forward: the zero-norm row count (u64) and the non-finite
+// flag (u32 right after it) come back in one copy.  spmm_hybrid throws
+// NonFiniteError for any layer whose output holds NaN/Inf
+// (tile_exec.cpp:311-312, via gnn.cpp:115); see nx.nonfinite for why the last
+// layer's check covers every layer.
+void finish_agnn(const uint64_t* zeros_dev, uint64_t* zero_rows_host, cudaStream_t s) {
+  uint64_t hv[2] = {0, 0};
+  CU(cudaMemcpyAsync(hv, zeros_dev, 16, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (zero_rows_host) *zero_rows_host = hv[0];
+  if (hv[1] & 0xFFFFFFFFull) raise(SGTK_ERR_NONFINITE, "agnn_forward: output contains NaN or Inf");
+}
+
 // mode 2: every layer on the 128-row panels (agnn_panel.cu)
 void agnn_forward_panel(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d, uint32_t L,
                         const float* betas, int prec, void* ws, float* out, uint64_t ldo,
@@ -165,7 +182,8 @@ void agnn_forward_panel(const sgtk_graph* g, const float* x, uint64_t ldx, uint6
   float* seg_o = take(std::max<uint64_t>(pn.n_segs, 1) * ldq * 4);
   float* seg_l = take(std::max<uint64_t>(pn.n_segs, 1) * 4);
   uint64_t* zeros = reinterpret_cast<uint64_t*>(p);
-  CU(cudaMemsetAsync(zeros, 0, 8, s));
+  uint32_t* flag = reinterpret_cast<uint32_t*>(zeros + 1);
+  CU(cudaMemsetAsync(zeros, 0, 16, s));
   // padding features [d, ldq) of every operand row must read as zeros
   if (d < ldq)
     CU(cudaMemsetAsync(set[0][0], 0, reinterpret_cast<char*>(set[1][4]) - reinterpret_cast<char*>(set[0][0]) +
@@ -182,6 +200,9 @@ void agnn_forward_panel(const sgtk_graph* g, const float* x, uint64_t ldx, uint6
     nx.ldo = last ? ldo : ldb;
     nx.ldq = ldq;
     nx.zeros = reinterpret_cast<unsigned long long*>(zeros);
+    // a NaN/Inf anywhere propagates to the last layer's rows (rows with
+    // edges read their own z), so checking the last layer's output suffices
+    nx.nonfinite = last ? flag : nullptr;
     if (!last) {
       nx.zq = nxt[1];
       nx.hq = nxt[3];
@@ -197,10 +218,7 @@ void agnn_forward_panel(const sgtk_graph* g, const float* x, uint64_t ldx, uint6
     agnn_panel_layer(g, cur[0], cur[1], cur[2], cur[3], cur[4], ldq, norm[l & 1], d, betas[l], prec,
                      opart, lpart, seg_o, seg_l, osp, lsp, nx, s);
   }
-  if (zero_rows_host) {
-    CU(cudaMemcpyAsync(zero_rows_host, zeros, 8, cudaMemcpyDeviceToHost, s));
-    CU(cudaStreamSynchronize(s));
-  }
+  finish_agnn(zeros, zero_rows_host, s);
 }
 }  // namespace
 
@@ -235,7 +253,8 @@ void agnn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
     }
     mode = d <= 64 ? 1 : 0;  // outside the panel path's envelope: fused 16-row windows, else the chain
   }
-  CU(cudaMemsetAsync(zeros, 0, 8, s));
+  uint32_t* flag = reinterpret_cast<uint32_t*>(zeros + 1);
+  CU(cudaMemsetAsync(zeros, 0, 16, s));
 
   if (L == 0) {
     CU(cudaMemcpy2DAsync(out, ldo * 4, x, ldx * 4, d * 4, N, cudaMemcpyDeviceToDevice, s));
@@ -250,7 +269,8 @@ void agnn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
     if (mode == 1) {
       // z = h * inv_norm materialised (as the reference does, gnn.cpp:109)
       l2norm_launch(h, l == 0 ? g->n_cols : N, d, ldh, zbuf, ldb, inv, zeros, s);
-      agnn_fused_launch(g, h, ldh, zbuf, ldb, inv, d, betas[l], prec, cut, dst, ldd, s);
+      agnn_fused_launch(g, h, ldh, zbuf, ldb, inv, d, betas[l], prec, cut, dst, ldd, s,
+                        last ? flag : nullptr);
     } else {
       l2norm_launch(h, l == 0 ? g->n_cols : N, d, ldh, nullptr, 0, inv, zeros, s);
       // The reference's SDDMM runs on reblock(t, 16) with make_split_plan(t16, ratio)
@@ -259,15 +279,12 @@ void agnn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
       sddmm_launch(g, h, ldh, h, ldh, d, cut, nullptr, /*unit_values=*/true, prec, inv,
                    betas[l], logits, s);
       edge_softmax_launch(g, logits, logits, s);
-      spmm_launch(g, h, ldh, d, cut, logits, prec, dst, ldd, nullptr, s);
+      spmm_launch(g, h, ldh, d, cut, logits, prec, dst, ldd, last ? flag : nullptr, s);
     }
     h = dst;
     ldh = ldd;
   }
-  if (zero_rows_host) {
-    CU(cudaMemcpyAsync(zero_rows_host, zeros, 8, cudaMemcpyDeviceToHost, s));
-    CU(cudaStreamSynchronize(s));
-  }
+  finish_agnn(zeros, zero_rows_host, s);
 }
 
 }  // namespace sgtkcu

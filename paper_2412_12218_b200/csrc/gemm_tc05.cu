@@ -385,8 +385,7 @@ bool gemm_tc05_launch(const float* a, uint64_t lda, const float* w, uint64_t m, 
   while (tmem_cols < n_pad) tmem_cols <<= 1;
   dim3 grid(unsigned((m + kBM - 1) / kBM));
   // the opt-in smem ceiling is set once per kernel (host overhead, not per call)
-  static std::once_flag attr_once;
-  std::call_once(attr_once, [] {
+  once_per_device(reinterpret_cast<const void*>(&gemm_tc05_kernel<SGTK_FP32>), [] {
     cudaFuncSetAttribute(gemm_tc05_kernel<SGTK_FP32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          227 * 1024);
     cudaFuncSetAttribute(gemm_tc05_kernel<SGTK_TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,

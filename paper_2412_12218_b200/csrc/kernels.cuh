@@ -37,7 +37,8 @@ void relu_nonfinite_launch(float* x, uint64_t rows, uint64_t cols, uint64_t ld, 
                            uint32_t* nonfinite, cudaStream_t s);
 void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, const float* z,
                        uint64_t ldz, const float* inv, uint64_t d, float beta, int prec,
-                       const uint32_t* cut_dev, float* out, uint64_t ldo, cudaStream_t s);
+                       const uint32_t* cut_dev, float* out, uint64_t ldo, cudaStream_t s,
+                       uint32_t* nonfinite = nullptr);
 
 // 128-row panel format + tcgen05 SpMM (panel.cu)
 Windows build_row_windows(const sgtk_graph& g, uint32_t bh, cudaStream_t s);
@@ -60,6 +61,7 @@ struct AgnnNext {
   float* norm;        // next layer |h| per row
   uint64_t ldq;
   unsigned long long* zeros;
+  uint32_t* nonfinite;  // set to 1 when an output value is NaN/Inf (last layer only)
 };
 bool agnn_panel_supported(const sgtk_graph* g, uint64_t d, float beta);
 void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, const float* zq1,

@@ -871,8 +871,7 @@ bool launch_dense(const PanelView& v, uint64_t P, uint32_t max_entries, const fl
                   uint32_t* nonfinite, cudaStream_t s) {
   PanelSmem L;
   if (!panel_smem<DC, PREC>(max_entries, L)) return false;
-  static std::once_flag once;
-  std::call_once(once, [] {
+  once_per_device(reinterpret_cast<const void*>(&spmm_panel_kernel<DC, PREC, false>), [] {
     cudaFuncSetAttribute(spmm_panel_kernel<DC, PREC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(kSmemCap));
     cudaFuncSetAttribute(spmm_panel_kernel<DC, PREC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

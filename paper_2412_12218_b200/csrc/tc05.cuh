@@ -154,8 +154,12 @@ __device__ __forceinline__ void st_shared_u32(uint32_t addr, uint32_t v) {
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// Named barrier over a subset of warps.  The non-.aligned form: the warps
+// arrive from mbarrier spin loops and lane-0-only branches, so the warp need
+// not be converged at this point (bar.sync = barrier.sync.aligned requires it;
+// compute-sanitizer synccheck flags the aligned form here).
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t threads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 // ---------------------------------------------------------------- UMMA

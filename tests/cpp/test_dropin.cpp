@@ -322,6 +322,33 @@ int main() {
     std::filesystem::remove(p + ".json");
     CHECK_THROWS_AS(load_gcn_layer(p), IoError);
   }
+  {  // the device copy follows csr.values edited in place (the cache
+     // fingerprint now covers values) and reassigned
+    CsrGraph g = random_graph(300, 6.0, 91, true);
+    TransformedGraph t = sgt_transform(g);
+    DenseMatrix x = DenseMatrix::random(300, 16, 5);
+    const auto p = make_split_plan(t);
+    CHECK(max_rel_err(spmm_hybrid(t, x, p), oracle_spmm(t.csr, x)) <= 1e-5);
+    for (float& v : t.csr.values) v *= 2.0f;  // same buffer, new content
+    CHECK(max_rel_err(spmm_hybrid(t, x, p), oracle_spmm(t.csr, x)) <= 1e-5);
+    t.csr.values = std::vector<float>(t.csr.values.size(), 0.5f);  // reassigned
+    CHECK(max_rel_err(spmm_hybrid(t, x, p), oracle_spmm(t.csr, x)) <= 1e-5);
+  }
+  {  // agnn_forward: NonFiniteError like spmm_hybrid (tile_exec.cpp:311-312 via
+     // gnn.cpp:115) in every mode; zero-width input counts rows x layers
+    CsrGraph gl = random_graph(200, 5.0, 92, false);
+    TransformedGraph t = sgt_transform(normalize_graph(gl, {false, true, true}));
+    DenseMatrix x = DenseMatrix::random(200, 32, 6);
+    x.at(17, 3) = std::numeric_limits<float>::infinity();
+    std::vector<AgnnLayerParams> al{{1.0f}, {0.5f}};
+    CHECK_THROWS_AS(agnn_forward(t, x, al, make_split_plan(t)), NonFiniteError);
+    x.at(17, 3) = std::numeric_limits<float>::quiet_NaN();
+    CHECK_THROWS_AS(agnn_forward(t, x, al, make_split_plan(t, 0.5)), NonFiniteError);
+    DenseMatrix x0(200, 0);
+    size_t zeros = 0;
+    agnn_forward(t, x0, al, make_split_plan(t), Precision::Fp32, 0, &zeros);
+    CHECK(zeros == 400);
+  }
   std::printf("%d/%d checks passed\n", g_checks - g_fail, g_checks);
   return g_fail ? 1 : 0;
 }

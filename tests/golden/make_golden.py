@@ -27,6 +27,7 @@ sys.path.insert(0, ROOT)
 from oracle.oracle import Csr, OracleError, RefLib  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
+OUT_CONFIGS = os.path.join(os.path.dirname(os.path.abspath(__file__)), "configs.npz")
 
 
 def graph_of(n, triples, weighted=False):
@@ -259,5 +260,66 @@ def main():
     print(f"wrote {OUT}: {len(G)} arrays, {os.path.getsize(OUT) / 1e6:.2f} MB")
 
 
+def identity_graph(R, n):
+    """The reference's own update GEMM through its public API (SURVEY §8a
+    note): gcn_forward(sgt_transform(identity(n)), X, {{W, relu}}) — identity
+    aggregation is exact (1.0f * x + 0)."""
+    g = Csr.of(n, np.arange(n + 1, dtype=np.uint64), np.arange(n, dtype=np.uint32),
+               np.ones(n, np.float32))
+    return R.transform_handle(g)
+
+
+def configs():
+    """BASELINE.json configs C1 and C2 end to end through the reference, on the
+    bench's own synthetic graphs and inputs (bench.make_graph with the
+    generator linked into oracle/_ref, DenseMatrix::random seed 8 = the
+    reference bench's seed + 7, random_gcn_layers seed 1; bench.cpp:114-135).
+    The reference's acceptance analogue: proj/tests/acceptance.cpp:191-225."""
+    import bench
+
+    R = RefLib()
+    G: dict[str, np.ndarray] = {}
+    # ---- C1: Cora-shaped GCN 1433 -> 16 -> 7 (normalize_graph + gcn values in the chain)
+    wl = bench.WORKLOADS["cora-gcn"]
+    g, _ = bench.make_graph(wl, "calibrated", synth=R.synth_graph)
+    gs = R.normalize_graph(g, True, True, True)
+    gn = R.gcn_normalize_values(gs)
+    th = R.transform_handle(gn)
+    x = R.dense_random(g.num_nodes, wl["d_in"], bench.INPUT_SEED)
+    layers = R.random_gcn_layers(wl["d_in"], wl["hidden"], wl["d_out"], wl["layers"],
+                                 bench.LAYER_SEED)
+    G["c1/n"] = np.array(g.num_nodes, np.uint64)
+    G["c1/node_pointer"], G["c1/edge_list"] = g.node_pointer, g.edge_list
+    G["c1/norm_node_pointer"], G["c1/norm_edge_list"] = gn.node_pointer, gn.edge_list
+    G["c1/gcn_values"] = gn.values
+    for tf in (0, 1):
+        G[f"c1/gcn_tf{tf}"] = R.gcn_forward(th, g.num_nodes, x, layers, 1.0, tf)
+    # ---- C2: Pubmed-shaped in-proj 500->32 (+ReLU), 4 x agnn_forward (beta 1), out-proj 32->3
+    wl = bench.WORKLOADS["pubmed-agnn"]
+    g, _ = bench.make_graph(wl, "calibrated", synth=R.synth_graph)
+    ga = R.normalize_graph(g, False, True, True)
+    tha = R.transform_handle(ga)
+    ident = identity_graph(R, g.num_nodes)
+    x = R.dense_random(g.num_nodes, wl["d_in"], bench.INPUT_SEED)
+    w_in = R.dense_random(wl["d_in"], wl["hidden"], 1, -0.1, 0.1)
+    w_out = R.dense_random(wl["hidden"], wl["d_out"], 2, -0.1, 0.1)
+    rows = np.unique(np.random.default_rng(2).integers(0, g.num_nodes, 2048))
+    G["c2/n"] = np.array(g.num_nodes, np.uint64)
+    G["c2/node_pointer"], G["c2/edge_list"] = ga.node_pointer, ga.edge_list
+    G["c2/w_in"], G["c2/w_out"], G["c2/rows"] = w_in, w_out, rows
+    for tf in (0, 1):
+        h0 = R.gcn_forward(ident, g.num_nodes, x, [(w_in, True)], 1.0, tf)
+        h4, zeros = R.agnn_forward(tha, h0, np.ones(wl["layers"], np.float32), 1.0, tf)
+        out = R.gcn_forward(ident, g.num_nodes, h4, [(w_out, False)], 1.0, tf)
+        G[f"c2/h0_tf{tf}_rows"] = h0[rows]
+        G[f"c2/h4_tf{tf}_rows"] = h4[rows]
+        G[f"c2/out_tf{tf}"] = out
+        G[f"c2/zeros_tf{tf}"] = np.array(zeros, np.uint64)
+    np.savez_compressed(OUT_CONFIGS, **G)
+    print(f"wrote {OUT_CONFIGS}: {len(G)} arrays, {os.path.getsize(OUT_CONFIGS) / 1e6:.2f} MB")
+
+
 if __name__ == "__main__":
-    main()
+    if "--configs" not in sys.argv:
+        main()
+    configs()

@@ -139,3 +139,34 @@ def test_split_plan_arithmetic():
         with pytest.raises(OracleError) as e:
             O.split_plan(t, bad)
         assert e.value.code == 8  # RangeError
+
+
+def test_oracle_matches_reference_configs():
+    """C1 / C2 (BASELINE.json) through the oracle restatement == the reference."""
+    import os
+
+    from oracle.oracle import Csr
+
+    z = dict(np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                  "configs.npz")))
+    O = Oracle()
+    n = int(z["c1/n"])
+    gs = O.normalize_graph(Csr.of(n, z["c1/node_pointer"], z["c1/edge_list"]), True, True, True)
+    gn = O.gcn_normalize_values(gs)
+    assert np.array_equal(gn.values, z["c1/gcn_values"])
+    x = O.dense_random(n, 1433, 8)
+    import paper_2412_12218_b200 as sg
+
+    layers = sg.random_gcn_layers(1433, 16, 7, 2, 1)
+    assert np.array_equal(O.gcn_forward(gn, x, layers), z["c1/gcn_tf0"])
+    assert np.array_equal(O.gcn_forward(gn, x, layers, tf32=True), z["c1/gcn_tf1"])
+    n = int(z["c2/n"])
+    ga = Csr.of(n, z["c2/node_pointer"], z["c2/edge_list"])
+    x = O.dense_random(n, 500, 8)
+    h0 = O.matmul(x, z["c2/w_in"], relu=True)
+    h4, zeros = O.agnn_forward(ga, h0, [1.0] * 4)
+    out = O.matmul(h4, z["c2/w_out"])
+    rows = z["c2/rows"]
+    assert np.array_equal(h0[rows], z["c2/h0_tf0_rows"])
+    assert np.array_equal(h4[rows], z["c2/h4_tf0_rows"])
+    assert np.array_equal(out, z["c2/out_tf0"])
