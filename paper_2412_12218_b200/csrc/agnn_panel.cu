@@ -478,15 +478,25 @@ __device__ __forceinline__ void agnn_finalize(uint64_t r, const float (&o)[FPL],
       if (i < fv) nx.out[r * nx.ldo + f + i] = v[i];
   }
   if (!nx.zq) return;
+  // The next layer's norm in exactly agnn_input_kernel's order (so a multi-
+  // layer call and per-layer calls — the row-partitioned path — agree bit for
+  // bit): groups of 4 features summed in sequence, then a butterfly over the
+  // groups (offsets 1, 2, 4[, 8] groups = G, 2G, 4G[, 8G] lanes).
+  constexpr uint32_t G = 4 / FPL;  // lanes per 4-feature group
+  double q[FPL];
+#pragma unroll
+  for (int i = 0; i < FPL; ++i) q[i] = i < fv ? double(v[i]) * double(v[i]) : 0.0;
+  const uint32_t g0 = lane & ~(G - 1);
   double sq = 0.0;
 #pragma unroll
-  for (int i = 0; i < FPL; ++i)
-    if (i < fv) sq += double(v[i]) * double(v[i]);
+  for (uint32_t k = 0; k < G; ++k)
 #pragma unroll
-  for (int o2 = 16; o2 > 0; o2 >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o2);
+    for (int i = 0; i < FPL; ++i) sq += __shfl_sync(0xFFFFFFFFu, q[i], g0 + k);
+#pragma unroll
+  for (uint32_t o2 = G; o2 < 32; o2 <<= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o2);
   const float inv = sq == 0.0 ? 0.0f : float(1.0 / sqrt(sq));
   if (sq == 0.0 && lane == 0) ++nz;
-  if (lane == 0 && nx.norm) nx.norm[r] = float(sqrt(sq));
+  if (lane == 0 && nx.norm) nx.norm[r] = inv > 0.0f ? 1.0f / inv : 0.0f;  // |h| = 1 / inv
 #pragma unroll
   for (int i = 0; i < FPL; ++i) {
     const float zz = i < fv ? v[i] * inv : 0.0f, hh = i < fv ? v[i] : 0.0f;
@@ -699,7 +709,7 @@ __global__ void agnn_final_kernel(const uint4* __restrict__ items, uint64_t n_it
     if (!ok) continue;
     const float inv = sq == 0.0 ? 0.0f : float(1.0 / sqrt(sq));
     if (sq == 0.0 && j == 0) ++nz;
-    if (j == 0 && nx.norm) nx.norm[r] = float(sqrt(sq));
+    if (j == 0 && nx.norm) nx.norm[r] = inv > 0.0f ? 1.0f / inv : 0.0f;  // as agnn_input_kernel
     float zz[4], hh[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
