@@ -108,11 +108,34 @@ int sgtk_graph_import(const uint64_t* node_pointer, const uint32_t* edge_list,
                       const uint32_t* window_unique_cols, void* stream,
                       sgtk_graph** out);
 
+/* Panel section (the 128-row panel formats the tcgen05 kernels run on),
+ * persisted beside an SGT1 file (sgt_file.cpp:47-107; SGT1 itself stays
+ * byte-compatible with the reference, whose reader rejects trailing bytes):
+ * "<file>.sgp" = magic "SGP1", version, graph fingerprint, both panel
+ * formats.  save writes g's formats; import_panels is sgtk_graph_import that
+ * loads them from `panel_section` when it matches this graph (skipping the
+ * panel build) and builds them otherwise; panels_loaded reports which. */
+int sgtk_graph_save_panels(const sgtk_graph* g, const char* path, void* stream);
+int sgtk_graph_import_panels(const uint64_t* node_pointer, const uint32_t* edge_list,
+                             const float* values, uint64_t num_nodes,
+                             uint64_t num_edges, uint32_t blk_h, uint32_t blk_w,
+                             const uint32_t* edge_to_column,
+                             const uint64_t* window_offsets,
+                             const uint32_t* window_unique_cols,
+                             const char* panel_section, void* stream,
+                             sgtk_graph** out);
+int sgtk_graph_panels_loaded(const sgtk_graph* g, int* loaded);
+
 void sgtk_graph_destroy(sgtk_graph* g);
 
 /* Sizes: {num_nodes, num_edges, num_windows, unique_cols, block_counter,
  *         blk_h, blk_w, has_values, tiles8, tiles16, work_units8} */
 int sgtk_graph_info(const sgtk_graph* g, uint64_t info[11]);
+/* Host wall time (ms) of each construction stage of g: upload, validate,
+ * edge_to_row, windows (user geometry), windows (16-row), tiles + work units,
+ * panel formats, 0.  Recorded only when the process sets SGTK_BUILD_TIMING
+ * (the build then synchronises at every stage boundary); zeros otherwise. */
+int sgtk_graph_build_times(const sgtk_graph* g, double ms[8]);
 
 /* Device pointers to the resident fields (read-only views; any may be NULL
  * for an empty graph).  Layout of `ptrs`:
@@ -252,7 +275,10 @@ uint64_t sgtk_gcn_workspace(const sgtk_graph* g, uint32_t num_layers,
  * explicit partial plan, to mode 0 for d > 64); mode 3 = auto: mode 2 for
  * graphs with >= 2M edges, else mode 1 (one launch per layer wins on small
  * graphs).  The Python API and the C++ drop-in default to mode 3.
- * zero_rows_host (may be NULL) receives the zero-norm row count (syncs). */
+ * zero_rows_host (may be NULL) receives the zero-norm row count; with it the
+ * call synchronises and returns SGTK_ERR_NONFINITE when the output holds NaN/Inf
+ * (gnn.cpp:115 -> tile_exec.cpp:311-312).  Without it the call is asynchronous
+ * and unchecked (as sgtk_spmm without a nonfinite pointer). */
 int sgtk_agnn_forward(const sgtk_graph* g, const float* x_dev, uint64_t ldx,
                       uint64_t d, uint32_t num_layers, const float* betas_host,
                       const uint32_t* cut_dev, int precision, int mode,

@@ -82,6 +82,11 @@ _SIGS = {
                                C.POINTER(vp)],
     "sgtk_graph_import": [vp, vp, vp, u64, u64, u32, u32, vp, vp, vp, vp, C.POINTER(vp)],
     "sgtk_graph_info": [vp, vp],
+    "sgtk_graph_save_panels": [vp, C.c_char_p, vp],
+    "sgtk_graph_import_panels": [vp, vp, vp, u64, u64, u32, u32, vp, vp, vp, C.c_char_p, vp,
+                                 C.POINTER(vp)],
+    "sgtk_graph_panels_loaded": [vp, C.POINTER(C.c_int)],
+    "sgtk_graph_build_times": [vp, vp],
     "sgtk_graph_device_ptrs": [vp, vp],
     "sgtk_panel_info": [vp, vp],
     "sgtk_panel_info_for": [vp, u64, vp],

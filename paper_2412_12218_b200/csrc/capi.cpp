@@ -131,6 +131,32 @@ int sgtk_graph_import(const uint64_t* np, const uint32_t* el, const float* vals,
   });
 }
 
+int sgtk_graph_import_panels(const uint64_t* np, const uint32_t* el, const float* vals,
+                             uint64_t n, uint64_t nnz, uint32_t blk_h, uint32_t blk_w,
+                             const uint32_t* e2c, const uint64_t* wo, const uint32_t* wuc,
+                             const char* panel_section, void* stream, sgtk_graph** out) {
+  return guard([&] {
+    need(out != nullptr, SGTK_ERR, "null output handle");
+    *out = graph_import(np, el, vals, n, nnz, blk_h, blk_w, e2c, wo, wuc, as_stream(stream),
+                        panel_section);
+  });
+}
+
+int sgtk_graph_save_panels(const sgtk_graph* g, const char* path, void* stream) {
+  return guard([&] {
+    check_graph(g);
+    need(path != nullptr, SGTK_ERR, "null path");
+    save_panel_section(*g, path, as_stream(stream));
+  });
+}
+
+int sgtk_graph_panels_loaded(const sgtk_graph* g, int* loaded) {
+  return guard([&] {
+    check_graph(g);
+    *loaded = g->panels_loaded ? 1 : 0;
+  });
+}
+
 void sgtk_graph_destroy(sgtk_graph* g) {
   if (g) {
     cudaDeviceSynchronize();
@@ -144,6 +170,13 @@ int sgtk_graph_info(const sgtk_graph* g, uint64_t info[11]) {
     const uint64_t v[11] = {g->n_rows, g->nnz, g->user.W, g->user.U, g->block_counter, g->blk_h,
                             g->blk_w, g->has_values ? 1u : 0u, g->T8, g->T16, g->plan8.n_units};
     std::memcpy(info, v, sizeof v);
+  });
+}
+
+int sgtk_graph_build_times(const sgtk_graph* g, double ms[8]) {
+  return guard([&] {
+    check_graph(g);
+    std::memcpy(ms, g->build_ms, sizeof g->build_ms);
   });
 }
 
@@ -457,9 +490,10 @@ int sgtk_agnn_forward_host(const sgtk_graph* g, const float* x_host, uint64_t d,
     char* cd = (char*)(((uintptr_t)(od + xb) + 255) & ~uintptr_t(255));
     CU(cudaMemcpyAsync(xd, x_host, xb, cudaMemcpyHostToDevice, s));
     if (!cut.empty()) CU(cudaMemcpyAsync(cd, cut.data(), cut.size() * 4, cudaMemcpyHostToDevice, s));
+    uint64_t zr = 0;  // the host entry always reports NaN/Inf (NonFiniteError)
     agnn_forward(g, reinterpret_cast<float*>(xd), d, d, L, betas,
                  cut.empty() ? nullptr : reinterpret_cast<uint32_t*>(cd), prec, mode, p, ws,
-                 reinterpret_cast<float*>(od), d, zero_rows, s);
+                 reinterpret_cast<float*>(od), d, zero_rows ? zero_rows : &zr, s);
     CU(cudaMemcpyAsync(out_host, od, xb, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
   });

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <fstream>
 #include <sstream>
+#include <type_traits>
 
 #include "sgtk/api.hpp"
 #include "sgtk_cuda.h"
@@ -539,81 +540,109 @@ SGTK_EXPORT CsrGraph gcn_normalize_values(const CsrGraph& g) {
 }
 
 // ----------------------------------------------------------------- sgt_file
-// "SGT1" container, byte-compatible with sgt_file.cpp:47-107.
+// "SGT1" container, byte-compatible with sgt_file.cpp:47-107: the magic, a
+// fixed header (geometry, a values flag, four counts), then the transform's
+// arrays back to back.  One table (sgt1_arrays) lists the arrays in file
+// order with their lengths, so the writer and the reader cannot drift apart.
+// The 128-row panel formats go to a sidecar "<file>.sgp" (the reference's
+// reader rejects trailing bytes, :101-102): written when the transform is
+// device-resident, loaded straight into the new device handle when present
+// and matching (sgtk_graph_import_panels), otherwise rebuilt on the GPU.
 namespace {
-template <class T>
-void wpod(std::ostream& os, T v) {
-  os.write(reinterpret_cast<const char*>(&v), sizeof(T));
+
+#pragma pack(push, 1)
+struct Sgt1Header {
+  char magic[4];
+  uint32_t blk_h, blk_w;
+  uint8_t flags;  // bit 0: csr.values present
+  uint64_t num_nodes, num_edges, num_windows, block_counter;
+};
+#pragma pack(pop)
+static_assert(sizeof(Sgt1Header) == 45, "SGT1 header is 45 packed bytes");
+
+struct Sgt1Array {
+  void* data;      // destination (load) / source (save)
+  uint64_t bytes;  // length in the file
+};
+
+// File-order arrays of t.  `sized` resizes them first (load), from the header
+// counts and, for the unique columns, the window offsets read just before.
+template <class Read>
+void sgt1_arrays(TransformedGraph& t, const Sgt1Header& h, bool sized, Read&& io) {
+  auto one = [&](auto& v, uint64_t count) {
+    using T = typename std::decay_t<decltype(v)>::value_type;
+    if (sized) {
+      if (count > (uint64_t(1) << 40) / sizeof(T)) throw IoError("SGT1: truncated payload");
+      v.resize(count);
+    }
+    io(Sgt1Array{v.data(), count * sizeof(T)});
+  };
+  const uint64_t E = h.num_edges;
+  one(t.csr.node_pointer, h.num_nodes + 1);
+  one(t.csr.edge_list, E);
+  if (h.flags & 1) one(t.csr.values, E);
+  one(t.edge_to_row, E);
+  one(t.edge_to_column, E);
+  one(t.block_partition, h.num_windows);
+  one(t.window_offsets, h.num_windows + 1);
+  if (t.window_offsets.empty() || t.window_offsets.front() != 0)
+    throw IoError("SGT1: corrupt window offsets");
+  one(t.window_unique_cols, t.window_offsets.back());
 }
-template <class T>
-void warr(std::ostream& os, const std::vector<T>& v) {
-  os.write(reinterpret_cast<const char*>(v.data()), std::streamsize(v.size() * sizeof(T)));
-}
-template <class T>
-T rpod(std::istream& is) {
-  T v{};
-  is.read(reinterpret_cast<char*>(&v), sizeof(T));
-  if (!is) throw IoError("SGT1: truncated header");
-  return v;
-}
-template <class T>
-void rarr(std::istream& is, std::vector<T>& v, uint64_t n) {
-  if (n > (uint64_t(1) << 40) / sizeof(T)) throw IoError("SGT1: truncated payload");
-  v.resize(n);
-  is.read(reinterpret_cast<char*>(v.data()), std::streamsize(n * sizeof(T)));
-  if (!is) throw IoError("SGT1: truncated payload");
-}
+
 }  // namespace
 
 SGTK_EXPORT void save_sgt(const TransformedGraph& t, const std::string& path) {
   std::ofstream os(path, std::ios::binary);
   if (!os) throw IoError("cannot write '" + path + "'");
-  os.write("SGT1", 4);
-  wpod<uint32_t>(os, t.geometry.blk_h);
-  wpod<uint32_t>(os, t.geometry.blk_w);
-  wpod<uint8_t>(os, t.csr.has_values() ? 1 : 0);
-  wpod<uint64_t>(os, t.csr.num_nodes);
-  wpod<uint64_t>(os, t.csr.num_edges());
-  wpod<uint64_t>(os, t.num_windows());
-  wpod<uint64_t>(os, t.block_counter);
-  warr(os, t.csr.node_pointer);
-  warr(os, t.csr.edge_list);
-  if (t.csr.has_values()) warr(os, t.csr.values);
-  warr(os, t.edge_to_row);
-  warr(os, t.edge_to_column);
-  warr(os, t.block_partition);
-  warr(os, t.window_offsets);
-  warr(os, t.window_unique_cols);
+  Sgt1Header h{{'S', 'G', 'T', '1'}, t.geometry.blk_h, t.geometry.blk_w,
+               uint8_t(t.csr.has_values() ? 1 : 0), t.csr.num_nodes, t.csr.num_edges(),
+               t.num_windows(), t.block_counter};
+  os.write(reinterpret_cast<const char*>(&h), sizeof h);
+  sgt1_arrays(const_cast<TransformedGraph&>(t), h, false, [&](const Sgt1Array& a) {
+    os.write(static_cast<const char*>(a.data), std::streamsize(a.bytes));
+  });
   if (!os) throw IoError("write failed for '" + path + "'");
+  os.close();
+  // panel section of a device-resident transform (up to date: device_of
+  // re-validates the cache against the host fields)
+  if (t.device) ck(sgtk_graph_save_panels(device_of(t), (path + ".sgp").c_str(), nullptr));
 }
 
 SGTK_EXPORT TransformedGraph load_sgt(const std::string& path) {
   std::ifstream is(path, std::ios::binary);
   if (!is) throw IoError("cannot open '" + path + "'");
-  char magic[4];
-  is.read(magic, 4);
-  if (!is || std::memcmp(magic, "SGT1", 4) != 0) throw IoError("SGT1: bad magic in '" + path + "'");
+  Sgt1Header h;
+  is.read(h.magic, 4);
+  if (!is || std::memcmp(h.magic, "SGT1", 4) != 0) throw IoError("SGT1: bad magic in '" + path + "'");
+  is.read(reinterpret_cast<char*>(&h) + 4, sizeof h - 4);
+  if (!is) throw IoError("SGT1: truncated header");
+  if (h.blk_h == 0 || h.blk_w == 0) throw IoError("SGT1: zero tile geometry");
   TransformedGraph t;
-  t.geometry.blk_h = rpod<uint32_t>(is);
-  t.geometry.blk_w = rpod<uint32_t>(is);
-  const uint8_t flags = rpod<uint8_t>(is);
-  const uint64_t n = rpod<uint64_t>(is), E = rpod<uint64_t>(is), W = rpod<uint64_t>(is);
-  t.block_counter = rpod<uint64_t>(is);
-  if (t.geometry.blk_h == 0 || t.geometry.blk_w == 0) throw IoError("SGT1: zero tile geometry");
-  t.csr.num_nodes = n;
-  rarr(is, t.csr.node_pointer, n + 1);
-  rarr(is, t.csr.edge_list, E);
-  if (flags & 1) rarr(is, t.csr.values, E);
-  rarr(is, t.edge_to_row, E);
-  rarr(is, t.edge_to_column, E);
-  rarr(is, t.block_partition, W);
-  rarr(is, t.window_offsets, W + 1);
-  if (t.window_offsets.front() != 0) throw IoError("SGT1: corrupt window offsets");
-  rarr(is, t.window_unique_cols, t.window_offsets.back());
+  t.geometry.blk_h = h.blk_h;
+  t.geometry.blk_w = h.blk_w;
+  t.block_counter = h.block_counter;
+  t.csr.num_nodes = h.num_nodes;
+  sgt1_arrays(t, h, true, [&](const Sgt1Array& a) {
+    is.read(static_cast<char*>(a.data), std::streamsize(a.bytes));
+    if (!is) throw IoError("SGT1: truncated payload");
+  });
   if (is.get() != std::ifstream::traits_type::eof())
     throw IoError("SGT1: trailing bytes in '" + path + "'");
   validate_csr(t.csr);
-  if (t.csr.node_pointer.back() != E) throw IoError("SGT1: inconsistent edge count");
+  if (t.csr.node_pointer.back() != h.num_edges) throw IoError("SGT1: inconsistent edge count");
+  // device handle, with the panel section when one sits beside the file
+  const std::string sgp = path + ".sgp";
+  if (std::ifstream(sgp, std::ios::binary).good() && t.csr.num_nodes) {
+    sgtk_graph* g = nullptr;
+    const auto& c = t.csr;
+    ck(sgtk_graph_import_panels(c.node_pointer.data(), c.edge_list.data(),
+                                c.has_values() ? c.values.data() : nullptr, c.num_nodes,
+                                c.num_edges(), t.geometry.blk_h, t.geometry.blk_w,
+                                t.edge_to_column.data(), t.window_offsets.data(),
+                                t.window_unique_cols.data(), sgp.c_str(), nullptr, &g));
+    attach(t, own(g));
+  }
   return t;
 }
 

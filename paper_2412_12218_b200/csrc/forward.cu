@@ -27,12 +27,15 @@ __global__ void relu_nonfinite_kernel(float* __restrict__ x, uint64_t rows, uint
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows * cols;
        i += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t r = i / cols, c = i - r * cols;
-    float v = x[r * ld + c];
+    const float v0 = x[r * ld + c];
+    float v = v0;
     if (relu) {
       v = v > 0.0f ? v : 0.0f;
       x[r * ld + c] = v;
     }
-    bad |= !isfinite(v);
+    // after a ReLU, -inf is zeroed like the reference's ReLU does; a NaN
+    // before it (inf - inf upstream) still counts
+    bad |= !isfinite(v) || isnan(v0);
   }
   if (nonfinite && __any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
 }
@@ -149,11 +152,16 @@ namespace {
 // NonFiniteError for any layer whose output holds NaN/Inf
 // (tile_exec.cpp:311-312, via gnn.cpp:115); see nx.nonfinite for why the last
 // layer's check covers every layer.
+// The synchronous check runs when the caller asks for the zero-row count
+// (every host-level API does: sg.agnn_forward, the drop-in, *_host); a
+// device-level call without it stays asynchronous, like sgtk_spmm without a
+// nonfinite pointer.
 void finish_agnn(const uint64_t* zeros_dev, uint64_t* zero_rows_host, cudaStream_t s) {
+  if (!zero_rows_host) return;
   uint64_t hv[2] = {0, 0};
   CU(cudaMemcpyAsync(hv, zeros_dev, 16, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
-  if (zero_rows_host) *zero_rows_host = hv[0];
+  *zero_rows_host = hv[0];
   if (hv[1] & 0xFFFFFFFFull) raise(SGTK_ERR_NONFINITE, "agnn_forward: output contains NaN or Inf");
 }
 

@@ -21,6 +21,8 @@
 #include <cub/device/device_segmented_radix_sort.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -501,6 +503,28 @@ void validate(const sgtk_graph& g, cudaStream_t s) {
   if (f & kVFinite) raise(SGTK_ERR, "csr: non-finite edge value");
 }
 
+// Stage timing of a graph build (SGTK_BUILD_TIMING): synchronise and take the
+// host clock at each stage boundary; a no-op otherwise.
+struct StageClock {
+  double* ms;
+  cudaStream_t s;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  StageClock(double* out, cudaStream_t st) : ms(out), s(st), on(std::getenv("SGTK_BUILD_TIMING")) {
+    if (on) {
+      CU(cudaStreamSynchronize(s));
+      t = std::chrono::steady_clock::now();
+    }
+  }
+  void mark(int stage) {
+    if (!on) return;
+    CU(cudaStreamSynchronize(s));
+    const auto now = std::chrono::steady_clock::now();
+    ms[stage] = std::chrono::duration<double, std::milli>(now - t).count();
+    t = now;
+  }
+};
+
 void build_e2r(sgtk_graph& g, cudaStream_t s) {
   g.e2r = std::make_shared<DevBuf>(std::max<uint64_t>(g.nnz, 1) * 4);
   if (g.n_rows && g.nnz) {
@@ -532,15 +556,23 @@ sgtk_graph* graph_create(const uint64_t* np, const uint32_t* el, const float* va
   g->row_offset = row_offset;
   g->blk_h = blk_h;
   g->blk_w = blk_w;
+  StageClock clk(g->build_ms, s);
   load_csr(*g, np, el, vals, kind, s);
+  clk.mark(0);
   validate(*g, s);
+  clk.mark(1);
   build_e2r(*g, s);
+  clk.mark(2);
   g->user = build_windows(*g, blk_h, s);
+  clk.mark(3);
   g->internal = blk_h == 16 ? g->user : build_windows(*g, 16, s);
+  clk.mark(4);
   set_partition(*g);
   g->bp = upload(g->bp_host.data(), g->bp_host.size(), s);
   finish_tiles(*g, s);
+  clk.mark(5);
   build_panels(*g, s);
+  clk.mark(6);
   g->scratch = std::make_shared<DevBuf>();
   return g.release();
 }
@@ -548,7 +580,7 @@ sgtk_graph* graph_create(const uint64_t* np, const uint32_t* el, const float* va
 sgtk_graph* graph_import(const uint64_t* np, const uint32_t* el, const float* vals,
                          uint64_t n_rows, uint64_t nnz, uint32_t blk_h, uint32_t blk_w,
                          const uint32_t* e2c, const uint64_t* wo, const uint32_t* wuc,
-                         cudaStream_t s) {
+                         cudaStream_t s, const char* panel_section) {
   if (blk_h == 0 || blk_w == 0) raise(SGTK_ERR_GEOMETRY, "tile dimensions must be positive");
   auto g = std::make_unique<sgtk_graph>();
   CU(cudaGetDevice(&g->device));
@@ -572,7 +604,7 @@ sgtk_graph* graph_import(const uint64_t* np, const uint32_t* el, const float* va
   set_partition(*g);
   g->bp = upload(g->bp_host.data(), g->bp_host.size(), s);
   finish_tiles(*g, s);
-  build_panels(*g, s);
+  if (!panel_section || !load_panel_section(*g, panel_section, s)) build_panels(*g, s);
   g->scratch = std::make_shared<DevBuf>();
   return g.release();
 }

@@ -129,9 +129,16 @@ struct sgtk_graph {
   sgtkcu::UnitPlan plan8, plan16;
   std::shared_ptr<sgtkcu::Panels> panels;    // 128-row panel format (panel.cu), kDenseMin
   std::shared_ptr<sgtkcu::Panels> panels32;  // same at kDenseMin32: operations with d <= 32
+  bool panels_loaded = false;                 // read from a panel section (no build_panels)
 
   // workspace for host-buffer entry points and forwards (mutable scratch)
   mutable std::shared_ptr<sgtkcu::DevBuf> scratch;
+
+  // Host wall time per construction stage (ms), recorded when SGTK_BUILD_TIMING
+  // is set (the stream is synchronised at every stage boundary, so the stages
+  // add up to the whole build): upload, validate, edge_to_row, windows (user
+  // geometry), windows (16-row internal), tiles + work units, panels.
+  double build_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
   sgtkcu::DevGraph view() const {
     sgtkcu::DevGraph v{};

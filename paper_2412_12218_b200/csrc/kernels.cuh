@@ -1,6 +1,8 @@
 // Internal launchers shared across translation units (host side).
 #pragma once
 
+#include <string>
+
 #include "graph.cuh"
 
 namespace sgtkcu {
@@ -11,7 +13,7 @@ sgtk_graph* graph_create(const uint64_t* np, const uint32_t* el, const float* va
 sgtk_graph* graph_import(const uint64_t* np, const uint32_t* el, const float* vals,
                          uint64_t n_rows, uint64_t nnz, uint32_t blk_h, uint32_t blk_w,
                          const uint32_t* e2c, const uint64_t* wo, const uint32_t* wuc,
-                         cudaStream_t s);
+                         cudaStream_t s, const char* panel_section = nullptr);
 sgtk_graph* graph_reblock(const sgtk_graph* src, uint32_t blk_w, cudaStream_t s);
 
 void spmm_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
@@ -43,8 +45,17 @@ void agnn_fused_launch(const sgtk_graph* g, const float* h, uint64_t ldh, const 
 // 128-row panel format + tcgen05 SpMM (panel.cu)
 Windows build_row_windows(const sgtk_graph& g, uint32_t bh, cudaStream_t s);
 void build_panels(sgtk_graph& g, cudaStream_t s);
+// Panel section beside an SGT1 file (panel.cu): save / load (false when the
+// section is absent, of another version or of another graph).
+void save_panel_section(const sgtk_graph& g, const std::string& path, cudaStream_t s);
+bool load_panel_section(sgtk_graph& g, const std::string& path, cudaStream_t s);
 // x_tf32: x is already TF32-rounded (RNE) by its producer (the fused GEMM
 // epilogue), so the TF32 path skips its rounding pass over x.
+// SDDMM on the panel format (sddmm_panel.cu): tcgen05 dense columns + CUDA-core
+// sparse edges; false outside its envelope (the 16-row kernel then runs).
+bool sddmm_panel_launch(const sgtk_graph* g, const float* x, uint64_t ldx, const float* y,
+                        uint64_t ldy, uint64_t d, const float* ev, bool unit_values, int prec,
+                        const float* inv_norm, float scale, float* out, cudaStream_t s);
 bool spmm_panel_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d,
                        const float* ev, int prec, float* out, uint64_t ldo, uint32_t* nonfinite,
                        cudaStream_t s, bool x_tf32 = false);

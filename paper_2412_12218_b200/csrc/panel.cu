@@ -43,7 +43,9 @@
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "kernels.cuh"
@@ -1090,6 +1092,147 @@ std::shared_ptr<Panels> build_panel_format(sgtk_graph& g, uint32_t dense_min, cu
   return pn;
 }
 }  // namespace
+
+// ------------------------------------------------------------ panel section
+// SGT1 (sgt_file.cpp:47-107) stores the reference's TransformedGraph and its
+// reader rejects trailing bytes (:101-102), so the panel formats are persisted
+// beside it, in "<file>.sgp": magic "SGP1", a format version, a fingerprint
+// of the graph they belong to, then per panel format its scalars and its
+// device arrays as (byte length, bytes) records.  Loading uploads the arrays
+// into the new handle and skips build_panels.
+namespace {
+constexpr char kSgpMagic[4] = {'S', 'G', 'P', '1'};
+constexpr uint32_t kSgpVersion = 1;
+
+uint64_t fnv(uint64_t h, const void* p, size_t n) {
+  const auto* b = static_cast<const unsigned char*>(p);
+  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001B3ull;
+  return h;
+}
+
+// The graph a panel section belongs to: sizes, geometry, node_pointer, and
+// 64 evenly spaced 1 KiB windows of edge_list (a consistency check against
+// stale sidecars, not a cryptographic one).
+uint64_t graph_fingerprint(const sgtk_graph& g, cudaStream_t s) {
+  uint64_t h = 0xCBF29CE484222325ull;
+  const uint64_t hdr[7] = {g.n_rows, g.n_cols, g.nnz, g.blk_h, g.blk_w, g.block_counter, g.user.U};
+  h = fnv(h, hdr, sizeof hdr);
+  std::vector<uint64_t> np = dl<uint64_t>(g.np->p, g.n_rows + 1, s);
+  h = fnv(h, np.data(), np.size() * 8);
+  std::vector<uint32_t> win(256);
+  for (uint64_t k = 0; k < 64 && g.nnz; ++k) {
+    const uint64_t at = std::min<uint64_t>(g.nnz - 1, g.nnz * k / 64);
+    const uint64_t cnt = std::min<uint64_t>(256, g.nnz - at);
+    CU(cudaMemcpyAsync(win.data(), g.el->as<uint32_t>() + at, cnt * 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    h = fnv(h, win.data(), cnt * 4);
+  }
+  return h;
+}
+
+template <class T>
+void put(std::FILE* f, const T& v) {
+  if (std::fwrite(&v, sizeof v, 1, f) != 1) raise(SGTK_ERR_IO, "SGP1: write failed");
+}
+template <class T>
+T get(std::FILE* f) {
+  T v{};
+  if (std::fread(&v, sizeof v, 1, f) != 1) raise(SGTK_ERR_IO, "SGP1: truncated section");
+  return v;
+}
+void put_buf(std::FILE* f, const std::shared_ptr<DevBuf>& b, cudaStream_t s) {
+  const uint64_t n = b ? b->bytes : 0;
+  put(f, n);
+  if (!n) return;
+  std::vector<char> h = dl<char>(b->p, n, s);
+  if (std::fwrite(h.data(), 1, n, f) != n) raise(SGTK_ERR_IO, "SGP1: write failed");
+}
+std::shared_ptr<DevBuf> get_buf(std::FILE* f, cudaStream_t s) {
+  const uint64_t n = get<uint64_t>(f);
+  std::vector<char> h(n);
+  if (n && std::fread(h.data(), 1, n, f) != n) raise(SGTK_ERR_IO, "SGP1: truncated section");
+  auto b = std::make_shared<DevBuf>(std::max<uint64_t>(n, 16));
+  if (n) CU(cudaMemcpyAsync(b->p, h.data(), n, cudaMemcpyHostToDevice, s));
+  CU(cudaStreamSynchronize(s));
+  return b;
+}
+
+void put_format(std::FILE* f, const Panels& pn, uint32_t dense_min, cudaStream_t s) {
+  put(f, dense_min);
+  const uint64_t sc[9] = {pn.P, pn.n_chunks, pn.n_dent, pn.n_sparse, pn.max_chunk_entries,
+                          pn.n_items, pn.n_long, pn.n_segs, pn.n_aitems};
+  for (uint64_t v : sc) put(f, v);
+  for (const auto* b : {&pn.cptr, &pn.dcols, &pn.coff, &pn.dent, &pn.dval, &pn.deid, &pn.dmask,
+                        &pn.sptr, &pn.sent, &pn.seid, &pn.items, &pn.lrows, &pn.aitems})
+    put_buf(f, *b, s);
+}
+
+std::shared_ptr<Panels> get_format(std::FILE* f, uint32_t want_min, cudaStream_t s) {
+  if (get<uint32_t>(f) != want_min) raise(SGTK_ERR_IO, "SGP1: unexpected panel format");
+  auto pn = std::make_shared<Panels>();
+  uint64_t sc[9];
+  for (uint64_t& v : sc) v = get<uint64_t>(f);
+  pn->P = sc[0];
+  pn->n_chunks = sc[1];
+  pn->n_dent = sc[2];
+  pn->n_sparse = sc[3];
+  pn->max_chunk_entries = uint32_t(sc[4]);
+  pn->n_items = sc[5];
+  pn->n_long = sc[6];
+  pn->n_segs = sc[7];
+  pn->n_aitems = sc[8];
+  for (auto* b : {&pn->cptr, &pn->dcols, &pn->coff, &pn->dent, &pn->dval, &pn->deid, &pn->dmask,
+                  &pn->sptr, &pn->sent, &pn->seid, &pn->items, &pn->lrows, &pn->aitems})
+    *b = get_buf(f, s);
+  return pn;
+}
+}  // namespace
+
+void save_panel_section(const sgtk_graph& g, const std::string& path, cudaStream_t s) {
+  if (!g.panels || !g.panels32) raise(SGTK_ERR, "graph has no panel formats");
+  std::FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) raise(SGTK_ERR_IO, "cannot write '" + path + "'");
+  try {
+    if (std::fwrite(kSgpMagic, 1, 4, f) != 4) raise(SGTK_ERR_IO, "SGP1: write failed");
+    put(f, kSgpVersion);
+    put(f, graph_fingerprint(g, s));
+    put_format(f, *g.panels, kDenseMin, s);
+    put_format(f, *g.panels32, kDenseMin32, s);
+  } catch (...) {
+    std::fclose(f);
+    throw;
+  }
+  if (std::fclose(f) != 0) raise(SGTK_ERR_IO, "SGP1: write failed");
+}
+
+// Loads the panel formats of `path` into g when the section exists, has this
+// version and belongs to this graph (fingerprint); false otherwise (the
+// caller builds them).  A section that matches but is damaged raises.
+bool load_panel_section(sgtk_graph& g, const std::string& path, cudaStream_t s) {
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) return false;
+  bool ok = false;
+  try {
+    char magic[4];
+    if (std::fread(magic, 1, 4, f) == 4 && std::memcmp(magic, kSgpMagic, 4) == 0 &&
+        get<uint32_t>(f) == kSgpVersion && get<uint64_t>(f) == graph_fingerprint(g, s)) {
+      auto a = get_format(f, kDenseMin, s);
+      auto b = get_format(f, kDenseMin32, s);
+      const uint64_t P = (g.n_rows + kPanelRows - 1) / kPanelRows;
+      if (a->P != P || b->P != P) raise(SGTK_ERR_IO, "SGP1: panel count does not match the graph");
+      if (std::fgetc(f) != EOF) raise(SGTK_ERR_IO, "SGP1: trailing bytes");
+      g.panels = a;
+      g.panels32 = b;
+      g.panels_loaded = true;
+      ok = true;
+    }
+  } catch (...) {
+    std::fclose(f);
+    throw;
+  }
+  std::fclose(f);
+  return ok;
+}
 
 // Two panel formats per graph, differing only in the dense-column threshold:
 // measured, 2-edge columns are cheaper on the CUDA cores for d <= 32 (AGNN

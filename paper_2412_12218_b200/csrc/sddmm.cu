@@ -14,7 +14,7 @@
 // Feature layout: k-column k of chunk s maps to feature fb + k*KS + s, so a
 // lane's A and B fragments are two contiguous KS-float segments (vector loads).
 
-#include "graph.cuh"
+#include "kernels.cuh"
 
 namespace sgtkcu {
 namespace {
@@ -236,6 +236,12 @@ void sddmm_launch(const sgtk_graph* g, const float* x, uint64_t ldx, const float
   }
   const float* vals =
       ev ? ev : (unit_values || !g->has_values ? nullptr : g->vals->as<float>());
+  // default plan: the 128-row panels (tcgen05 dense columns + CUDA-core
+  // sparse edges, sddmm_panel.cu); explicit partial plans keep the
+  // reference's 16-row tile split below
+  if (!cut16_dev &&
+      sddmm_panel_launch(g, x, ldx, y, ldy, d, ev, unit_values, prec, inv_norm, scale, out, s))
+    return;
   const bool vec = (ldx % 4 == 0) && (ldy % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(y) % 16 == 0);
   const auto& P = g->plan16;

@@ -154,6 +154,15 @@ class DeviceGraph:
         out["block_counter"] = np.array(i.block_counter, np.uint64)
         return out
 
+    def build_times(self) -> dict:
+        """Per-stage host wall time (ms) of this graph's build; populated when
+        the process set SGTK_BUILD_TIMING before building (sgtk_graph_build_times)."""
+        a = np.zeros(8, np.float64)
+        check(lib().sgtk_graph_build_times(self._h, a.ctypes.data))
+        names = ["upload", "validate", "edge_to_row", "windows_user", "windows_16",
+                 "tiles_units", "panels"]
+        return {k: round(float(v), 3) for k, v in zip(names, a)}
+
     def panel_info(self, d: int | None = None) -> dict:
         """128-row panel format sizes (sgtk_panel_info); with d, of the format
         an operation of width d runs on (sgtk_panel_info_for)."""

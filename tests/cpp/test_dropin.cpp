@@ -16,6 +16,7 @@
 #include <unistd.h>
 
 #include "sgtk/gnn.hpp"
+#include "sgtk_cuda.h"
 #include "sgtk/graph_io.hpp"
 #include "sgtk/sgt_file.hpp"
 #include "sgtk/sgt_transform.hpp"
@@ -82,7 +83,10 @@ static DenseMatrix oracle_spmm(const CsrGraph& g, const DenseMatrix& x) {
   return o;
 }
 
-int main() {
+static std::string g_golden = "tests/golden";
+
+int main(int argc, char** argv) {
+  if (argc > 1) g_golden = argv[1];
   // --- translator (test_sgt_transform.cpp:47-111, 169-224) ---------------
   {
     TransformedGraph t = sgt_transform(identity_graph(16));
@@ -146,7 +150,72 @@ int main() {
     CHECK_THROWS_AS(load_sgt(p + ".g"), IoError);
     std::ofstream(p + ".m") << "NOPE";
     CHECK_THROWS_AS(load_sgt(p + ".m"), IoError);
-    for (auto s : {"", ".t", ".g", ".m"}) std::filesystem::remove(p + s);
+    for (auto s : {"", ".t", ".g", ".m", ".sgp"}) std::filesystem::remove(p + s);
+  }
+  {  // SGT1 files written by the REFERENCE's save_sgt (tests/golden/ref_*.sgt,
+     // make_golden.py --sgt): load_sgt reads them, and save_sgt of what it
+     // read reproduces them byte for byte (sgt_file.cpp:47-107)
+    for (const char* name : {"ref_rand3_16x8.sgt", "ref_rand0_3x5.sgt"}) {
+      const std::string src = g_golden + "/" + name;
+      std::ifstream in(src, std::ios::binary);
+      CHECK(in.good());
+      const std::string want((std::istreambuf_iterator<char>(in)), {});
+      TransformedGraph b = load_sgt(src);
+      // the same transform from the drop-in's GPU translator
+      TransformedGraph t = sgt_transform(b.csr, b.geometry);
+      CHECK(b.edge_to_row == t.edge_to_row && b.edge_to_column == t.edge_to_column &&
+            b.block_partition == t.block_partition && b.window_offsets == t.window_offsets &&
+            b.window_unique_cols == t.window_unique_cols && b.block_counter == t.block_counter);
+      const std::string out = (std::filesystem::temp_directory_path() /
+                               ("dropin_ref_" + std::to_string(getpid()) + ".sgt")).string();
+      save_sgt(b, out);  // b is host-only: SGT1 bytes, no panel section
+      std::ifstream o(out, std::ios::binary);
+      const std::string got((std::istreambuf_iterator<char>(o)), {});
+      CHECK(got == want);
+      CHECK(!std::filesystem::exists(out + ".sgp"));
+      std::filesystem::remove(out);
+    }
+  }
+  {  // panel section: save_sgt of a device-resident transform writes <file>.sgp;
+     // load_sgt imports the panel formats from it (no panel build) and the
+     // kernels give bit-identical results to a freshly built handle
+    const std::string p = (std::filesystem::temp_directory_path() /
+                           ("dropin_sgp_" + std::to_string(getpid()) + ".sgt")).string();
+    CsrGraph g = gcn_normalize_values(normalize_graph(random_graph(5000, 24, 77, false),
+                                                      {true, true, true}));
+    TransformedGraph t = sgt_transform(g);
+    save_sgt(t, p);
+    CHECK(std::filesystem::exists(p + ".sgp"));
+    TransformedGraph b = load_sgt(p);
+    DenseMatrix x = DenseMatrix::random(5000, 32, 8);
+    for (Precision pr : {Precision::Fp32, Precision::Tf32})
+      CHECK(spmm_hybrid(b, x, make_split_plan(b), pr).data ==
+            spmm_hybrid(t, x, make_split_plan(t), pr).data);
+    // through the C ABI: the handle reports its panels came from the file
+    sgtk_graph* h = nullptr;
+    const auto& c = b.csr;
+    CHECK(sgtk_graph_import_panels(c.node_pointer.data(), c.edge_list.data(), c.values.data(),
+                                   c.num_nodes, c.num_edges(), 16, 8, b.edge_to_column.data(),
+                                   b.window_offsets.data(), b.window_unique_cols.data(),
+                                   (p + ".sgp").c_str(), nullptr, &h) == SGTK_OK);
+    int loaded = 0;
+    sgtk_graph_panels_loaded(h, &loaded);
+    CHECK(loaded == 1);
+    sgtk_graph_destroy(h);
+    // a section of another graph is ignored (fingerprint): panels rebuilt
+    CsrGraph g2 = gcn_normalize_values(normalize_graph(random_graph(5000, 24, 78, false),
+                                                       {true, true, true}));
+    TransformedGraph t2 = sgt_transform(g2);
+    const auto& c2 = t2.csr;
+    CHECK(sgtk_graph_import_panels(c2.node_pointer.data(), c2.edge_list.data(), c2.values.data(),
+                                   c2.num_nodes, c2.num_edges(), 16, 8, t2.edge_to_column.data(),
+                                   t2.window_offsets.data(), t2.window_unique_cols.data(),
+                                   (p + ".sgp").c_str(), nullptr, &h) == SGTK_OK);
+    sgtk_graph_panels_loaded(h, &loaded);
+    CHECK(loaded == 0);
+    sgtk_graph_destroy(h);
+    std::filesystem::remove(p);
+    std::filesystem::remove(p + ".sgp");
   }
 
   // --- kernels (test_tile_exec.cpp) -----------------------------------------

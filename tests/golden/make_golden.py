@@ -319,7 +319,26 @@ def configs():
     print(f"wrote {OUT_CONFIGS}: {len(G)} arrays, {os.path.getsize(OUT_CONFIGS) / 1e6:.2f} MB")
 
 
+def sgt_fixtures():
+    """SGT1 files written by the reference's own save_sgt (sgt_file.cpp:47-66)
+    for the drop-in's load_sgt / save_sgt byte-compatibility tests: a weighted
+    graph at the default 16x8 geometry and an unweighted one at 3x5 (ragged
+    windows), both from the golden set."""
+    R = RefLib()
+    here = os.path.dirname(os.path.abspath(__file__))
+    G = dict(np.load(OUT))
+    for key, geom in (("rand3", (16, 8)), ("rand0", (3, 5))):
+        n = int(G[f"{key}/n"])
+        g = Csr.of(n, G[f"{key}/node_pointer"], G[f"{key}/edge_list"], G.get(f"{key}/values"))
+        th = R.transform_handle(g, *geom)
+        path = os.path.join(here, f"ref_{key}_{geom[0]}x{geom[1]}.sgt")
+        R.save_sgt(th, path)
+        print(f"wrote {path}: {os.path.getsize(path)} bytes")
+
+
 if __name__ == "__main__":
-    if "--configs" not in sys.argv:
+    if "--configs" not in sys.argv and "--sgt" not in sys.argv:
         main()
-    configs()
+    if "--sgt" not in sys.argv:
+        configs()
+    sgt_fixtures()

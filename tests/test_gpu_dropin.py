@@ -23,7 +23,8 @@ def test_dropin_compiles_against_reference_api():
 @pytest.mark.gpu
 def test_dropin_cpp_suite():
     exe = build()
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([exe, os.path.join(ROOT, "tests", "golden")], capture_output=True,
+                       text=True, timeout=600)
     print(r.stdout[-3000:])
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "checks passed" in r.stdout

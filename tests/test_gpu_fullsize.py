@@ -85,3 +85,42 @@ def test_spmm_c3_sampled_rows(prec):
     else:  # componentwise TF32 bound, both operands rounded
         lim = 2.0 ** -10 * bound + 1e-6 * np.abs(ref).max()
         assert np.all(np.abs(got - ref) <= lim), "SpMM C3 tf32 outside the componentwise bound"
+
+
+def test_gcn_c5_sampled_rows():
+    """C5 (BASELINE.json configs[4]): the 10M-node / 1B-edge power-law graph
+    on one B200 — GPU translator + panel formats at 1B edges (u32 panel
+    offsets, 32-bit CUB sort offsets) and the d = 128 SpMM (two 64-feature
+    slices), checked on sampled rows against float64 (SURVEY §8d prescribes
+    sampled windows at C5).  FP32 <= 1e-5; TF32 within the componentwise bound."""
+    import paper_2412_12218_b200 as sg
+    from paper_2412_12218_b200.device import DeviceGraph, gcn_normalize_values
+
+    g = _graph("powerlaw-gcn")
+    n = g.num_nodes
+    assert g.num_edges > 900_000_000
+    np_d = torch.from_numpy(g.node_pointer.view(np.int64)).cuda()
+    el_d = torch.from_numpy(g.edge_list.view(np.int32)).cuda()
+    vals = gcn_normalize_values(np_d, el_d)
+    dg = DeviceGraph.from_csr(np_d, el_d, vals, n)
+    del np_d, el_d
+    x = torch.from_numpy(sg.dense_random(n, 128, 13)).cuda()
+    rows = _sample(n, 64, 5)
+    npz = g.node_pointer.astype(np.int64)
+    vh = vals.cpu().numpy()
+    xd = x.cpu().numpy().astype(np.float64)
+    ref = np.empty((len(rows), 128))
+    bound = np.empty((len(rows), 128))
+    for t, i in enumerate(rows):
+        nb = g.edge_list[npz[i]:npz[i + 1]].astype(np.int64)
+        a = vh[npz[i]:npz[i + 1]].astype(np.float64)
+        ref[t] = a @ xd[nb]
+        bound[t] = np.abs(a) @ np.abs(xd[nb])
+    for prec in ("fp32", "tf32"):
+        got = dg.spmm(x, precision=prec)[torch.from_numpy(rows).cuda()].cpu().numpy()
+        if prec == "fp32":
+            err = np.abs(got - ref).max() / np.abs(ref).max()
+            assert err <= 1e-5, f"SpMM C5 fp32 sampled max_rel_err {err:.2e}"
+        else:
+            lim = 2.0 ** -10 * bound + 1e-6 * np.abs(ref).max()
+            assert np.all(np.abs(got - ref) <= lim), "SpMM C5 tf32 outside the componentwise bound"

@@ -236,7 +236,9 @@ def test_sddmm_vs_reference(key, ratio):
     x, y = G[f"{key}/x"], G[f"{key}/y"]
     plan = sg.make_split_plan(t16, ratio)
     assert mre(sg.sddmm_hybrid(t16, x, y, plan), G[f"{key}/sddmm_tf0"]) <= TOL_FP32
-    assert mre(sg.sddmm_hybrid(t16, x, y, plan, precision="tf32"), G[f"{key}/sddmm_tf1"]) <= 1e-4
+    # TF32: the reference rounds each dot to TF32 (tile_exec.cpp:386,402); an
+    # fp32 sum in another order can land one TF32 step (<= 2^-10 relative) away
+    assert mre(sg.sddmm_hybrid(t16, x, y, plan, precision="tf32"), G[f"{key}/sddmm_tf1"]) <= 2.0 ** -10
 
 
 def test_sddmm_kats():
