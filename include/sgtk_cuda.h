@@ -52,11 +52,12 @@ typedef enum sgtk_status {
   SGTK_ERR_NCCL = 12       /* NCCL failure -> sgtk::Error                 */
 } sgtk_status;
 
-/* tile_exec.hpp:12-15 Precision; BF16 is an additive value. */
+/* tile_exec.hpp:12-15 Precision: exactly the reference's two modes.  (A BF16
+ * mode is not offered: the reference has none to be a drop-in for, and
+ * rejecting an advertised value on every call would only be a trap.) */
 typedef enum sgtk_precision {
-  SGTK_FP32 = 0, /* fp32-accurate: 4-term TF32 split MMA, fp32 accumulate */
-  SGTK_TF32 = 1, /* operands RNE-rounded to TF32 (tile_exec.cpp:131-142)  */
-  SGTK_BF16 = 2  /* operands rounded to BF16, fp32 accumulate (additive)  */
+  SGTK_FP32 = 0, /* fp32-accurate: split-TF32 MMA, fp32 accumulate        */
+  SGTK_TF32 = 1  /* operands RNE-rounded to TF32 (tile_exec.cpp:131-142)  */
 } sgtk_precision;
 
 /* Thread-local message of the last failing call on this thread. */

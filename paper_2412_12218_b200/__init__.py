@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import (BF16, FP32, TF32, CudaError, DegreeError, GeometryError, GraphIoError,
+from ._lib import (FP32, TF32, CudaError, DegreeError, GeometryError, GraphIoError,
                    GraphParseError, NodeIdOverflowError, NonFiniteError, RangeError, SgtkError,
                    ShapeError, TileIndexError, check, exported_symbols, lib)
 
@@ -356,7 +356,7 @@ def synth_graph(num_nodes: int, avg_picks: float, alpha: float = 0.0, p_local: f
 from .device import DeviceGraph  # noqa: E402  (re-export)
 
 __all__ = [
-    "BF16", "FP32", "TF32", "BlockStats", "CsrGraph", "CudaError", "DegreeError", "DeviceGraph",
+    "FP32", "TF32", "BlockStats", "CsrGraph", "CudaError", "DegreeError", "DeviceGraph",
     "GeometryError", "GraphIoError", "GraphParseError", "HybridSplitPlan", "NodeIdOverflowError",
     "NonFiniteError", "RangeError", "SgtkError", "ShapeError", "TileGeometry", "TileIndexError",
     "TransformedGraph", "agnn_forward", "block_stats", "csr_from_coo", "dense_random",

@@ -67,8 +67,8 @@ _BY_CODE = {c.code: c for c in (SgtkError, GraphIoError, GraphParseError, NodeId
                                 DegreeError, GeometryError, TileIndexError, RangeError,
                                 ShapeError, NonFiniteError, CudaError)}
 
-FP32, TF32, BF16 = 0, 1, 2
-PRECISIONS = {"fp32": FP32, "tf32": TF32, "bf16": BF16}
+FP32, TF32 = 0, 1  # Precision (tile_exec.hpp:12-15)
+PRECISIONS = {"fp32": FP32, "tf32": TF32}
 
 _lib = None
 

@@ -33,6 +33,7 @@
 #include <cstdlib>
 #include <vector>
 #include <mutex>
+#include <string>
 
 #include "kernels.cuh"
 #include "tc05.cuh"
@@ -847,29 +848,6 @@ inline unsigned final_grid(uint64_t items) {  // 4 rows per warp instruction
 }
 inline unsigned blocks_for(uint64_t n, unsigned bs = 256) {
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + bs - 1) / bs, 148ull * 16)));
-}
-
-// The CUDA-core half of a layer runs on an auxiliary stream.  One stream and
-// its two events per (host thread, device): concurrent callers never share an
-// event (no record/wait interleaving across threads) and every device gets
-// its own stream.  Created on first use, kept for the thread's lifetime.
-struct AuxStreams {
-  cudaStream_t aux = nullptr;
-  cudaEvent_t ready = nullptr, join = nullptr;
-};
-
-const AuxStreams& aux_streams() {
-  thread_local std::vector<std::pair<int, AuxStreams>> per_dev;
-  int dev = 0;
-  CU(cudaGetDevice(&dev));
-  for (auto& e : per_dev)
-    if (e.first == dev) return e.second;
-  AuxStreams a;
-  CU(cudaStreamCreateWithFlags(&a.aux, cudaStreamNonBlocking));
-  CU(cudaEventCreateWithFlags(&a.ready, cudaEventDisableTiming));
-  CU(cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming));
-  per_dev.emplace_back(dev, a);
-  return per_dev.back().second;
 }
 
 template <int DC, int PREC>

@@ -10,6 +10,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "sgtk_cuda.h"
 
@@ -48,6 +49,30 @@ inline void once_per_device(const void* key, const std::function<void()>& fn) {
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
   if (done.insert({dev, key}).second) fn();
+}
+
+// The CUDA-core halves of the panel kernels (AGNN rows, SDDMM sparse edges)
+// run on an auxiliary stream, concurrently with the tensor-core half.  One stream and
+// its two events per (host thread, device): concurrent callers never share an
+// event (no record/wait interleaving across threads) and every device gets
+// its own stream.  Created on first use, kept for the thread's lifetime.
+struct AuxStreams {
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ready = nullptr, join = nullptr;
+};
+
+inline const AuxStreams& aux_streams() {
+  thread_local std::vector<std::pair<int, AuxStreams>> per_dev;
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  for (auto& e : per_dev)
+    if (e.first == dev) return e.second;
+  AuxStreams a;
+  CU(cudaStreamCreateWithFlags(&a.aux, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&a.ready, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming));
+  per_dev.emplace_back(dev, a);
+  return per_dev.back().second;
 }
 
 constexpr uint32_t kNoSlot = 0xFFFFFFFFu;

@@ -65,6 +65,7 @@ struct Panels {
   std::shared_ptr<DevBuf> dval;   // f32[n_dent]  full fp32 value
   std::shared_ptr<DevBuf> deid;   // u32[n_dent]  CSR edge id (0xFFFFFFFF for padding)
   std::shared_ptr<DevBuf> dmask;  // u32[n_chunks * 128] row r's edge bits in the chunk (AGNN)
+  std::shared_ptr<DevBuf> rowoff; // u16[n_chunks * 128] entries of the chunk before row r (SDDMM)
   std::shared_ptr<DevBuf> sptr;   // u32[n_rows+1] sparse edges of a row
   std::shared_ptr<DevBuf> sent;   // uint2[n_sparse] (column, value bits)
   std::shared_ptr<DevBuf> seid;   // u32[n_sparse] CSR edge id

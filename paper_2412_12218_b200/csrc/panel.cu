@@ -1005,7 +1005,9 @@ std::shared_ptr<Panels> build_panel_format(sgtk_graph& g, uint32_t dense_min, cu
                                                       grank.as<uint32_t>(), pn->cptr->as<uint32_t>(),
                                                       E, pn->dmask->as<uint32_t>());
   CU_LAUNCH("edge_mask_kernel");
-  DevBuf ccnt(std::max<uint64_t>(NC, 1) * 4), rowoff(std::max<uint64_t>(NC, 1) * kPanelRows * 2);
+  DevBuf ccnt(std::max<uint64_t>(NC, 1) * 4);
+  pn->rowoff = std::make_shared<DevBuf>(std::max<uint64_t>(NC, 1) * kPanelRows * 2);
+  DevBuf& rowoff = *pn->rowoff;
   if (NC)
     row_offsets_kernel<<<grid_for(NC * 32, 256), 256, 0, s>>>(pn->dmask->as<uint32_t>(), NC,
                                                               rowoff.as<uint16_t>(), ccnt.as<uint32_t>());
@@ -1102,7 +1104,7 @@ std::shared_ptr<Panels> build_panel_format(sgtk_graph& g, uint32_t dense_min, cu
 // into the new handle and skips build_panels.
 namespace {
 constexpr char kSgpMagic[4] = {'S', 'G', 'P', '1'};
-constexpr uint32_t kSgpVersion = 1;
+constexpr uint32_t kSgpVersion = 2;  // 2: + per-chunk row offsets
 
 uint64_t fnv(uint64_t h, const void* p, size_t n) {
   const auto* b = static_cast<const unsigned char*>(p);
@@ -1163,7 +1165,8 @@ void put_format(std::FILE* f, const Panels& pn, uint32_t dense_min, cudaStream_t
                           pn.n_items, pn.n_long, pn.n_segs, pn.n_aitems};
   for (uint64_t v : sc) put(f, v);
   for (const auto* b : {&pn.cptr, &pn.dcols, &pn.coff, &pn.dent, &pn.dval, &pn.deid, &pn.dmask,
-                        &pn.sptr, &pn.sent, &pn.seid, &pn.items, &pn.lrows, &pn.aitems})
+                        &pn.rowoff, &pn.sptr, &pn.sent, &pn.seid, &pn.items, &pn.lrows,
+                        &pn.aitems})
     put_buf(f, *b, s);
 }
 
@@ -1182,7 +1185,8 @@ std::shared_ptr<Panels> get_format(std::FILE* f, uint32_t want_min, cudaStream_t
   pn->n_segs = sc[7];
   pn->n_aitems = sc[8];
   for (auto* b : {&pn->cptr, &pn->dcols, &pn->coff, &pn->dent, &pn->dval, &pn->deid, &pn->dmask,
-                  &pn->sptr, &pn->sent, &pn->seid, &pn->items, &pn->lrows, &pn->aitems})
+                  &pn->rowoff, &pn->sptr, &pn->sent, &pn->seid, &pn->items, &pn->lrows,
+                  &pn->aitems})
     *b = get_buf(f, s);
   return pn;
 }

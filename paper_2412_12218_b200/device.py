@@ -38,7 +38,7 @@ def _prec(p) -> int:
         return PRECISIONS[p]
     except KeyError:
         from ._lib import RangeError
-        raise RangeError("precision must be 'fp32', 'tf32' or 'bf16'") from None
+        raise RangeError("precision must be 'fp32' or 'tf32'") from None
 
 
 def _f32_2d(x: torch.Tensor, name: str) -> torch.Tensor:

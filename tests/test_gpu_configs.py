@@ -9,9 +9,10 @@ C2: Pubmed-shaped in-proj 500->32 (+ReLU) -> 4 x agnn_forward -> out-proj 32->3,
     in the library's auto mode (what the bench runs) and in every AGNN mode.
 
 Bars: graph preprocessing bit-exact; FP32 max_rel_err <= 1e-5 (the reference
-tests allow 1e-4); TF32 as in test_gpu_parity.py (GCN: 2e-3 vs the reference's
-TF32 mode — the default order A(hW) rounds a different operand set than the
-reference's (Ah)W; AGNN: 2e-3, error model in test_agnn_tf32_componentwise).
+tests allow 1e-4); TF32 vs the reference's TF32 mode by the error models of
+tests/_bars.py (GCN: the default order A(hW) rounds another operand set than
+the reference's (Ah)W; AGNN: (1 + |beta|) 2^-10; the projections: one TF32
+step for the weights the reference leaves unrounded).
 """
 import os
 
@@ -22,6 +23,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_2412_12218_b200 as sg  # noqa: E402
+from tests._bars import TF32_STEP, agnn_tf32_bar, gcn_tf32_bar  # noqa: E402
 from paper_2412_12218_b200.device import DeviceGraph, gemm  # noqa: E402
 
 PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "configs.npz")
@@ -53,7 +55,8 @@ def test_c1_cora_gcn(order):
     x = sg.dense_random(n, 1433, INPUT_SEED)
     layers = sg.random_gcn_layers(1433, 16, 7, 2, LAYER_SEED)
     assert mre(sg.gcn_forward(t, x, layers, order=order), G["c1/gcn_tf0"]) <= 1e-5
-    assert mre(sg.gcn_forward(t, x, layers, precision="tf32", order=order), G["c1/gcn_tf1"]) <= 2e-3
+    assert mre(sg.gcn_forward(t, x, layers, precision="tf32", order=order),
+               G["c1/gcn_tf1"]) <= gcn_tf32_bar()
 
 
 def c2_forward(prec, mode):
@@ -78,6 +81,6 @@ def test_c2_pubmed_agnn(mode):
     h0, h4, out, zeros = c2_forward("tf32", mode)
     # the reference's in-proj rounds X only (tf32 SpMM over identity, then a
     # plain fp32 matmul); ours rounds X and W: componentwise 2^-10 |X||W|
-    assert mre(h0[rows], G["c2/h0_tf1_rows"]) <= 2e-3
-    assert mre(h4[rows], G["c2/h4_tf1_rows"]) <= 2e-3
-    assert mre(out, G["c2/out_tf1"]) <= 2e-3
+    assert mre(h0[rows], G["c2/h0_tf1_rows"]) <= TF32_STEP
+    assert mre(h4[rows], G["c2/h4_tf1_rows"]) <= TF32_STEP + agnn_tf32_bar([1.0])
+    assert mre(out, G["c2/out_tf1"]) <= 2 * TF32_STEP + agnn_tf32_bar([1.0])

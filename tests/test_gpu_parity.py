@@ -22,6 +22,7 @@ pytestmark = pytest.mark.gpu
 import paper_2412_12218_b200 as sg  # noqa: E402
 from paper_2412_12218_b200.device import DeviceGraph, gemm, l2_normalize_rows  # noqa: E402
 from oracle.oracle import Csr, Oracle  # noqa: E402
+from tests._bars import agnn_tf32_bar, gcn_tf32_bar  # noqa: E402
 from tests._golden import csr, golden, random_keys, transform  # noqa: E402
 
 O = Oracle()
@@ -280,7 +281,7 @@ def test_gcn_vs_reference(key, order):
     x = G[f"{key}/x"]
     assert mre(sg.gcn_forward(t, x, layers, order=order), G[f"{key}_gcn/gcn_tf0"]) <= TOL_FP32
     assert mre(sg.gcn_forward(t, x, layers, precision="tf32", order=order),
-               G[f"{key}_gcn/gcn_tf1"]) <= 2e-3
+               G[f"{key}_gcn/gcn_tf1"]) <= gcn_tf32_bar()
 
 
 def test_gcn_identity_and_zero():
@@ -305,7 +306,8 @@ def test_agnn_vs_reference(key):
     x = G[f"{key}/x"]
     betas = G[f"{key}_agnn/betas"]
     assert mre(sg.agnn_forward(t, x, betas), G[f"{key}_agnn/agnn_tf0"]) <= TOL_FP32
-    assert mre(sg.agnn_forward(t, x, betas, precision="tf32"), G[f"{key}_agnn/agnn_tf1"]) <= 2e-3
+    bar = agnn_tf32_bar(betas)  # error model: tests/_bars.py
+    assert mre(sg.agnn_forward(t, x, betas, precision="tf32"), G[f"{key}_agnn/agnn_tf1"]) <= bar
     assert mre(sg.agnn_forward(t, x, betas, plan=sg.make_split_plan(t, 0.0)),
                G[f"{key}_agnn/agnn_tf0"]) <= TOL_FP32
     # fused single-pass mode (online softmax; attention never materialised)
@@ -314,11 +316,11 @@ def test_agnn_vs_reference(key):
         assert mre(sg.agnn_forward(t, x, betas, plan=plan, mode=1),
                    G[f"{key}_agnn/agnn_tf0"]) <= TOL_FP32
     assert mre(sg.agnn_forward(t, x, betas, precision="tf32", mode=1),
-               G[f"{key}_agnn/agnn_tf1"]) <= 2e-3
+               G[f"{key}_agnn/agnn_tf1"]) <= bar
     # panel mode (agnn_panel.cu)
     assert mre(sg.agnn_forward(t, x, betas, mode=2), G[f"{key}_agnn/agnn_tf0"]) <= TOL_FP32
     assert mre(sg.agnn_forward(t, x, betas, precision="tf32", mode=2),
-               G[f"{key}_agnn/agnn_tf1"]) <= 2e-3
+               G[f"{key}_agnn/agnn_tf1"]) <= bar
 
 
 @pytest.mark.parametrize("name,g", big_graphs())
