@@ -340,15 +340,24 @@ int device_sm_major() {
 
 }  // namespace
 
-// Returns false (caller uses the mma.sync kernel) when the shape/alignment is
-// outside this kernel's envelope: n > 128, lda % 4 != 0, unaligned base.
+// Returns false (caller uses the mma.sync kernel) when the shape is outside
+// this kernel's envelope (n > 128).  Rows whose pitch or base the TMA cannot
+// address (16-byte multiples; e.g. Cora's K = 1433) are first copied into a
+// stream-ordered scratch with a padded pitch (one extra pass over A).
 bool gemm_tc05_launch(const float* a, uint64_t lda, const float* w, uint64_t m, uint64_t k,
                       uint64_t n, int relu, int prec, float* out, uint64_t ldo, cudaStream_t s,
                       bool round_tf32, uint32_t* nonfinite) {
   if (getenv("SGTK_DISABLE_TC05")) return false;
   if (n == 0 || n > 128 || m == 0 || k == 0) return false;
-  if (lda % 4 != 0 || reinterpret_cast<uintptr_t>(a) % 16 != 0) return false;
   if (device_sm_major() != 10) return false;
+  float* staged = nullptr;
+  if (lda % 4 != 0 || reinterpret_cast<uintptr_t>(a) % 16 != 0) {
+    const uint64_t lds = (k + 3) / 4 * 4;
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&staged), m * lds * 4, s));
+    CU(cudaMemcpy2DAsync(staged, lds * 4, a, lda * 4, k * 4, m, cudaMemcpyDeviceToDevice, s));
+    a = staged;
+    lda = lds;
+  }
   const uint32_t n_pad = uint32_t((n + 15) / 16 * 16);
   const uint32_t k_pad = uint32_t((k + kBK - 1) / kBK * kBK);
   const int P_A = prec == SGTK_FP32 ? 3 : 1, P_W = prec == SGTK_FP32 ? 2 : 1;
@@ -363,6 +372,7 @@ bool gemm_tc05_launch(const float* a, uint64_t lda, const float* w, uint64_t m, 
             make_map(&mw, wt, k_pad, uint64_t(P_W) * n_pad, uint64_t(k_pad) * 4, kBK, n_pad);
   if (!ok) {
     CU(cudaFreeAsync(wt, s));
+    if (staged) CU(cudaFreeAsync(staged, s));
     return false;
   }
   const uint32_t a_bytes = kBM * kBK * 4, w_bytes = n_pad * kBK * 4;
@@ -402,6 +412,7 @@ bool gemm_tc05_launch(const float* a, uint64_t lda, const float* w, uint64_t m, 
   }
   CU_LAUNCH("gemm_tc05_kernel");
   CU(cudaFreeAsync(wt, s));
+  if (staged) CU(cudaFreeAsync(staged, s));
   return true;
 }
 
