@@ -138,7 +138,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
   uint8_t* ps = smem + C::P_OFF;
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t p = pv.porder ? pv.porder[blockIdx.x] : blockIdx.x;
+  const uint64_t p = blockIdx.x;
   const uint32_t c0 = pv.cptr[p], nch = pv.cptr[p + 1] - c0;
   const uint32_t ngroups = (nch + C::FOLD - 1) / C::FOLD;
   const int dvalid = d < uint64_t(DC) ? int(d) : DC;

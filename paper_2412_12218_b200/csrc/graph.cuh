@@ -59,7 +59,6 @@ struct Panels {
   uint64_t P = 0, n_chunks = 0, n_dent = 0, n_sparse = 0;
   uint32_t max_chunk_entries = 0;
   std::shared_ptr<DevBuf> cptr;   // u32[P+1]   first chunk of panel p
-  std::shared_ptr<DevBuf> porder; // u32[P]     panels by chunk count, largest first (launch order)
   std::shared_ptr<DevBuf> dcols;  // u32[32*n_chunks] dense column ids (pad 0xFFFFFFFF)
   std::shared_ptr<DevBuf> coff;   // u64[n_chunks+1] entry range of a chunk (multiple of 4)
   std::shared_ptr<DevBuf> dent;   // u32[n_dent]  tf32(value) | swizzled A-tile word offset
@@ -85,7 +84,6 @@ struct Panels {
 struct PanelView {
   uint64_t n_rows, P;
   const uint32_t* cptr;
-  const uint32_t* porder;  // CTA i runs panel porder[i] (nullptr: panel i)
   const uint32_t* dcols;
   const uint64_t* coff;
   const uint32_t* dent;

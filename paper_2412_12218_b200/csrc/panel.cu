@@ -411,7 +411,7 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
   uint8_t* dring = smem + L.dring_off;   // [nd] entry slots (+ [nd] value slots, FP32)
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t p = pv.porder ? pv.porder[blockIdx.x] : blockIdx.x;
+  const uint64_t p = blockIdx.x;
   const uint64_t fbase = uint64_t(blockIdx.y) * DC;
   const int dvalid = d - fbase < uint64_t(DC) ? int(d - fbase) : DC;
   const uint32_t c0 = pv.cptr[p], nch = pv.cptr[p + 1] - c0;
@@ -989,15 +989,6 @@ std::shared_ptr<Panels> build_panel_format(sgtk_graph& g, uint32_t dense_min, cu
   const uint64_t NC = cptr[P];
   pn->n_chunks = NC;
   pn->cptr = ul(cptr.data(), P + 1, s);
-  {  // longest-first launch order: the heaviest panels (hub regions) start in
-     // the first wave instead of forming the last one's tail
-    std::vector<uint32_t> order(P);
-    for (uint64_t p = 0; p < P; ++p) order[p] = uint32_t(p);
-    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-      return cptr[a + 1] - cptr[a] > cptr[b + 1] - cptr[b];
-    });
-    pn->porder = ul(order.data(), P, s);
-  }
   pn->dcols = std::make_shared<DevBuf>(std::max<uint64_t>(NC * kChunkCols, 1) * 4);
   CU(cudaMemsetAsync(pn->dcols->p, 0xFF, pn->dcols->bytes, s));
   if (P)
@@ -1113,7 +1104,7 @@ std::shared_ptr<Panels> build_panel_format(sgtk_graph& g, uint32_t dense_min, cu
 // into the new handle and skips build_panels.
 namespace {
 constexpr char kSgpMagic[4] = {'S', 'G', 'P', '1'};
-constexpr uint32_t kSgpVersion = 3;  // 2: + per-chunk row offsets, 3: + launch order
+constexpr uint32_t kSgpVersion = 2;  // 2: + per-chunk row offsets
 
 uint64_t fnv(uint64_t h, const void* p, size_t n) {
   const auto* b = static_cast<const unsigned char*>(p);
@@ -1173,7 +1164,7 @@ void put_format(std::FILE* f, const Panels& pn, uint32_t dense_min, cudaStream_t
   const uint64_t sc[9] = {pn.P, pn.n_chunks, pn.n_dent, pn.n_sparse, pn.max_chunk_entries,
                           pn.n_items, pn.n_long, pn.n_segs, pn.n_aitems};
   for (uint64_t v : sc) put(f, v);
-  for (const auto* b : {&pn.cptr, &pn.porder, &pn.dcols, &pn.coff, &pn.dent, &pn.dval, &pn.deid, &pn.dmask,
+  for (const auto* b : {&pn.cptr, &pn.dcols, &pn.coff, &pn.dent, &pn.dval, &pn.deid, &pn.dmask,
                         &pn.rowoff, &pn.sptr, &pn.sent, &pn.seid, &pn.items, &pn.lrows,
                         &pn.aitems})
     put_buf(f, *b, s);
@@ -1193,7 +1184,7 @@ std::shared_ptr<Panels> get_format(std::FILE* f, uint32_t want_min, cudaStream_t
   pn->n_long = sc[6];
   pn->n_segs = sc[7];
   pn->n_aitems = sc[8];
-  for (auto* b : {&pn->cptr, &pn->porder, &pn->dcols, &pn->coff, &pn->dent, &pn->dval, &pn->deid, &pn->dmask,
+  for (auto* b : {&pn->cptr, &pn->dcols, &pn->coff, &pn->dent, &pn->dval, &pn->deid, &pn->dmask,
                   &pn->rowoff, &pn->sptr, &pn->sent, &pn->seid, &pn->items, &pn->lrows,
                   &pn->aitems})
     *b = get_buf(f, s);
@@ -1268,11 +1259,6 @@ PanelView panel_view(const sgtk_graph* g, uint64_t d) {
   v.n_rows = g->n_rows;
   v.P = pn.P;
   v.cptr = pn.cptr->as<uint32_t>();
-  static const bool natural = [] {
-    const char* e = std::getenv("SGTK_PANEL_ORDER");
-    return e && std::string(e) == "natural";
-  }();
-  v.porder = natural || !pn.porder ? nullptr : pn.porder->as<uint32_t>();
   v.dcols = pn.dcols->as<uint32_t>();
   v.coff = pn.coff->as<uint64_t>();
   v.dent = pn.dent->as<uint32_t>();

@@ -109,7 +109,7 @@ sddmm_dense_kernel(const PanelView pv, const uint32_t* __restrict__ deid,
   const bool has_dval = dval != nullptr;
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t p = pv.porder ? pv.porder[blockIdx.x] : blockIdx.x;
+  const uint64_t p = blockIdx.x;
   const uint32_t c0 = pv.cptr[p], nch = pv.cptr[p + 1] - c0;
 
   if (threadIdx.x == 0) {
