@@ -46,6 +46,12 @@ for tool in ("memcheck", "synccheck", "initcheck", "racecheck"):
             return "cp.async.bulk (TMA engine) write, completion via mbarrier complete_tx, consumer waits the mbarrier"
         if "cp_async16" in names:
             return "cp.async write, completion via cp.async.mbarrier.arrive.noinc, consumer waits the mbarrier"
+        if names & {"sddmm_dense_kernel"}:
+            # checked by hand: sddmm_panel.cu stage-slot writes (stage warps) ->
+            # __syncwarp + arrive(stfull) -> store warps wait(stfull) -> reads;
+            # ecnt written by the loader before its expect_tx arrive on efull
+            return ("generic-proxy hand-off between warp roles through an mbarrier "
+                    "(arrive = release, try_wait.parity = acquire)")
         if "gemm_tc05_kernel" in names:
             return ("operand conversion (prep warps) -> mbarrier -> MMA issue -> tcgen05.commit(tmem_full) "
                     "-> epilogue staging: ordered through the tensor core's commit arrive")
