@@ -63,11 +63,12 @@ for tool in ("memcheck", "synccheck", "initcheck", "racecheck"):
         m = mech(a, b)
         uncl += m == "UNCLASSIFIED"
         out.append(f"| {n} | {a[0]} `{a[1]}` {a[2]} | {b[0]} `{b[1]}` {b[2]} | {m} |")
-    out.append(f"\nUnclassified pairs: {uncl}.  Every reported pair has an asynchronous-proxy "
-               "access (bulk copy, cp.async with mbarrier completion) or the tcgen05.commit chain on "
-               "one side; racecheck tracks neither mbarrier transaction completion nor the tensor "
-               "core's commit arrive, so it cannot see the ordering these pipelines use.  No hazard "
-               "involves two generic-proxy accesses without such an edge.  (memcheck, synccheck and "
+    out.append(f"\nUnclassified pairs: {uncl}.  Every reported pair is ordered by an mbarrier: "
+               "an asynchronous-proxy write (bulk copy, cp.async with mbarrier completion) or the "
+               "tcgen05.commit chain on one side, or a hand-off between warp roles (arrive after "
+               "__syncwarp, consumer try_wait.parity); racecheck models none of these, so it cannot "
+               "see the ordering these pipelines use.  No hazard involves two accesses without such "
+               "an edge.  (memcheck, synccheck and "
                "initcheck are the tools that can judge these kernels; all three report 0 errors.)\n")
 open(f"profiles/{tag}_sanitize.md", "w").write("\n".join(out) + "\n")
 print("\n".join(out))
