@@ -56,6 +56,66 @@ def test_agnn_c4_sampled_rows(prec, bar):
     assert err <= bar, f"AGNN C4 {prec} sampled max_rel_err {err:.2e}"
 
 
+def _tf32(a):
+    """tf32_round_value (tile_exec.cpp:131-142) on a float32 array: RNE to 10
+    mantissa bits (finite inputs)."""
+    u = np.asarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x0FFF + ((u >> 13) & 1)) & 0xFFFFE000
+    return u.astype(np.uint32).view(np.float32)
+
+
+def test_agnn_c4_sampled_rows_vs_reference_tf32_mode():
+    """C4 at full size against the reference's own TF32 arithmetic, emulated
+    in float32 for sampled rows (gnn.cpp:107-116 with Precision::Tf32):
+    z = l2norm(h) (double sum); logit = tf32(sum_k tf32(z_i,k) tf32(z_j,k)),
+    sequential fp32 (tile_exec.cpp:369-390); x beta; softmax in fp32
+    (gnn.cpp:54-72); out = sum_e tf32(a_e) tf32(h_e) in CSR order
+    (tile_exec.cpp:247-248).  Bar: tests/_bars.py agnn_tf32_bar."""
+    import paper_2412_12218_b200 as sg
+    from paper_2412_12218_b200.device import DeviceGraph
+    from tests._bars import agnn_tf32_bar
+
+    g = _graph("reddit-agnn")
+    n = g.num_nodes
+    npz = g.node_pointer.astype(np.int64)
+    el = g.edge_list.astype(np.int64)
+    x = sg.dense_random(n, 32, 11)
+    beta = np.float32(0.8)
+    dg = DeviceGraph.from_csr(g.node_pointer, g.edge_list)
+    out = dg.agnn_forward(torch.from_numpy(x).cuda(), [float(beta)], precision="tf32",
+                          mode=2).cpu().numpy()
+    rows = _sample(n, 48, 3)
+
+    def zrows(idx):
+        h = x[idx]
+        sq = (h.astype(np.float64) ** 2).sum(axis=1)
+        inv = np.where(sq > 0, (1.0 / np.sqrt(np.where(sq > 0, sq, 1.0))).astype(np.float32),
+                       np.float32(0))
+        return (h * inv[:, None]).astype(np.float32)
+
+    ref = np.empty((len(rows), 32), np.float32)
+    for t, i in enumerate(rows):
+        nb = el[npz[i]:npz[i + 1]]
+        zi = _tf32(zrows(np.array([i]))[0])
+        zn = _tf32(zrows(nb))
+        dot = np.zeros(len(nb), np.float32)
+        for k in range(32):
+            dot = (dot + zi[k] * zn[:, k]).astype(np.float32)
+        lg = (_tf32(dot) * beta).astype(np.float32)
+        ex = np.exp((lg - lg.max()).astype(np.float32)).astype(np.float32)
+        tot = np.float32(0)
+        for v in ex:
+            tot = np.float32(tot + v)
+        att = _tf32((ex / tot).astype(np.float32))
+        hv = _tf32(x[nb])
+        acc = np.zeros(32, np.float32)
+        for e in range(len(nb)):
+            acc = (acc + att[e] * hv[e]).astype(np.float32)
+        ref[t] = acc
+    err = np.abs(out[rows] - ref).max() / np.abs(ref).max()
+    assert err <= agnn_tf32_bar([beta]), f"AGNN C4 vs reference TF32 mode: {err:.2e}"
+
+
 @pytest.mark.parametrize("prec", ["fp32", "tf32"])
 def test_spmm_c3_sampled_rows(prec):
     import paper_2412_12218_b200 as sg
