@@ -616,9 +616,12 @@ def run_b200(args, wl):
         layers = [(torch.from_numpy(w).to(dev), r) for w, r in
                   sg.random_gcn_layers(wl["d_in"], wl["hidden"], wl["d_out"], L, LAYER_SEED)]
         reps = {}
+        # asynchronous form (no per-call host sync: CUDA-graph capturable); the
+        # non-finite flag is checked after the timing
+        nf = torch.zeros(1, dtype=torch.int32, device=dev)
 
         def step():
-            return sl.gcn_forward(x_loc, layers, precision=prec, reps=reps)
+            return sl.gcn_forward(x_loc, layers, precision=prec, reps=reps, nonfinite=nf)
 
         launches_per_step = L * 3 + (L if dg_has_splits(dg, 8) else 0)
         if world > 1:
@@ -657,7 +660,7 @@ def run_b200(args, wl):
 
     warm = max(3, args.warmup)
     graph_note = None
-    if args.cuda_graph and world == 1 and wl["kind"] == "agnn":
+    if args.cuda_graph and world == 1:
         # launch-bound configs (C1/C2: microsecond kernels): capture the whole
         # step once, replay it per step -- every kernel of the call still runs
         for _ in range(3):
@@ -665,12 +668,12 @@ def run_b200(args, wl):
         torch.cuda.synchronize()
         cg = torch.cuda.CUDAGraph()
         with torch.cuda.graph(cg):
-            step()
+            g_out = step()  # the captured call's output (graph memory: stable across replays)
         eager_step = step
 
         def step():  # noqa: F811
             cg.replay()
-            return out_buf if wl["kind"] == "agnn" else None
+            return g_out
 
         graph_note = "step captured once as a CUDA graph (torch.cuda.CUDAGraph) and replayed"
         stream = torch.cuda.current_stream()
@@ -681,6 +684,8 @@ def run_b200(args, wl):
     clocks = summarize_clocks(rows)
     value = step_ms / L
 
+    if wl["kind"] == "gcn" and int(nf.item()):
+        raise SystemExit("gcn_forward produced NaN/Inf during the timed steps")
     if graph_note:
         # the replayed graph computes exactly what the eager call does
         replayed = step().clone()
@@ -770,7 +775,25 @@ def run_b200(args, wl):
             cpu = {"value": None, "unavailable": str(e)}
 
     pk, pk_src = peaks()
-    if roof:
+    if world > 1:
+        # whole job: the layer's algorithmic bytes over the whole graph (SURVEY
+        # §8d; AGNN: the fused lower bound, GCN: B_spmm + B_gemm) per layer time,
+        # against N GPUs' worth of HBM; the exchange is not counted as useful bytes
+        s_ = 4
+        if wl["kind"] == "agnn":
+            B = 8 * (N + 1) + 4 * E + 4 * N + 2 * s_ * N * d
+            formula = "8(N+1) + 4E + 4N + 2*s*N*d per layer (fused AGNN lower bound), whole graph"
+        else:
+            B = (8 * (N + 1) + 8 * E + 2 * s_ * N * d) + (s_ * N * d + 4 * d * d + 4 * N * d)
+            formula = "B_spmm + B_gemm per layer (d -> d), whole graph"
+        roof = {"bound": "hbm", "kernel": f"whole layer on {world} GPUs (step / layers)",
+                "achieved": round(B / (value * 1e-3) / 1e9, 1), "unit": "GB/s",
+                "algorithmic_bytes": int(B), "formula": formula, "kernel_ms": round(value, 4),
+                "traffic": None}
+        roof["peak"] = pk["hbm_gbs"] * world
+        roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+        roof["peak_source"] = f"MEASURED_PEAKS.json hbm_gbs x {world} GPUs ({pk_src})"
+    elif roof:
         roof["traffic"] = profiled_traffic(roof["kernel"], gcn=wl["kind"] == "gcn")
         roof["peak"] = pk["hbm_gbs"]
         roof["frac"] = round(roof["achieved"] / pk["hbm_gbs"], 4)

@@ -262,6 +262,15 @@ int sgtk_gcn_forward(const sgtk_graph* g, const float* x_dev, uint64_t ldx,
                      const uint32_t* cut_dev, int precision, int order,
                      void* ws_dev, uint64_t ws_bytes, float* out_dev,
                      uint64_t ldo, void* stream);
+/* The same, asynchronous: no synchronisation, no SGTK_ERR_NONFINITE; a NaN/Inf
+ * output sets *nonfinite_dev (u32, device, zeroed by the caller) to 1 instead
+ * (capturable in a CUDA graph). */
+int sgtk_gcn_forward_async(const sgtk_graph* g, const float* x_dev, uint64_t ldx,
+                           uint32_t num_layers, const uint64_t* dims_host,
+                           const float* weights_dev, const int* relu_host,
+                           const uint32_t* cut_dev, int precision, int order,
+                           void* ws_dev, uint64_t ws_bytes, float* out_dev,
+                           uint64_t ldo, uint32_t* nonfinite_dev, void* stream);
 uint64_t sgtk_gcn_workspace(const sgtk_graph* g, uint32_t num_layers,
                             const uint64_t* dims_host);
 

@@ -103,6 +103,8 @@ _SIGS = {
     "sgtk_l2_normalize_rows": [vp, u64, u64, u64, vp, u64, vp, vp, vp],
     "sgtk_gemm": [vp, u64, vp, u64, u64, u64, C.c_int, C.c_int, vp, u64, vp],
     "sgtk_gcn_forward": [vp, vp, u64, u32, vp, vp, vp, vp, C.c_int, C.c_int, vp, u64, vp, u64, vp],
+    "sgtk_gcn_forward_async": [vp, vp, u64, u32, vp, vp, vp, vp, C.c_int, C.c_int, vp, u64, vp,
+                               u64, vp, vp],
     "sgtk_agnn_forward": [vp, vp, u64, u64, u32, vp, vp, C.c_int, C.c_int, vp, u64, vp, u64, vp,
                           vp],
     "sgtk_gcn_normalize_values": [vp, vp, u64, vp, vp],

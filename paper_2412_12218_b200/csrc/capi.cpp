@@ -20,7 +20,7 @@ uint64_t gcn_workspace(const sgtk_graph* g, uint32_t L, const uint64_t* dims);
 void gcn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint32_t L,
                  const uint64_t* dims, const float* weights, const int* relu,
                  const uint32_t* cut, int prec, int order, void* ws, uint64_t ws_bytes, float* out,
-                 uint64_t ldo, cudaStream_t s);
+                 uint64_t ldo, cudaStream_t s, uint32_t* nonfinite_dev = nullptr);
 uint64_t agnn_workspace(const sgtk_graph* g, uint64_t d);
 void agnn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint64_t d, uint32_t L,
                   const float* betas, const uint32_t* cut, int prec, int mode, void* ws,
@@ -371,7 +371,20 @@ int sgtk_gcn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint32_t
     check_graph(g);
     check_prec(prec);
     gcn_forward(g, x, ldx, L, dims, weights, relu, cut, prec, order, ws, ws_bytes, out, ldo,
-                as_stream(stream));
+                as_stream(stream), nullptr);
+  });
+}
+
+int sgtk_gcn_forward_async(const sgtk_graph* g, const float* x, uint64_t ldx, uint32_t L,
+                           const uint64_t* dims, const float* weights, const int* relu,
+                           const uint32_t* cut, int prec, int order, void* ws, uint64_t ws_bytes,
+                           float* out, uint64_t ldo, uint32_t* nonfinite, void* stream) {
+  return guard([&] {
+    check_graph(g);
+    check_prec(prec);
+    need(nonfinite != nullptr, SGTK_ERR, "null nonfinite flag");
+    gcn_forward(g, x, ldx, L, dims, weights, relu, cut, prec, order, ws, ws_bytes, out, ldo,
+                as_stream(stream), nonfinite);
   });
 }
 

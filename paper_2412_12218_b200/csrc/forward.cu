@@ -71,7 +71,7 @@ uint64_t gcn_workspace(const sgtk_graph* g, uint32_t L, const uint64_t* dims) {
 void gcn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint32_t L,
                  const uint64_t* dims, const float* weights, const int* relu,
                  const uint32_t* cut, int prec, int order, void* ws, uint64_t ws_bytes, float* out,
-                 uint64_t ldo, cudaStream_t s) {
+                 uint64_t ldo, cudaStream_t s, uint32_t* nonfinite_dev) {
   const uint64_t N = g->n_rows;
   if (L == 0) raise(SGTK_ERR_SHAPE, "gcn_forward: no layers");
   if (ws_bytes < gcn_workspace(g, L, dims)) raise(SGTK_ERR_SHAPE, "gcn_forward: workspace too small");
@@ -81,8 +81,10 @@ void gcn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint32_t L,
   const uint64_t slab = align256(N * mx * 4);
   float* buf[2] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + slab)};
   float* tmp = reinterpret_cast<float*>(base + 2 * slab);
-  uint32_t* flag = reinterpret_cast<uint32_t*>(base + 3 * slab);
-  CU(cudaMemsetAsync(flag, 0, 4, s));
+  // the check goes to the caller's flag (asynchronous entry) or to a
+  // workspace word read back below (the synchronous, raising one)
+  uint32_t* flag = nonfinite_dev ? nonfinite_dev : reinterpret_cast<uint32_t*>(base + 3 * slab);
+  if (!nonfinite_dev) CU(cudaMemsetAsync(flag, 0, 4, s));
 
   const float* h = x;
   uint64_t ldh = ldx;
@@ -115,6 +117,7 @@ void gcn_forward(const sgtk_graph* g, const float* x, uint64_t ldx, uint32_t L,
     h = dst;
     ldh = ldd;
   }
+  if (nonfinite_dev) return;
   uint32_t hf = 0;
   CU(cudaMemcpyAsync(&hf, flag, 4, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));

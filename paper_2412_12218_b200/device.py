@@ -259,8 +259,11 @@ class DeviceGraph:
         check(lib().sgtk_edge_softmax(self._h, _ptr(logits), _ptr(out), _stream()))
         return out
 
-    def gcn_forward(self, x, layers, cut=None, precision="fp32", order=2) -> torch.Tensor:
-        """layers: list of (W [d_in x d_out] CUDA f32, relu)."""
+    def gcn_forward(self, x, layers, cut=None, precision="fp32", order=2,
+                    nonfinite: torch.Tensor | None = None) -> torch.Tensor:
+        """layers: list of (W [d_in x d_out] CUDA f32, relu).  With `nonfinite`
+        (a zeroed int32 CUDA tensor) the call is asynchronous (CUDA-graph
+        capturable) and a NaN/Inf output sets it instead of raising."""
         _f32_2d(x, "x")
         if x.shape[0] != self.info.num_nodes:
             raise ShapeError("gcn_forward: x.rows != num_nodes")
@@ -276,6 +279,12 @@ class DeviceGraph:
         ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=x.device)
         out = torch.empty((self.info.num_nodes, dims[-1]), dtype=torch.float32, device=x.device)
         cut = self._cut(cut)
+        if nonfinite is not None:
+            check(lib().sgtk_gcn_forward_async(
+                self._h, _ptr(x), u64(x.stride(0)), len(layers), dims_a.ctypes.data, _ptr(wcat),
+                relu.ctypes.data, _ptr(cut), _prec(precision), order, _ptr(ws), u64(ws_bytes),
+                _ptr(out), u64(out.stride(0)), _ptr(nonfinite), _stream()))
+            return out
         check(lib().sgtk_gcn_forward(self._h, _ptr(x), u64(x.stride(0)), len(layers),
                                      dims_a.ctypes.data, _ptr(wcat), relu.ctypes.data, _ptr(cut),
                                      _prec(precision), order, _ptr(ws), u64(ws_bytes), _ptr(out),

@@ -40,6 +40,7 @@ from ._lib import check, lib
 
 
 ROW_QUANTUM = 128  # panel height: slices made of whole panels keep every output bit
+_INPLACE_OK = True  # NCCL's in-place all-gather (send buffer inside the receive buffer)
 
 
 def partition(node_pointer: np.ndarray, num_nodes: int, parts: int,
@@ -112,7 +113,18 @@ def exchange_inplace(buf: torch.Tensor, rank: int, world: int, group=None) -> No
     stride = buf.shape[0] // world
     mine = buf[rank * stride:(rank + 1) * stride]
     if buf.is_cuda and dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(buf, mine, group=group)
+        global _INPLACE_OK
+        if _INPLACE_OK:
+            try:
+                dist.all_gather_into_tensor(buf, mine, group=group)
+                return
+            except (RuntimeError, ValueError) as e:  # a torch build refusing aliased buffers
+                _INPLACE_OK = False
+                import warnings
+
+                warnings.warn(f"in-place all_gather_into_tensor refused ({e}); "
+                              "exchanging through a send copy")
+        dist.all_gather_into_tensor(buf, mine.clone(), group=group)
         return
     host = buf.cpu() if buf.is_cuda else buf
     blocks = list(host.view(world, stride, *buf.shape[1:]).unbind(0))
@@ -205,7 +217,7 @@ class RowSlice:
         return self.mine(h_rep).clone() if out is None else out.copy_(self.mine(h_rep))
 
     def gcn_forward(self, x_local: torch.Tensor, layers, precision="tf32",
-                    reps: dict | None = None) -> torch.Tensor:
+                    reps: dict | None = None, nonfinite=None) -> torch.Tensor:
         """Per layer, the same operand order as single-GPU gcn_forward(order=2):
         d_out < d_in: local h W (into the replica), all-gather, SpMM, ReLU;
         otherwise   : h into the replica, all-gather, SpMM, local GEMM + ReLU.
@@ -214,7 +226,8 @@ class RowSlice:
         from .device import gemm, relu_
 
         if self.world == 1:
-            return self.graph.gcn_forward(x_local, layers, precision=precision, order=2)
+            return self.graph.gcn_forward(x_local, layers, precision=precision, order=2,
+                                          nonfinite=nonfinite)
         reps = {} if reps is None else reps
 
         def rep(d):
