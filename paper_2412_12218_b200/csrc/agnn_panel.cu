@@ -27,6 +27,9 @@
 //   logits of the row's sparse edges (lane = edge dot products), exp, l and O
 //   updates (lane = feature), out = O / l, then the next layer's l2 norm.
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -44,7 +47,9 @@ namespace {
 using namespace tc05;
 
 constexpr float kMaxBeta = 40.0f;
-constexpr int kAgnnThreads = 352;
+// 12 warps: 4 softmax, 4 accumulator, S issuer, 2 loaders, PV issuer (the
+// PV issuer is its own warp in the TF32 d = 32 configuration, see SPLIT_MMA)
+constexpr int kAgnnThreads = 384;
 
 template <int DC, int PREC>
 struct AgnnCfg {
@@ -92,6 +97,14 @@ struct AgnnCfg {
   static constexpr bool PAIR = NB >= 4;
   static constexpr uint32_t SG = PAIR ? 2 : 1;  // chunks per S group
   static constexpr bool EARLY_S = PAIR && NB >= 6;
+  // S and PV issued by two threads (warps 8 and 11), each blocking only on its
+  // own inputs: S(g) on its gathers and its TMEM buffer, PV(c) on P(c).  One
+  // in-order issuer makes PV(c) wait behind S(c + 2)'s gathers.
+#ifdef SGTK_AGNN_ONE_ISSUER
+  static constexpr bool SPLIT_MMA = false;
+#else
+  static constexpr bool SPLIT_MMA = PT;
+#endif
   static_assert(SMEM <= 227u * 1024u, "agnn panel smem");
 };
 
@@ -106,14 +119,20 @@ __device__ __forceinline__ uint32_t kmaj_off(uint32_t row, uint32_t k, uint32_t 
          ((((k >> 2) & 7u) ^ (row & 7u)) << 4) + (k & 3u) * 4u;
 }
 
-template <int DC, int PREC>
-__global__ void __launch_bounds__(kAgnnThreads, 1)
+// TG: the loaders gather the chunk's z and h rows with TMA tile::gather4
+// (4 rows per instruction, swizzled by the tensor maps tmz / tmh straight into
+// the UMMA operand layouts, padding columns zero-filled as out-of-bounds rows)
+// instead of cp.async; TF32 only.
+template <int DC, int PREC, bool TG>
+__global__ void __launch_bounds__(kAgnnThreads, (DC == 32 && PREC != SGTK_FP32) ? 2 : 1)
 agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const float* __restrict__ z,
                   const float* __restrict__ z1, const float* __restrict__ h,
                   const float* __restrict__ h1, uint64_t ld, uint64_t d, uint64_t row_offset,
                   float beta, float* __restrict__ opart, float* __restrict__ lpart,
-                  long long* __restrict__ trace) {
+                  long long* __restrict__ trace, const __grid_constant__ CUtensorMap tmz,
+                  const __grid_constant__ CUtensorMap tmh) {
   using C = AgnnCfg<DC, PREC>;
+  static_assert(!TG || !C::F32, "TMA gathers: TF32 operands only");
   auto mark = [&](uint32_t c, int ev) {
 #ifdef SGTK_TRACE  // pipeline event trace (tools/panel_debug.py); compiled out by default
     if (trace && blockIdx.x < 4 && c < 256) trace[((uint64_t(blockIdx.x) * 256 + c) * 8) + ev] = clock64();
@@ -146,7 +165,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NB; ++i) {
-      mbar_init(bfull + i, 32);  // cp.async.mbarrier.arrive.noinc, one per loader lane
+      mbar_init(bfull + i, TG ? 1 : 32);  // TG: expect_tx; else cp.async.mbarrier.arrive.noinc per lane
       mbar_init(bempty + i, 1);
     }
     for (int i = 0; i < C::NSB; ++i) mbar_init(sfull + i, 1);
@@ -311,9 +330,9 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       }
       if (grow < pv.n_rows) lpart[grow] = lbuf[r];
     }
-  } else if (warp == 8) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && nch) {
+  } else if (warp == 8 || warp == 11) {
+    // ------------------------------------------------------------ MMA issuers
+    if (lane == 0 && nch && (warp == 8 || C::SPLIT_MMA)) {
       constexpr uint32_t id_s = idesc_tf32(32 * C::SG, false);  // N = a S group's columns, B K-major
       constexpr uint32_t id_o = idesc_tf32(DC, true);   // N = DC features, B MN-major
       const uint32_t qb = smem_u32(qs), pb = smem_u32(ps);
@@ -349,23 +368,16 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
         umma_commit(sfull + g % C::NSB);
         mark(c, 0);
       };
-      issue_s(0);
-      for (uint32_t c = 0; c < nch; ++c) {
-        // S of the next group.  Its S buffer held group g - 1, whose last P
-        // was waited for at the previous iteration.  With a deep gather ring
-        // (EARLY_S) it goes at the group's first chunk -- the softmax then has
-        // a whole group of slack -- since its gathers only need PV(c + 2 - NB)
-        // retired; shallow rings issue it at the group's last chunk.
-        if constexpr (C::EARLY_S) {
-          if ((c % C::SG) == 0 && c + C::SG < nch) issue_s(c / C::SG + 1);
-        } else {
-          if ((c % C::SG) == C::SG - 1 && c + 1 < nch) issue_s(c / C::SG + 1);
-        }
+      auto issue_pv = [&](uint32_t c) {
         const uint32_t ds = c % C::NB, pslot = c % C::NP;
         const uint32_t g = c / C::FOLD, buf = g % C::NF;
         const bool first = (c % C::FOLD) == 0;
         if (first && g >= uint32_t(C::NF)) mbar_wait(accempty + buf, ((g / C::NF) - 1u) & 1u);
         mbar_wait(pfull + pslot, (c / C::NP) & 1u);
+        if constexpr (C::SPLIT_MMA) {  // the h tile: landed (long ago), visible to the async proxy
+          mbar_wait(bfull + ds, (c / C::NB) & 1u);
+          fence_async_smem();
+        }
         tc_fence_after();
         const uint32_t pt = pb + pslot * C::PP * C::P_BYTES;
         const uint32_t ht = hr_s + ds * C::T_BYTES;
@@ -387,10 +399,32 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
         mark(c, 3);
         umma_commit(bempty + ds);  // gather slot and P slot free
         if ((c % C::FOLD) == C::FOLD - 1 || c + 1 == nch) umma_commit(accfull + buf);
+      };
+      if constexpr (C::SPLIT_MMA) {
+        if (warp == 8) {
+          for (uint32_t g = 0; g * C::SG < nch; ++g) issue_s(g);
+        } else {
+          for (uint32_t c = 0; c < nch; ++c) issue_pv(c);
+        }
+      } else {
+        issue_s(0);
+        for (uint32_t c = 0; c < nch; ++c) {
+          // S of the next group.  Its S buffer held group g - 1, whose last P
+          // was waited for at the previous iteration.  With a deep gather ring
+          // (EARLY_S) it goes at the group's first chunk -- the softmax then has
+          // a whole group of slack -- since its gathers only need PV(c + 2 - NB)
+          // retired; shallow rings issue it at the group's last chunk.
+          if constexpr (C::EARLY_S) {
+            if ((c % C::SG) == 0 && c + C::SG < nch) issue_s(c / C::SG + 1);
+          } else {
+            if ((c % C::SG) == C::SG - 1 && c + 1 < nch) issue_s(c / C::SG + 1);
+          }
+          issue_pv(c);
+        }
       }
     }
   } else {
-    // ------------------------------------------------------------ loaders
+    // ------------------------------------------------------------ loaders (warps 9, 10)
     // warp 9 takes even chunks, warp 10 odd ones.  Per chunk: 32 z rows
     // (K-major SWIZZLE_128B B of S), 32 h rows (MN-major SWIZZLE_128B_BASE32B
     // B of PV), 128 row masks; completion via cp.async.mbarrier.arrive.noinc.
@@ -409,6 +443,27 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       mbar_wait(bempty + ds, ((c / C::NB) & 1u) ^ 1u);
       if (lane == 0) mark(c, 4);
       const uint32_t ht = hr_s + ds * C::T_BYTES;
+      if constexpr (TG) {
+        // lane g < 8 gathers chunk rows 4g..4g+3: z (K-major SWIZZLE_128B, one
+        // 4 KB tile per 32-feature K block) and h (MN-major 128B_BASE32B, one
+        // 4 KB block per 32 features); padding ids ~0u = row -1: zero-filled
+        const int r0 = int(__shfl_sync(0xFFFFFFFFu, col, (4 * lane) & 31));
+        const int r1 = int(__shfl_sync(0xFFFFFFFFu, col, (4 * lane + 1) & 31));
+        const int r2 = int(__shfl_sync(0xFFFFFFFFu, col, (4 * lane + 2) & 31));
+        const int r3 = int(__shfl_sync(0xFFFFFFFFu, col, (4 * lane + 3) & 31));
+        if (lane < 8) {
+#pragma unroll
+          for (int kb = 0; kb < C::KB; ++kb) {
+            tma_gather4(zr_s + (kb * C::NB + ds) * 4096u + lane * 512u, &tmz, 32 * kb, r0, r1, r2, r3, bfull + ds);
+            tma_gather4(ht + kb * 4096u + lane * 512u, &tmh, 32 * kb, r0, r1, r2, r3, bfull + ds);
+          }
+        } else if (lane == 8) {
+          bulk_load(smem + C::M_OFF + ds * C::M_BYTES, pv.dmask + uint64_t(c0 + c) * kPanelRows, C::M_BYTES,
+                    bfull + ds);
+          mbar_expect_tx(bfull + ds, 2u * C::KB * 32u * 128u + C::M_BYTES);
+        }
+        continue;
+      }
       constexpr uint32_t LPR = DC / 4, RPI = 32 / LPR;
       const uint32_t j = lane % LPR, jj = j & 7u;
 #pragma unroll
@@ -435,7 +490,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       cp_async16(mr_s + ds * C::M_BYTES + lane * 16, pv.dmask + (uint64_t(c0 + c) * kPanelRows) + lane * 4);
       cp_async_arrive_noinc(bfull + ds);
     }
-    cp_async_wait<0>();
+    if constexpr (!TG) cp_async_wait<0>();
   }
 
   tc_fence_before();
@@ -656,6 +711,187 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
   if (nx.zeros && lane == 0 && nz) atomicAdd(nx.zeros, nz);
 }
 
+// Sparse edges, lane = edge form.  Per batch of 32 edges the rows are gathered
+// into a per-warp shared-memory tile exactly as agnn_rows_kernel does (8 / 16
+// lanes per row: whole 128-byte lines per cp.async instruction); then KL =
+// DC/32 lanes per edge (1 at d = 32, 2 at d = 64) each read their 32 features
+// of the row ONCE into registers and
+//   logit: partial dot with z_row (tile row 32, broadcast reads) and, TF32,
+//          |h_col|^2, combined over the KL lanes; p = exp2(beta*log2e*s -
+//          |beta|*log2e);
+//   update: O[32] += coef * row in the lane's own registers (paired FFMA2).
+// End of item: a reduce-scatter over the EPW = 32/KL edge slots (31 / 30
+// shuffle + add steps per lane) leaves DC/32 features per lane (feature index
+// agnn_sparse_feature()), l by an xor tree over the warp.  Same arithmetic
+// per edge as agnn_rows_kernel; the per-row sums are added in a fixed tree
+// order instead of edge order (deterministic, any partition).  Against
+// agnn_rows_kernel: each row is read from shared memory once instead of
+// twice, and the update needs no per-edge broadcast shuffle.
+template <int DC>
+__device__ __forceinline__ uint32_t agnn_sparse_feature(uint32_t lane, uint32_t t) {
+  constexpr uint32_t KL = DC / 32, LV = DC == 32 ? 5 : 4;  // reduce levels = log2(32 / KL)
+  uint32_t idx = 0;
+#pragma unroll
+  for (uint32_t i = 0; i < LV; ++i)
+    if (lane & (KL << i)) idx += 16u >> i;
+  return 32u * (lane % KL) + idx + t;
+}
+// lane holding feature f after the reduce-scatter
+template <int DC>
+__device__ __forceinline__ uint32_t agnn_sparse_lane_of(uint32_t f) {
+  constexpr uint32_t KL = DC / 32, LV = DC == 32 ? 5 : 4;
+  const uint32_t q = f / 32, idx = f % 32;
+  uint32_t s = q;
+#pragma unroll
+  for (uint32_t i = 0; i < LV; ++i)
+    if (idx & (16u >> i)) s += KL << i;
+  return s;
+}
+#ifndef SGTK_SPARSE_MINB
+#define SGTK_SPARSE_MINB 3
+#endif
+template <int DC, int PREC, bool SPLIT>
+__global__ void __launch_bounds__(256, SGTK_SPARSE_MINB)
+agnn_sparse_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2* __restrict__ sent,
+                   const float* __restrict__ zown, const float* __restrict__ z, uint64_t ld,
+                   const float* __restrict__ norm, uint64_t d, uint64_t row_offset, float beta,
+                   const float* __restrict__ opart, const float* __restrict__ lpart,
+                   float* __restrict__ seg_o, float* __restrict__ seg_l, float* __restrict__ osp,
+                   float* __restrict__ lsp, AgnnNext nx) {
+  constexpr uint32_t KL = DC / 32, EPW = 32 / KL, FO = DC / 32;
+  constexpr uint32_t LV = DC == 32 ? 5 : 4;
+  constexpr int TS = DC + 4;  // tile row stride (floats): 16-byte rows, conflict-free quarter warps
+  __shared__ __align__(16) float tile[8][33 * TS];
+  const uint32_t lane = threadIdx.x & 31, q = lane % KL, sub = lane / KL;
+  const uint32_t tb = smem_u32(tile[threadIdx.x >> 5]);
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const float bl2 = beta * 1.4426950408889634f, off = fabsf(beta) * 1.4426950408889634f;
+  unsigned long long nz = 0;
+  for (uint64_t it = warp; it < n_items; it += nw) {
+    const uint4 w = items[it];
+    const uint64_t r = w.x;
+    const bool direct = w.w == 0xFFFFFFFFu;
+    if (w.y < w.z && lane < uint32_t(DC / 4))  // z of the row -> tile row 32
+      cp_async16(tb + (32 * TS + 4 * lane) * 4, zown + (row_offset + r) * ld + 4 * lane);
+    float2 o[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) o[k] = make_float2(0.0f, 0.0f);
+    float lpp = 0.0f;
+    uint32_t col = w.y < w.z && lane < min(32u, w.z - w.y) ? sent[w.y + lane].x : 0u;
+    for (uint32_t e = w.y; e < w.z; e += 32) {
+      const uint32_t cnt = min(32u, w.z - e);
+      const uint32_t col_next = e + 32 < w.z && lane < min(32u, w.z - e - 32) ? sent[e + 32 + lane].x : 0u;
+      {  // cooperative, coalesced gather of the batch's rows into the tile
+        constexpr uint32_t LPR = DC / 4, RPI = 32 / LPR;
+        const uint32_t j = lane % LPR;
+#pragma unroll
+        for (uint32_t t = 0; t < 32 / RPI; ++t) {
+          const uint32_t u = t * RPI + lane / LPR;
+          const uint32_t cu = __shfl_sync(0xFFFFFFFFu, col, u);
+          if (u < cnt) cp_async16(tb + (u * TS + 4 * j) * 4, z + uint64_t(cu) * ld + 4 * j);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp();
+      }
+#pragma unroll
+      for (uint32_t st = 0; st < KL; ++st) {
+        const uint32_t u = st * EPW + sub;  // the lane's edge in the batch
+        const bool val = u < cnt;
+        const uint32_t cu = __shfl_sync(0xFFFFFFFFu, col, u);
+        float2 v[16];
+        float2 s2 = make_float2(0.0f, 0.0f), n22 = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          // slots past the batch hold stale rows: zeros (0 * NaN would stick)
+          const float4 a = val ? ld_shared_f4(tb + (u * TS + 32 * q + 4 * k) * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 zr = ld_shared_f4(tb + (32 * TS + 32 * q + 4 * k) * 4);
+          v[2 * k] = make_float2(a.x, a.y);
+          v[2 * k + 1] = make_float2(a.z, a.w);
+          s2 = __ffma2_rn(make_float2(zr.x, zr.y), v[2 * k], s2);
+          s2 = __ffma2_rn(make_float2(zr.z, zr.w), v[2 * k + 1], s2);
+          if constexpr (PREC == SGTK_TF32) {
+            n22 = __ffma2_rn(v[2 * k], v[2 * k], n22);
+            n22 = __ffma2_rn(v[2 * k + 1], v[2 * k + 1], n22);
+          }
+        }
+        float s = s2.x + s2.y, n2 = n22.x + n22.y;
+#pragma unroll
+        for (uint32_t m = 1; m < KL; m <<= 1) {
+          s += __shfl_xor_sync(0xFFFFFFFFu, s, m);
+          if constexpr (PREC == SGTK_TF32) n2 += __shfl_xor_sync(0xFFFFFFFFu, n2, m);
+        }
+        float cf, pe;
+        if constexpr (PREC == SGTK_TF32) {
+          // tile rows are hq_col = tf32(h_col): z_col = h_col / |h_col| on the
+          // fly; sddmm TF32 rounds the dot (tile_exec.cpp:386)
+          s = tf32_rne(n2 > 0.0f ? s * rsqrtf(n2) : 0.0f);
+          pe = val ? __uint_as_float(tf32_op(ex2_approx(fmaf(s, bl2, -off)))) : 0.0f;
+          cf = pe;
+        } else {
+          pe = val ? ex2_approx(fmaf(s, bl2, -off)) : 0.0f;
+          cf = val ? pe * __ldg(norm + cu) : 0.0f;
+        }
+        if (q == 0) lpp += pe;
+        const float2 cfv = make_float2(cf, cf);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) o[k] = __ffma2_rn(cfv, v[k], o[k]);
+      }
+      __syncwarp();
+      col = col_next;
+    }
+    // reduce-scatter over the edge slots: level i halves the lane's values,
+    // keeping the half selected by lane bit (KL << i)
+    float ov[32];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      ov[2 * k] = o[k].x;
+      ov[2 * k + 1] = o[k].y;
+    }
+#pragma unroll
+    for (uint32_t i = 0; i < LV; ++i) {
+      const uint32_t half = 16u >> i, m = KL << i;
+      const bool b = (lane & m) != 0;
+#pragma unroll
+      for (uint32_t j = 0; j < half; ++j) {
+        const float send = b ? ov[j] : ov[j + half];
+        const float keep = b ? ov[j + half] : ov[j];
+        ov[j] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, m);
+      }
+    }
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) lpp += __shfl_xor_sync(0xFFFFFFFFu, lpp, o2);
+    if (direct && SPLIT) {  // sparse partial; agnn_final_kernel combines
+#pragma unroll
+      for (uint32_t t = 0; t < FO; ++t) {
+        const uint32_t f = agnn_sparse_feature<DC>(lane, t);
+        if (f < d) osp[r * DC + f] = ov[t];
+      }
+      if (lane == 0) lsp[r] = lpp;
+    } else if (direct) {  // + dense partial, in agnn_final_kernel's order; finalise
+      float of[FO];
+      const uint32_t src = agnn_sparse_lane_of<DC>(lane * FO);
+#pragma unroll
+      for (uint32_t t = 0; t < FO; ++t) {
+        const uint32_t f = lane * FO + t;
+        const float mine = __shfl_sync(0xFFFFFFFFu, ov[t], src);
+        of[t] = f < d ? opart[r * DC + f] + mine : 0.0f;
+      }
+      const int fv = lane * FO >= d ? 0 : (d - lane * FO >= FO ? int(FO) : int(d - lane * FO));
+      agnn_finalize<int(FO), PREC>(r, of, lpart[r] + lpp, lane, fv, nx, nz);
+    } else {
+#pragma unroll
+      for (uint32_t t = 0; t < FO; ++t) {
+        const uint32_t f = agnn_sparse_feature<DC>(lane, t);
+        if (f < d) seg_o[uint64_t(w.w) * DC + f] = ov[t];
+      }
+      if (lane == 0) seg_l[w.w] = lpp;
+    }
+  }
+  if (nx.zeros && lane == 0 && nz) atomicAdd(nx.zeros, nz);
+}
+
 // Concurrent mode: (dense + sparse) partials of the non-hub rows, finalised.
 // Streaming: LPR = DC/4 lanes per row (float4 each), 32/LPR rows per warp
 // instruction; the row's l2 norm reduces over its lanes in double by a fixed
@@ -839,6 +1075,14 @@ inline unsigned rows_grid(uint64_t items, unsigned bs) {
   const uint64_t b = (items * 32 + bs - 1) / bs;
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(b, 148ull * SGTK_ROWS_GRID)));
 }
+#ifndef SGTK_SPARSE_GRID
+#define SGTK_SPARSE_GRID 16
+#endif
+// register-form sparse kernel: 8 warps per block, warps loop over items
+inline unsigned sparse_grid(uint64_t items) {
+  const uint64_t b = (items + 7) / 8;
+  return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(b, 148ull * SGTK_SPARSE_GRID)));
+}
 #ifndef SGTK_FINAL_GRID
 #define SGTK_FINAL_GRID 16
 #endif
@@ -850,10 +1094,38 @@ inline unsigned blocks_for(uint64_t n, unsigned bs = 256) {
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + bs - 1) / bs, 148ull * 16)));
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 agnn_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+// Row-gather map over an operand table (rows x ld fp32): box {32 features, 1
+// row}, swizzled for the UMMA layout the tile is read with.
+bool make_gather_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t ld, CUtensorMapSwizzle sw) {
+  auto fn = agnn_encode_fn();
+  if (!fn || (reinterpret_cast<uintptr_t>(base) & 15u) || (ld * 4) % 16 || rows == 0 || rows > 0x7FFFFFFFull)
+    return false;
+  const cuuint64_t dims[2] = {ld, rows};
+  const cuuint64_t strides[1] = {ld * 4};
+  const cuuint32_t box[2] = {32, 1};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int DC, int PREC>
 void launch_agnn_dense(const PanelView& v, uint64_t P, const float* zraw, const float* zq, const float* zq1,
                        const float* hq, const float* hq1, uint64_t ldq, uint64_t d,
-                       uint64_t row_offset, float beta, float* opart, float* lpart, cudaStream_t s) {
+                       uint64_t row_offset, float beta, float* opart, float* lpart, uint64_t table_rows,
+                       cudaStream_t s) {
   using C = AgnnCfg<DC, PREC>;
   // SGTK_AGNN_DENSE_SMEM (bytes): pad the dense kernel's shared memory, e.g.
   // to hold one CTA per SM and leave room for the concurrent CUDA-core kernel
@@ -862,10 +1134,22 @@ void launch_agnn_dense(const PanelView& v, uint64_t P, const float* zraw, const 
     return e ? uint32_t(std::atoi(e)) : 0u;
   }();
   const uint32_t smem = std::max<uint32_t>(C::SMEM, std::min<uint32_t>(pad, 227u * 1024u));
-  once_per_device(reinterpret_cast<const void*>(&agnn_dense_kernel<DC, PREC>), [] {
-    cudaFuncSetAttribute(agnn_dense_kernel<DC, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  once_per_device(reinterpret_cast<const void*>(&agnn_dense_kernel<DC, PREC, false>), [] {
+    cudaFuncSetAttribute(agnn_dense_kernel<DC, PREC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(227u * 1024u));
+    cudaFuncSetAttribute(agnn_dense_kernel<DC, PREC, PREC != SGTK_FP32>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(227u * 1024u));
   });
+  // SGTK_AGNN_GATHER=cp: cp.async gathers instead of TMA tile::gather4
+  static const bool cp_gather = [] {
+    const char* e = std::getenv("SGTK_AGNN_GATHER");
+    return e && std::string(e) == "cp";
+  }();
+  CUtensorMap tmz{}, tmh{};
+  bool tg = PREC != SGTK_FP32 && !cp_gather;
+  if (tg)
+    tg = make_gather_map(&tmz, zq, table_rows, ldq, CU_TENSOR_MAP_SWIZZLE_128B) &&
+         make_gather_map(&tmh, hq, table_rows, ldq, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   // SGTK_PANEL_TRACE=<file>: per-chunk pipeline timestamps of the first 4
   // CTAs (only in a build with -DSGTK_TRACE; otherwise the file is zeros)
   static long long* trace = [] {
@@ -876,8 +1160,12 @@ void launch_agnn_dense(const PanelView& v, uint64_t P, const float* zraw, const 
     }
     return t;
   }();
-  agnn_dense_kernel<DC, PREC><<<unsigned(P), kAgnnThreads, smem, s>>>(
-      v, zraw, zq, zq1, hq, hq1, ldq, d, row_offset, beta, opart, lpart, trace);
+  if (tg)
+    agnn_dense_kernel<DC, PREC, PREC != SGTK_FP32><<<unsigned(P), kAgnnThreads, smem, s>>>(
+        v, zraw, zq, zq1, hq, hq1, ldq, d, row_offset, beta, opart, lpart, trace, tmz, tmh);
+  else
+    agnn_dense_kernel<DC, PREC, false><<<unsigned(P), kAgnnThreads, smem, s>>>(
+        v, zraw, zq, zq1, hq, hq1, ldq, d, row_offset, beta, opart, lpart, trace, tmz, tmh);
   if (trace) {
     std::vector<long long> hb(4 * 256 * 8);
     cudaMemcpy(hb.data(), trace, hb.size() * 8, cudaMemcpyDeviceToHost);
@@ -895,7 +1183,24 @@ void launch_agnn_rows(const Panels& pn, const float* zown, const float* z, uint6
                       float* seg_o, float* seg_l, float* osp, float* lsp, const AgnnNext& nx,
                       cudaStream_t s, cudaStream_t s_final) {
   constexpr unsigned bs = FPL == 1 ? 256 : 128;
-  if (pn.n_aitems) {
+  // SGTK_AGNN_ROWS=lane: the lane-per-edge kernel (agnn_sparse_kernel, d = 32;
+  // measured slower than the tile kernel: 0.38 vs 0.30 ms alone at C4)
+  static const bool tile_rows = [] {
+    const char* e = std::getenv("SGTK_AGNN_ROWS");
+    return !(e && std::string(e) == "lane");
+  }();
+  if (pn.n_aitems && !tile_rows && FPL == 1) {
+    const unsigned grid = sparse_grid(pn.n_aitems);
+    if (osp)
+      agnn_sparse_kernel<32, PREC, true><<<grid, 256, 0, s>>>(
+          pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), zown, z, ld, norm, d, row_offset, beta,
+          opart, lpart, seg_o, seg_l, osp, lsp, nx);
+    else
+      agnn_sparse_kernel<32, PREC, false><<<grid, 256, 0, s>>>(
+          pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), zown, z, ld, norm, d, row_offset, beta,
+          opart, lpart, seg_o, seg_l, osp, lsp, nx);
+    CU_LAUNCH("agnn_sparse_kernel");
+  } else if (pn.n_aitems) {
     if (osp)
       agnn_rows_kernel<FPL, PREC, true><<<rows_grid(pn.n_aitems, bs), bs, 0, s>>>(
           pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), zown, z, ld, norm, d, row_offset, beta,
@@ -949,11 +1254,11 @@ void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, cons
   static const bool serial = std::getenv("SGTK_AGNN_SERIAL") != nullptr;
   auto dense = [&](cudaStream_t st) {
     if (prec == SGTK_FP32) {
-      if (ldq == 32) launch_agnn_dense<32, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, st);
-      else launch_agnn_dense<64, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, st);
+      if (ldq == 32) launch_agnn_dense<32, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, g->n_cols, st);
+      else launch_agnn_dense<64, SGTK_FP32>(v, pn.P, z, zq, zq1, hq, hq1, ldq, d, ro, beta, opart, lpart, g->n_cols, st);
     } else {
-      if (ldq == 32) launch_agnn_dense<32, SGTK_TF32>(v, pn.P, zq, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, st);
-      else launch_agnn_dense<64, SGTK_TF32>(v, pn.P, zq, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, st);
+      if (ldq == 32) launch_agnn_dense<32, SGTK_TF32>(v, pn.P, zq, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, g->n_cols, st);
+      else launch_agnn_dense<64, SGTK_TF32>(v, pn.P, zq, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart, g->n_cols, st);
     }
   };
   auto rows = [&](cudaStream_t st, float* o_sp, float* l_sp, cudaStream_t st_final) {
