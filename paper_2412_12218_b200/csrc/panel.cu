@@ -1247,7 +1247,12 @@ void build_panels(sgtk_graph& g, cudaStream_t s) {
 }
 
 const Panels& panels_for(const sgtk_graph* g, uint64_t d) {
-  return d <= 32 && g->panels32 ? *g->panels32 : *g->panels;
+  // SGTK_PANEL_FORMAT=2: the >= 2-edge format at every width (experiment)
+  static const bool f2 = [] {
+    const char* e = std::getenv("SGTK_PANEL_FORMAT");
+    return e && std::string(e) == "2";
+  }();
+  return d <= 32 && g->panels32 && !f2 ? *g->panels32 : *g->panels;
 }
 
 void panel_debug_set(int mode) { g_panel_debug.store(mode, std::memory_order_relaxed); }

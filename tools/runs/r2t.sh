@@ -1,0 +1,8 @@
+timeout 600 python -m pytest tests/test_gpu_panel.py tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_multigpu.py tests/test_gpu_fullsize.py tests/test_gpu_robust.py -m gpu -q -x -k "agnn or AGNN or robust" 2>&1 | tail -2
+for lib in head default sp32; do
+ if [ $lib = default ]; then unset SGTK_LIB; else export SGTK_LIB=$PWD/variants/libsgtk_$lib.so; fi
+ for e in "X=1" "SGTK_AGNN_ROWS=lane"; do
+  p=tf32
+  echo "$lib $e $p: $(env $e python tools/agnn_only.py --precision $p | tail -1) sparse $(env $e SGTK_PANEL_DEBUG=2 python tools/agnn_only.py --precision $p | tail -1)"
+ done
+done
