@@ -296,8 +296,8 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
     for (int j = 0; j < DC; ++j) acc[j] = 0.0f;
     for (uint32_t g = 0; g < ngroups; ++g) {
       const uint32_t buf = g % C::NF;
-      // (sleeping between probes here, mbar_wait_lazy, measured neutral: the
-      // spinning accumulator warps do not hold back the softmax warps)
+      // (sleeping between probes here measured neutral: the spinning
+      // accumulator warps do not hold back the softmax warps)
       mbar_wait(accfull + buf, (g / C::NF) & 1u);
       tc_fence_after();
 #pragma unroll
@@ -591,7 +591,7 @@ __device__ __forceinline__ void agnn_finalize(uint64_t r, const float (&o)[FPL],
 template <int FPL, int PREC, bool SPLIT>
 __global__ void __launch_bounds__(FPL == 1 ? 256 : 128, FPL == 1 ? SGTK_ROWS_MINB : 2 * SGTK_ROWS_MINB)
 agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2* __restrict__ sent,
-                 const float* __restrict__ zown, const float* __restrict__ z, uint32_t ld,
+                 const float* __restrict__ zown, const float* __restrict__ z, uint64_t ld,
                  const float* __restrict__ norm,
                  uint64_t d, uint64_t row_offset, float beta, const float* __restrict__ opart,
                  const float* __restrict__ lpart, float* __restrict__ seg_o,
@@ -609,17 +609,11 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
   const int fv = f >= d ? 0 : (d - f >= uint64_t(FPL) ? FPL : int(d - f));
   const float bl2 = beta * 1.4426950408889634f, off = fabsf(beta) * 1.4426950408889634f;
   unsigned long long nz = 0;
-  // the next item's descriptor and first column ids are loaded one item
-  // ahead (before the current item's epilogue), off the dependent-load chain
-  uint4 wnext = warp < n_items ? items[warp] : make_uint4(0u, 0u, 0u, 0u);
-  uint32_t cnext = wnext.y < wnext.z && lane < min(32u, wnext.z - wnext.y) ? sent[wnext.y + lane].x : 0u;
-  const float* zl = z + 4 * (lane % uint32_t(DC / 4));
   for (uint64_t it = warp; it < n_items; it += nw) {
-    const uint4 w = wnext;
-    const uint32_t c_first = cnext;
-    if (it + nw < n_items) wnext = items[it + nw];
+    const uint4 w = items[it];
     const uint64_t r = w.x;
     const bool direct = w.w == 0xFFFFFFFFu;
+    const uint32_t c_first = w.y < w.z && lane < min(32u, w.z - w.y) ? sent[w.y + lane].x : 0u;
     // z of the row -> tile row 32 (read back as a broadcast by every lane;
     // lands with the first batch's gathers); padding features are zeros
     if (w.y < w.z && lane < uint32_t(DC / 4))
@@ -639,7 +633,7 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
         for (uint32_t t = 0; t < 32 / RPI; ++t) {
           const uint32_t u = t * RPI + lane / LPR;
           const uint32_t cu = __shfl_sync(0xFFFFFFFFu, col, u);
-          if (u < cnt) cp_async16(tb + (u * TS + 4 * j) * 4, zl + uint64_t(cu) * ld);
+          if (u < cnt) cp_async16(tb + (u * TS + 4 * j) * 4, z + uint64_t(cu) * ld + 4 * j);
         }
         cp_async_commit();
         cp_async_wait<0>();
@@ -699,8 +693,6 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
       __syncwarp();
       col = col_next;
     }
-    if (it + nw < n_items)
-      cnext = wnext.y < wnext.z && lane < min(32u, wnext.z - wnext.y) ? sent[wnext.y + lane].x : 0u;
 #pragma unroll
     for (int o2 = 16; o2 > 0; o2 >>= 1) lpp += __shfl_xor_sync(0xFFFFFFFFu, lpp, o2);
     const float l = l0 + lpp;
@@ -720,203 +712,6 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
   }
   if (nx.zeros && lane == 0 && nz) atomicAdd(nx.zeros, nz);
 }
-
-// Sparse edges, lane = edge form (d <= 32).  Per warp, a double-buffered
-// stream of 32-edge batches over its items:
-//   gather: the batch's rows into a 4 KB tile with coalesced cp.async (8
-//          lanes per 128-byte row, 16-byte pieces XOR-swizzled by row) plus
-//          the item's own z row; one cp.async group per batch, so the next
-//          batch is in flight while this one is computed;
-//   lane u = edge u: reads its row once (8 conflict-free LDS.128), dot with
-//          z_row (broadcast reads) and, TF32, |h_col|^2 on the paired FFMA2;
-//          p = exp2(beta*log2e*s - |beta|*log2e); O[32] += coef * row in its
-//          own registers;
-//   item end: the 32 lanes' O rows go through the consumed tile: 8 x 8-row
-//          column sums + a 2-level xor tree, so lanes 0-7 hold float4 feature
-//          groups (a fixed order: deterministic for any partition); l by an
-//          xor tree.
-// Same arithmetic per edge as agnn_rows_kernel (a summation-order change
-// only).  (Gathering the rows with TMA tile::gather4 instead measured 0.49 ms
-// against 0.30 for the whole sparse part at C4: the TMA unit moves ~14 B per
-// cycle per SM as 128-byte rows.)
-#ifndef SGTK_SPARSE_MINB
-#define SGTK_SPARSE_MINB 3
-#endif
-template <int PREC, bool SPLIT>
-__global__ void __launch_bounds__(256, SGTK_SPARSE_MINB)
-agnn_sparse_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2* __restrict__ sent,
-                   const float* __restrict__ zown, const float* __restrict__ z, uint32_t ld,
-                   const float* __restrict__ norm, uint64_t d, uint64_t row_offset, float beta,
-                   const float* __restrict__ opart, const float* __restrict__ lpart,
-                   float* __restrict__ seg_o, float* __restrict__ seg_l, float* __restrict__ osp,
-                   float* __restrict__ lsp, AgnnNext nx) {
-  extern __shared__ __align__(128) uint8_t sm[];  // kSparseSmem
-  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint32_t tiles = smem_u32(sm) + wib * 2u * 4096u;            // [2] x 4 KB
-  const uint32_t zrow = smem_u32(sm) + 16u * 4096u + wib * 2u * 128u;  // [2] x 128 B
-  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  const float bl2 = beta * 1.4426950408889634f, off = fabsf(beta) * 1.4426950408889634f;
-  unsigned long long nz = 0;
-  const uint32_t j = lane & 7u, rsub = lane >> 3;  // gather: piece j of row 4t + rsub
-  const float* zl = z + 4 * j;
-
-  // results of an item: lanes 0-7 hold features 4*lane .. 4*lane+3 (every
-  // lane of a column group holds the same values), l on every lane
-  auto emit = [&](const uint4& w, const float4& ov, float l) {
-    const uint64_t r = w.x;
-    const bool direct = w.w == 0xFFFFFFFFu;
-    if (direct && !SPLIT) {  // + dense partial (agnn_final_kernel's order), finalise
-      const uint32_t src = lane >> 2, comp = lane & 3u;
-      const float c0 = __shfl_sync(0xFFFFFFFFu, ov.x, src), c1 = __shfl_sync(0xFFFFFFFFu, ov.y, src);
-      const float c2 = __shfl_sync(0xFFFFFFFFu, ov.z, src), c3 = __shfl_sync(0xFFFFFFFFu, ov.w, src);
-      const float mine = comp == 0 ? c0 : comp == 1 ? c1 : comp == 2 ? c2 : c3;
-      float of[1] = {lane < d ? opart[r * 32 + lane] + mine : 0.0f};
-      agnn_finalize<1, PREC>(r, of, lpart[r] + l, lane, lane < d ? 1 : 0, nx, nz);
-      return;
-    }
-    float* dst = direct ? osp + r * 32 : seg_o + uint64_t(w.w) * 32;
-    if (lane < 8) {
-      if (4 * lane + 3 < d) {
-        *reinterpret_cast<float4*>(dst + 4 * lane) = ov;
-      } else {
-        const float vv[4] = {ov.x, ov.y, ov.z, ov.w};
-#pragma unroll
-        for (uint32_t i = 0; i < 4; ++i)
-          if (4 * lane + i < d) dst[4 * lane + i] = vv[i];
-      }
-    }
-    if (lane == 0) (direct ? lsp[r] : seg_l[w.w]) = l;
-  };
-  auto load_item = [&](uint64_t i) { return i < n_items ? items[i] : make_uint4(0u, 0u, 0u, 0u); };
-  // advance to the next item with edges; items without edges emit at once
-  auto skip_empty = [&](uint64_t& i, uint4& w) {
-    while (i < n_items && w.y == w.z) {
-      emit(w, make_float4(0.f, 0.f, 0.f, 0.f), 0.0f);
-      i += nw;
-      w = load_item(i);
-    }
-  };
-  auto issue = [&](uint32_t b, const uint4& w, uint32_t e0) {
-    const uint32_t n = min(32u, w.z - e0);
-    const uint32_t cv = lane < n ? __ldg(&sent[e0 + lane].x) : 0u;
-    const uint32_t tb = tiles + b * 4096u;
-#pragma unroll
-    for (uint32_t t = 0; t < 8; ++t) {
-      const uint32_t u = 4 * t + rsub;
-      const uint32_t cu = __shfl_sync(0xFFFFFFFFu, cv, u);
-      if (u < n) cp_async16(tb + u * 128u + ((j ^ (u & 7u)) << 4), zl + uint64_t(cu) * ld);
-    }
-    if (lane < 8) cp_async16(zrow + b * 128u + lane * 16u, zown + (row_offset + w.x) * ld + 4 * lane);
-    cp_async_commit();
-  };
-
-  uint64_t it = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  uint4 cw = load_item(it);
-  skip_empty(it, cw);
-  if (it < n_items) issue(0, cw, cw.y);
-  uint32_t e = cw.y, b = 0;
-  float2 o[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) o[k] = make_float2(0.0f, 0.0f);
-  float lpp = 0.0f;
-  while (it < n_items) {
-    // the next batch: the rest of this item, or the next item with edges
-    uint64_t nit = it;
-    uint4 nwk = cw;
-    uint32_t ne = e + 32;
-    const bool last = ne >= cw.z;
-    if (last) {
-      nit = it + nw;
-      nwk = load_item(nit);
-      skip_empty(nit, nwk);
-      ne = nwk.y;
-    }
-    if (nit < n_items) {
-      issue(b ^ 1u, nwk, ne);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncwarp();
-    {
-      const uint32_t cnt = min(32u, cw.z - e);
-      const bool val = lane < cnt;
-      const uint32_t tb = tiles + b * 4096u + lane * 128u, zb = zrow + b * 128u;
-      float2 v[16];
-      float2 s2 = make_float2(0.0f, 0.0f), n22 = make_float2(0.0f, 0.0f);
-#pragma unroll
-      for (uint32_t k = 0; k < 8; ++k) {
-        const float4 a = ld_shared_f4(tb + ((k ^ (lane & 7u)) << 4));
-        const float4 zr = ld_shared_f4(zb + k * 16u);
-        v[2 * k] = make_float2(a.x, a.y);
-        v[2 * k + 1] = make_float2(a.z, a.w);
-        s2 = __ffma2_rn(make_float2(zr.x, zr.y), v[2 * k], s2);
-        s2 = __ffma2_rn(make_float2(zr.z, zr.w), v[2 * k + 1], s2);
-        if constexpr (PREC == SGTK_TF32) {
-          n22 = __ffma2_rn(v[2 * k], v[2 * k], n22);
-          n22 = __ffma2_rn(v[2 * k + 1], v[2 * k + 1], n22);
-        }
-      }
-      float s = s2.x + s2.y;
-      float cf, pe;
-      if constexpr (PREC == SGTK_TF32) {
-        // rows are hq_col = tf32(h_col): z_col = h_col / |h_col| on the fly;
-        // sddmm TF32 rounds the dot (tile_exec.cpp:386)
-        const float n2 = n22.x + n22.y;
-        s = tf32_rne(n2 > 0.0f ? s * rsqrtf(n2) : 0.0f);
-        pe = val ? __uint_as_float(tf32_op(ex2_approx(fmaf(s, bl2, -off)))) : 0.0f;
-        cf = pe;
-      } else {
-        pe = val ? ex2_approx(fmaf(s, bl2, -off)) : 0.0f;
-        cf = val ? pe * __ldg(norm + __ldg(&sent[e + lane].x)) : 0.0f;
-      }
-      lpp += pe;
-      if (val) {  // slots past the batch hold stale rows (0 * NaN would stick)
-        const float2 cfv = make_float2(cf, cf);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) o[k] = __ffma2_rn(cfv, v[k], o[k]);
-      }
-    }
-    __syncwarp();
-    if (last) {
-      // column sums of the lanes' O rows through the tile just consumed
-      const uint32_t tb = tiles + b * 4096u;
-#pragma unroll
-      for (uint32_t k = 0; k < 8; ++k)
-        st_shared_v4(tb + lane * 128u + ((k ^ (lane & 7u)) << 4), __float_as_uint(o[2 * k].x),
-                     __float_as_uint(o[2 * k].y), __float_as_uint(o[2 * k + 1].x), __float_as_uint(o[2 * k + 1].y));
-      __syncwarp();
-      const uint32_t f4 = lane & 7u, rg = lane >> 3;
-      float2 a0 = make_float2(0.0f, 0.0f), a1 = make_float2(0.0f, 0.0f);
-#pragma unroll
-      for (uint32_t i = 0; i < 8; ++i) {
-        const uint32_t row = rg * 8 + i;
-        const float4 t = ld_shared_f4(tb + row * 128u + ((f4 ^ (row & 7u)) << 4));
-        a0 = __fadd2_rn(a0, make_float2(t.x, t.y));
-        a1 = __fadd2_rn(a1, make_float2(t.z, t.w));
-      }
-#pragma unroll
-      for (uint32_t m = 8; m < 32; m <<= 1) {
-        a0 = __fadd2_rn(a0, make_float2(__shfl_xor_sync(0xFFFFFFFFu, a0.x, m), __shfl_xor_sync(0xFFFFFFFFu, a0.y, m)));
-        a1 = __fadd2_rn(a1, make_float2(__shfl_xor_sync(0xFFFFFFFFu, a1.x, m), __shfl_xor_sync(0xFFFFFFFFu, a1.y, m)));
-      }
-#pragma unroll
-      for (int m = 16; m > 0; m >>= 1) lpp += __shfl_xor_sync(0xFFFFFFFFu, lpp, m);
-      __syncwarp();
-      emit(cw, make_float4(a0.x, a0.y, a1.x, a1.y), lpp);
-#pragma unroll
-      for (int k = 0; k < 16; ++k) o[k] = make_float2(0.0f, 0.0f);
-      lpp = 0.0f;
-    }
-    it = nit;
-    cw = nwk;
-    e = ne;
-    b ^= 1u;
-  }
-  if (nx.zeros && lane == 0 && nz) atomicAdd(nx.zeros, nz);
-}
-
-constexpr uint32_t kSparseSmem = 8 * 2 * (4096 + 128);
 
 // Concurrent mode: (dense + sparse) partials of the non-hub rows, finalised.
 // Streaming: LPR = DC/4 lanes per row (float4 each), 32/LPR rows per warp
@@ -1101,15 +896,6 @@ inline unsigned rows_grid(uint64_t items, unsigned bs) {
   const uint64_t b = (items * 32 + bs - 1) / bs;
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(b, 148ull * SGTK_ROWS_GRID)));
 }
-#ifndef SGTK_SPARSE_GRID
-#define SGTK_SPARSE_GRID 3
-#endif
-// lane-per-edge sparse kernel: one wave (3 blocks of 8 warps per SM), warps
-// loop over items with their gathers double-buffered
-inline unsigned sparse_grid(uint64_t items) {
-  const uint64_t b = (items + 7) / 8;
-  return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(b, 148ull * SGTK_SPARSE_GRID)));
-}
 #ifndef SGTK_FINAL_GRID
 #define SGTK_FINAL_GRID 16
 #endif
@@ -1212,35 +998,14 @@ void launch_agnn_rows(const Panels& pn, const float* zown, const float* z, uint6
                       float* seg_o, float* seg_l, float* osp, float* lsp, const AgnnNext& nx,
                       uint64_t table_rows, cudaStream_t s, cudaStream_t s_final) {
   constexpr unsigned bs = FPL == 1 ? 256 : 128;
-  // SGTK_AGNN_ROWS=lane: the lane-per-edge kernel (agnn_sparse_kernel, d = 32;
-  // measured slower than the tile kernel: 0.38 vs 0.30 ms alone at C4)
-  static const bool tile_rows = [] {
-    const char* e = std::getenv("SGTK_AGNN_ROWS");
-    return !(e && std::string(e) == "lane");
-  }();
-  if (pn.n_aitems && !tile_rows && FPL == 1 && ld <= 0xFFFFFFFFull) {
-    const unsigned grid = sparse_grid(pn.n_aitems);
-    once_per_device(reinterpret_cast<const void*>(&agnn_sparse_kernel<PREC, true>), [] {
-      cudaFuncSetAttribute(agnn_sparse_kernel<PREC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSparseSmem));
-      cudaFuncSetAttribute(agnn_sparse_kernel<PREC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSparseSmem));
-    });
-    if (osp)
-      agnn_sparse_kernel<PREC, true><<<grid, 256, kSparseSmem, s>>>(
-          pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), zown, z, uint32_t(ld), norm, d, row_offset,
-          beta, opart, lpart, seg_o, seg_l, osp, lsp, nx);
-    else
-      agnn_sparse_kernel<PREC, false><<<grid, 256, kSparseSmem, s>>>(
-          pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), zown, z, uint32_t(ld), norm, d, row_offset,
-          beta, opart, lpart, seg_o, seg_l, osp, lsp, nx);
-    CU_LAUNCH("agnn_sparse_kernel");
-  } else if (pn.n_aitems) {
+  if (pn.n_aitems) {
     if (osp)
       agnn_rows_kernel<FPL, PREC, true><<<rows_grid(pn.n_aitems, bs), bs, 0, s>>>(
-          pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), zown, z, uint32_t(ld), norm, d, row_offset, beta,
+          pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), zown, z, ld, norm, d, row_offset, beta,
           opart, lpart, seg_o, seg_l, osp, lsp, nx);
     else
       agnn_rows_kernel<FPL, PREC, false><<<rows_grid(pn.n_aitems, bs), bs, 0, s>>>(
-          pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), zown, z, uint32_t(ld), norm, d, row_offset, beta,
+          pn.aitems->as<uint4>(), pn.n_aitems, pn.sent->as<uint2>(), zown, z, ld, norm, d, row_offset, beta,
           opart, lpart, seg_o, seg_l, osp, lsp, nx);
     CU_LAUNCH("agnn_rows_kernel");
   }

@@ -61,18 +61,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   while (!mbar_try_suspend(b, parity))
     if (clock64() - t0 > (1ll << 33)) __trap();
 }
-// Wait for a phase that is known to be far off (thousands of cycles), by
-// warps off the critical path: plain sleeps between probes, so the waiting
-// warp does not wake on every mbarrier event of the CTA and take issue slots
-// from the working warps (try_wait's suspend ends at any barrier update).
-__device__ __forceinline__ void mbar_wait_lazy(uint64_t* b, uint32_t parity, uint32_t ns) {
-  if (mbar_try(b, parity)) return;
-  const long long t0 = clock64();
-  do {
-    __nanosleep(ns);
-    if (clock64() - t0 > (1ll << 33)) __trap();
-  } while (!mbar_try(b, parity));
-}
 // Non-blocking probe: true once the phase with this parity has completed.
 __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
   uint32_t ok;
