@@ -123,8 +123,13 @@ __device__ __forceinline__ uint32_t kmaj_off(uint32_t row, uint32_t k, uint32_t 
 // (4 rows per instruction, swizzled by the tensor maps tmz / tmh straight into
 // the UMMA operand layouts, padding columns zero-filled as out-of-bounds rows)
 // instead of cp.async; TF32 only.
+#ifdef SGTK_DENSE_MAXREG
+template <int DC, int PREC, bool TG>
+__global__ void __launch_bounds__(kAgnnThreads) __maxnreg__((DC == 32 && PREC != SGTK_FP32) ? SGTK_DENSE_MAXREG : 168)
+#else
 template <int DC, int PREC, bool TG>
 __global__ void __launch_bounds__(kAgnnThreads, (DC == 32 && PREC != SGTK_FP32) ? 2 : 1)
+#endif
 agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const float* __restrict__ z,
                   const float* __restrict__ z1, const float* __restrict__ h,
                   const float* __restrict__ h1, uint64_t ld, uint64_t d, uint64_t row_offset,
@@ -588,8 +593,14 @@ __device__ __forceinline__ void agnn_finalize(uint64_t r, const float (&o)[FPL],
 #ifndef SGTK_ROWS_MINB
 #define SGTK_ROWS_MINB 5
 #endif
+#ifndef SGTK_ROWS_WARPS
+#define SGTK_ROWS_WARPS 2
+#endif
+// rows kernel block: SGTK_ROWS_WARPS warps (d = 32), half as many at d = 64
+constexpr int kRowsWarps1 = SGTK_ROWS_WARPS, kRowsWarps2 = SGTK_ROWS_WARPS > 1 ? SGTK_ROWS_WARPS / 2 : 1;
 template <int FPL, int PREC, bool SPLIT>
-__global__ void __launch_bounds__(FPL == 1 ? 256 : 128, FPL == 1 ? SGTK_ROWS_MINB : 2 * SGTK_ROWS_MINB)
+__global__ void __launch_bounds__(FPL == 1 ? 32 * kRowsWarps1 : 32 * kRowsWarps2,
+                                  (FPL == 1 ? SGTK_ROWS_MINB : 2 * SGTK_ROWS_MINB) * 8 / SGTK_ROWS_WARPS)
 agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2* __restrict__ sent,
                  const float* __restrict__ zown, const float* __restrict__ z, uint64_t ld,
                  const float* __restrict__ norm,
@@ -599,7 +610,7 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
                  AgnnNext nx) {
   constexpr int DC = 32 * FPL;
   constexpr int TS = DC + 4;  // smem tile row stride (floats): 16-byte rows, spread banks
-  __shared__ __align__(16) float tile[FPL == 1 ? 8 : 4][33 * TS];  // 32 z_col rows + z_row
+  __shared__ __align__(16) float tile[FPL == 1 ? kRowsWarps1 : kRowsWarps2][33 * TS];  // 32 z_col rows + z_row
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float* T = tile[wib];
   const uint32_t tb = smem_u32(T);
@@ -894,7 +905,7 @@ __global__ void agnn_input_kernel(const float* __restrict__ x, uint64_t ldx, uin
 // SM (measured: 16 -> 32 is -1.5%, 64+ and 10- slower)
 inline unsigned rows_grid(uint64_t items, unsigned bs) {
   const uint64_t b = (items * 32 + bs - 1) / bs;
-  return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(b, 148ull * SGTK_ROWS_GRID)));
+  return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(b, 148ull * SGTK_ROWS_GRID * 256 / bs)));
 }
 #ifndef SGTK_FINAL_GRID
 #define SGTK_FINAL_GRID 16
@@ -997,7 +1008,7 @@ void launch_agnn_rows(const Panels& pn, const float* zown, const float* z, uint6
                       uint64_t row_offset, float beta, const float* opart, const float* lpart,
                       float* seg_o, float* seg_l, float* osp, float* lsp, const AgnnNext& nx,
                       uint64_t table_rows, cudaStream_t s, cudaStream_t s_final) {
-  constexpr unsigned bs = FPL == 1 ? 256 : 128;
+  constexpr unsigned bs = FPL == 1 ? 32 * kRowsWarps1 : 32 * kRowsWarps2;
   if (pn.n_aitems) {
     if (osp)
       agnn_rows_kernel<FPL, PREC, true><<<rows_grid(pn.n_aitems, bs), bs, 0, s>>>(
