@@ -66,6 +66,11 @@ struct Panels {
   std::shared_ptr<DevBuf> deid;   // u32[n_dent]  CSR edge id (0xFFFFFFFF for padding)
   std::shared_ptr<DevBuf> dmask;  // u32[n_chunks * 128] row r's edge bits in the chunk (AGNN)
   std::shared_ptr<DevBuf> rowoff; // u16[n_chunks * 128] entries of the chunk before row r (SDDMM)
+  // u32[n_dent] SDDMM entry: (position in the CSR row) << 12 | panel row << 5 |
+  // chunk column (0xFFFFFFFF for padding); built with the format (not
+  // persisted); dpos_ok = every position < 2^20
+  std::shared_ptr<DevBuf> dpos;
+  bool dpos_ok = false;
   std::shared_ptr<DevBuf> sptr;   // u32[n_rows+1] sparse edges of a row
   std::shared_ptr<DevBuf> sent;   // uint2[n_sparse] (column, value bits)
   std::shared_ptr<DevBuf> seid;   // u32[n_sparse] CSR edge id

@@ -193,6 +193,35 @@ __global__ void entry_fill_sorted_kernel(const uint32_t* __restrict__ e2r, const
 
 
 
+// SDDMM entries (dpos): the entry's panel row and chunk column from its
+// packed tile offset (a_word inverted), its position in the CSR row from its
+// edge id.  Block per panel.
+__global__ void dpos_kernel(const uint32_t* __restrict__ cptr, const uint64_t* __restrict__ coff,
+                            const uint32_t* __restrict__ dent, const uint32_t* __restrict__ deid,
+                            const uint64_t* __restrict__ np, uint64_t P, uint32_t* __restrict__ dpos,
+                            uint32_t* __restrict__ overflow) {
+  for (uint64_t p = blockIdx.x; p < P; p += gridDim.x) {
+    const uint64_t i0 = coff[cptr[p]], i1 = coff[cptr[p + 1]];
+    for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+      const uint32_t e = deid[i];
+      if (e == 0xFFFFFFFFu) {
+        dpos[i] = 0xFFFFFFFFu;
+        continue;
+      }
+      const uint32_t w = dent[i] & 0xFFFu;
+      const uint32_t row = (w >> 8) * 8u + ((w >> 5) & 7u);
+      const uint32_t k = ((((w >> 2) & 7u) ^ (row & 7u)) << 2) | (w & 3u);
+      const uint64_t pos = uint64_t(e) - np[p * kPanelRows + row];
+      if (pos >= (1u << 20)) {
+        atomicOr(overflow, 1u);
+        dpos[i] = 0xFFFFFFFFu;
+      } else {
+        dpos[i] = (uint32_t(pos) << 12) | (row << 5) | k;
+      }
+    }
+  }
+}
+
 // Padding entries of a chunk: value 0 at the first position with no edge
 // (a chunk with all 4096 positions taken has no padding).  Warp per chunk.
 __global__ void entry_pad_kernel(const uint32_t* __restrict__ ccnt, const uint64_t* __restrict__ coff,
@@ -960,6 +989,25 @@ void launch_sparse(const Panels& pn, const uint2* sent, const float* x, uint64_t
 
 // ---------------------------------------------------------------- builder
 namespace {
+void build_dpos(const sgtk_graph& g, Panels& pn, cudaStream_t s) {
+  pn.dpos = std::make_shared<DevBuf>(std::max<uint64_t>(pn.n_dent, 4) * 4);
+  pn.dpos_ok = false;
+  if (!pn.n_dent || !pn.P) {
+    pn.dpos_ok = true;
+    return;
+  }
+  DevBuf ov(4);
+  CU(cudaMemsetAsync(ov.p, 0, 4, s));
+  dpos_kernel<<<unsigned(std::min<uint64_t>(pn.P, 148ull * 16)), 256, 0, s>>>(
+      pn.cptr->as<uint32_t>(), pn.coff->as<uint64_t>(), pn.dent->as<uint32_t>(), pn.deid->as<uint32_t>(),
+      g.np->as<uint64_t>(), pn.P, pn.dpos->as<uint32_t>(), ov.as<uint32_t>());
+  CU_LAUNCH("dpos_kernel");
+  uint32_t h = 1;
+  CU(cudaMemcpyAsync(&h, ov.p, 4, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  pn.dpos_ok = h == 0;
+}
+
 std::shared_ptr<Panels> build_panel_format(sgtk_graph& g, uint32_t dense_min, cudaStream_t s) {
   auto pn = std::make_shared<Panels>();
   const uint64_t n = g.n_rows, E = g.nnz;
@@ -1091,6 +1139,7 @@ std::shared_ptr<Panels> build_panel_format(sgtk_graph& g, uint32_t dense_min, cu
   pn->items = ul(items.data(), items.size(), s);
   pn->lrows = ul(lrows.data(), lrows.size(), s);
   CU(cudaStreamSynchronize(s));
+  build_dpos(g, *pn, s);
   return pn;
 }
 }  // namespace
@@ -1225,6 +1274,8 @@ bool load_panel_section(sgtk_graph& g, const std::string& path, cudaStream_t s) 
       const uint64_t P = (g.n_rows + kPanelRows - 1) / kPanelRows;
       if (a->P != P || b->P != P) raise(SGTK_ERR_IO, "SGP1: panel count does not match the graph");
       if (std::fgetc(f) != EOF) raise(SGTK_ERR_IO, "SGP1: trailing bytes");
+      build_dpos(g, *a, s);
+      build_dpos(g, *b, s);
       g.panels = a;
       g.panels32 = b;
       g.panels_loaded = true;

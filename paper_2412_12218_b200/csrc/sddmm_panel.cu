@@ -36,6 +36,8 @@
 // split (hi*hi + hi*lo + lo*hi, dropped terms < 2^-21 relative per product).
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "kernels.cuh"
 #include "tc05.cuh"
@@ -322,6 +324,276 @@ sddmm_dense_kernel(const PanelView pv, const uint32_t* __restrict__ deid,
   }
 }
 
+// Dense part, direct form (sddmm_dense2_kernel): the chunk's dots go once
+// through a row tile in shared memory and the store warps read each entry's
+// dot from it by the entry's (panel row, chunk column) -- no per-row
+// compaction loop.  An entry is one u32 (Panels::dpos: position in its CSR
+// row << 12 | panel row << 5 | chunk column); out[np[row] + position].
+//   warps 0-3  stage: the A operand; per chunk the row's 32 dots from TMEM
+//              (tcgen05.ld) into row tile c % NR (8 conflict-free 16-byte
+//              stores, stride 36 floats);
+//   warps 4-7  store: the chunk's entries (bulk-copied ahead by the TMA
+//              engine), a_e * dot, out[e];
+//   warp 8     TMEM allocator + tcgen05.mma issuer (S buffers over 4 x 32
+//              TMEM columns);
+//   warps 9-10 loaders (even / odd chunks): the chunk's 32 y rows (cp.async,
+//              K-major SWIZZLE_128B), the bulk copy of its entries.
+template <int DC, int PREC>
+struct Sd2Cfg {
+  static constexpr bool F32 = PREC == SGTK_FP32;
+  static constexpr int PL = F32 ? 2 : 1;
+  static constexpr int KB = DC / 32;
+  static constexpr int NB = (F32 && DC == 64) ? 4 : 6;
+  static constexpr int NS = 4;
+  static constexpr int NR = 2;                               // row tiles
+  static constexpr int NE = 4;                               // entry ring
+  static constexpr uint32_t RS = 36;                         // row tile stride (floats)
+  static constexpr uint32_t Q_BYTES = kPanelRows * DC * 4;
+  static constexpr uint32_t TILE = kChunkCols * 128;
+  static constexpr uint32_t Q_OFF = 1024;
+  static constexpr uint32_t Z_OFF = Q_OFF + PL * Q_BYTES;
+  static constexpr uint32_t R_OFF = Z_OFF + PL * KB * NB * TILE;
+  static constexpr uint32_t NP_OFF = R_OFF + NR * kPanelRows * RS * 4;  // u64[128] row starts
+  static constexpr uint32_t E_OFF = NP_OFF + kPanelRows * 8;
+  static uint32_t smem_bytes(uint32_t eslot, bool with_vals) {
+    return E_OFF + NE * eslot * (with_vals ? 2u : 1u) + 1024;
+  }
+  static constexpr uint32_t TMEM_COLS = NS * 32;
+};
+
+template <int DC, int PREC>
+__global__ void __launch_bounds__(kSdThreads, 2)
+sddmm_dense2_kernel(const PanelView pv, const uint32_t* __restrict__ dpos, const uint64_t* __restrict__ np,
+                    uint32_t eslot, const float* __restrict__ x, uint64_t ldx, uint64_t d,
+                    uint64_t row_offset, const float* __restrict__ inv, const float* __restrict__ yq,
+                    const float* __restrict__ yq1, uint64_t ldq, const float* __restrict__ dval,
+                    const float* __restrict__ ev, float scale, float* __restrict__ out) {
+  using C = Sd2Cfg<DC, PREC>;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(smem);  // [NB] y rows landed
+  uint64_t* bempty = bfull + C::NB;                     // [NB] MMA retired
+  uint64_t* sfull = bempty + C::NB;                     // [NS] S in TMEM
+  uint64_t* sempty = sfull + C::NS;                     // [NS] S read back
+  uint64_t* qfull = sempty + C::NS;                     // A operand staged (+ row starts)
+  uint64_t* efull = qfull + 1;                          // [NE] entries landed
+  uint64_t* eempty = efull + C::NE;                     // [NE] entries consumed
+  uint64_t* rfull = eempty + C::NE;                     // [NR] row tile written
+  uint64_t* rempty = rfull + C::NR;                     // [NR] row tile consumed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + C::NR);
+  uint32_t* ecnt = tmem_slot + 4;                       // [NE] entries of the slot's chunk
+  const uint32_t qb = smem_u32(smem + C::Q_OFF), zb = smem_u32(smem + C::Z_OFF);
+  const uint32_t rb = smem_u32(smem + C::R_OFF);
+  uint64_t* nps = reinterpret_cast<uint64_t*>(smem + C::NP_OFF);
+  uint8_t* ering = smem + C::E_OFF;
+  const bool has_dval = dval != nullptr;
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t p = blockIdx.x;
+  const uint32_t c0 = pv.cptr[p], nch = pv.cptr[p + 1] - c0;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NB; ++i) {
+      mbar_init(bfull + i, 32);  // one cp.async.mbarrier.arrive.noinc per loader lane
+      mbar_init(bempty + i, 1);  // tcgen05.commit
+    }
+    for (int i = 0; i < C::NS; ++i) {
+      mbar_init(sfull + i, 1);
+      mbar_init(sempty + i, 4);
+    }
+    mbar_init(qfull, 4);
+    for (int i = 0; i < C::NE; ++i) {
+      mbar_init(efull + i, 1);
+      mbar_init(eempty + i, 8);  // the 8 storing warps
+    }
+    for (int i = 0; i < C::NR; ++i) {
+      mbar_init(rfull + i, 4);
+      mbar_init(rempty + i, 8);
+    }
+    mbar_init_fence();
+  }
+  if (warp == 8) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // a share of chunk c's entries: thread t of the 256 storing threads (store
+  // warps t < 128, stage warps t >= 128) takes entries t, t + 256, ...
+  auto store_chunk = [&](uint32_t c, uint32_t t) {
+      const uint32_t rt = c % C::NR, de = c % C::NE;
+      mbar_wait(efull + de, (c / C::NE) & 1u);
+      const uint32_t cnt = ecnt[de];
+      mbar_wait(rfull + rt, (c / C::NR) & 1u);
+      const uint32_t* ent = reinterpret_cast<const uint32_t*>(ering + de * eslot);
+      const float* evl = reinterpret_cast<const float*>(ering + (C::NE + de) * eslot);
+      const float* rtile = reinterpret_cast<const float*>(smem + C::R_OFF) + rt * kPanelRows * C::RS;
+      if (!ev && !has_dval) {  // unit values: a_e = 1 (tf32(1) = 1)
+        for (uint32_t i = t; i < cnt; i += 256) {
+          const uint32_t w = ent[i];
+          if (w == 0xFFFFFFFFu) continue;  // padding entry
+          const float dot = rtile[((w >> 5) & 127u) * C::RS + (w & 31u)];
+          const uint64_t e = nps[(w >> 5) & 127u] + (w >> 12);
+          out[e] = (PREC == SGTK_TF32 ? tf32_rne(dot) : dot) * scale;
+        }
+      } else {
+        for (uint32_t i = t; i < cnt; i += 256) {
+          const uint32_t w = ent[i];
+          if (w == 0xFFFFFFFFu) continue;  // padding entry
+          const uint32_t row = (w >> 5) & 127u, k = w & 31u;
+          const float dot = rtile[row * C::RS + k];
+          const uint64_t e = nps[row] + (w >> 12);
+          const float a = ev ? __ldg(ev + e) : evl[i];
+          const float v = PREC == SGTK_TF32 ? tf32_rne(a) * tf32_rne(dot) : a * dot;
+          out[e] = v * scale;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(rempty + rt);
+        mbar_arrive(eempty + de);
+      }
+  };
+
+  if (warp < 4) {
+    // ---------------------------------------------------------- stage warps
+    const uint32_t r = warp * 32 + lane;
+    const uint64_t grow = p * kPanelRows + r;
+    {  // A = x[panel rows] (z = x * inv when normalising on the fly)
+      const bool rv = grow < pv.n_rows;
+      nps[r] = rv ? np[grow] : 0ull;
+      const float* src = x + (row_offset + grow) * ldx;
+      const float sc = (rv && inv) ? inv[row_offset + grow] : 1.0f;
+#pragma unroll
+      for (int j = 0; j < DC / 4; ++j) {
+        float v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint64_t f = 4 * j + i;
+          float t = (rv && f < d) ? __ldg(src + f) : 0.0f;
+          v[i] = inv ? t * sc : t;
+        }
+        const uint32_t o = sd_kmaj(r, 4 * j, kPanelRows);
+        if constexpr (C::F32) {
+          uint32_t a0[4], a1[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) split2(v[i], a0[i], a1[i]);
+          st_shared_v4(qb + o, a0[0], a0[1], a0[2], a0[3]);
+          st_shared_v4(qb + C::Q_BYTES + o, a1[0], a1[1], a1[2], a1[3]);
+        } else {
+          st_shared_v4(qb + o, tf32_op(v[0]), tf32_op(v[1]), tf32_op(v[2]), tf32_op(v[3]));
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qfull);
+    }
+    for (uint32_t c = 0; c < nch; ++c) {
+      const uint32_t b = c % C::NS, rt = c % C::NR;
+      mbar_wait(sfull + b, (c / C::NS) & 1u);
+      tc_fence_after();
+      uint32_t sv[32];
+      tmem_ld16(tmem + ((warp * 32u) << 16) + b * 32, *reinterpret_cast<uint32_t(*)[16]>(sv));
+      tmem_ld16(tmem + ((warp * 32u) << 16) + b * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sempty + b);
+      if (c >= uint32_t(C::NR)) mbar_wait(rempty + rt, ((c / C::NR) - 1u) & 1u);
+      const uint32_t rr = rb + (rt * kPanelRows + r) * C::RS * 4;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) st_shared_v4(rr + q * 16, sv[4 * q], sv[4 * q + 1], sv[4 * q + 2], sv[4 * q + 3]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(rfull + rt);
+      store_chunk(c, threadIdx.x + 128);  // waits for the other stage warps' rows
+    }
+  } else if (warp < 8) {
+    // ---------------------------------------------------------- store warps
+    mbar_wait(qfull, 0);  // row starts staged
+    for (uint32_t c = 0; c < nch; ++c) store_chunk(c, threadIdx.x - 128);
+  } else if (warp == 8) {
+    // ---------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t id_s = idesc_tf32(kChunkCols, false);
+      mbar_wait(qfull, 0);
+      tc_fence_after();
+      for (uint32_t c = 0; c < nch; ++c) {
+        const uint32_t ds = c % C::NB, b = c % C::NS;
+        if (c >= uint32_t(C::NS)) mbar_wait(sempty + b, ((c / C::NS) - 1u) & 1u);
+        mbar_wait(bfull + ds, (c / C::NB) & 1u);
+        fence_async_smem();  // cp.async (generic proxy) -> MMA (async proxy)
+        tc_fence_after();
+        const uint32_t dt = tmem + b * 32;
+#pragma unroll
+        for (uint32_t ks = 0; ks < DC / 8; ++ks) {
+          const uint32_t ko = (ks >> 2) * (kPanelRows * 128u) + (ks & 3u) * 32u;
+          const uint32_t kz = ((ks >> 2) * C::NB + ds) * C::TILE + (ks & 3u) * 32u;
+          const uint64_t q0 = umma_desc(qb + ko), z0 = umma_desc(zb + kz);
+          if constexpr (C::F32) {
+            umma_tf32(dt, q0, umma_desc(zb + C::KB * C::NB * C::TILE + kz), id_s, ks ? 1u : 0u);
+            umma_tf32(dt, umma_desc(qb + C::Q_BYTES + ko), z0, id_s, 1u);
+            umma_tf32(dt, q0, z0, id_s, 1u);
+          } else {
+            umma_tf32(dt, q0, z0, id_s, ks ? 1u : 0u);
+          }
+        }
+        umma_commit(sfull + b);
+        umma_commit(bempty + ds);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- loaders
+    const uint32_t par = warp - 9;
+    constexpr uint32_t LPR = DC / 4, RPI = 32 / LPR;
+    const uint32_t j = lane % LPR, jj = j & 7u;
+    uint32_t coln = par < nch ? pv.dcols[uint64_t(c0 + par) * kChunkCols + lane] : 0u;
+    uint64_t kn0 = par < nch ? pv.coff[c0 + par] : 0, kn1 = par < nch ? pv.coff[c0 + par + 1] : 0;
+    for (uint32_t c = par; c < nch; c += 2) {
+      const uint32_t ds = c % C::NB;
+      const uint64_t ch = c0 + c;
+      const uint32_t col = coln;
+      const uint64_t k0 = kn0, k1 = kn1;
+      if (c + 2 < nch) {
+        coln = pv.dcols[(ch + 2) * kChunkCols + lane];
+        kn0 = pv.coff[ch + 2];
+        kn1 = pv.coff[ch + 3];
+      }
+      mbar_wait(bempty + ds, ((c / C::NB) & 1u) ^ 1u);
+#pragma unroll
+      for (uint32_t t = 0; t < 32 / RPI; ++t) {
+        const uint32_t kr = t * RPI + lane / LPR;
+        const uint32_t ck = __shfl_sync(0xFFFFFFFFu, col, kr);
+        if (ck == 0xFFFFFFFFu) continue;  // padding column: its S column is never read
+        const uint64_t gofs = uint64_t(ck) * ldq + 4 * j;
+        const uint32_t zo = ((j >> 3) * C::NB + ds) * C::TILE + (kr >> 3) * 1024u + (kr & 7u) * 128u +
+                            ((jj ^ (kr & 7u)) << 4);
+        cp_async16(zb + zo, yq + gofs);
+        if constexpr (C::F32) cp_async16(zb + C::KB * C::NB * C::TILE + zo, yq1 + gofs);
+      }
+      cp_async_arrive_noinc(bfull + ds);
+      const uint32_t de = c % C::NE;
+      mbar_wait(eempty + de, ((c / C::NE) & 1u) ^ 1u);
+      if (lane == 0) {
+        const uint32_t bytes = uint32_t(k1 - k0) * 4u;  // entries padded to 4: 16-byte multiple
+        ecnt[de] = uint32_t(k1 - k0);
+        mbar_expect_tx(efull + de, bytes * (has_dval ? 2u : 1u));
+        if (bytes) {
+          bulk_load(ering + de * eslot, dpos + k0, bytes, efull + de);
+          if (has_dval) bulk_load(ering + (C::NE + de) * eslot, dval + k0, bytes, efull + de);
+        }
+      }
+    }
+    cp_async_wait<0>();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
 // y operand copies for the gathers: rows of ldq (32 / 64) floats, zero
 // padding features, z = y * inv when normalising on the fly; TF32 -> RNE,
 // FP32 -> hi / lo split.
@@ -445,6 +717,25 @@ bool launch_sd_dense(const PanelView& v, uint64_t P, uint32_t max_entries, const
   return true;
 }
 
+template <int DC, int PREC>
+bool launch_sd_dense2(const PanelView& v, uint64_t P, uint32_t max_entries, const uint32_t* dpos,
+                      const uint64_t* np, const float* x, uint64_t ldx, uint64_t d, uint64_t ro, const float* inv,
+                      const float* yq, const float* yq1, uint64_t ldq, const float* dval,
+                      const float* ev, float scale, float* out, cudaStream_t s) {
+  using C = Sd2Cfg<DC, PREC>;
+  const uint32_t eslot = (max_entries + 3) / 4 * 16;
+  const uint32_t smem = C::smem_bytes(eslot, dval != nullptr);
+  if (smem > 227u * 1024u) return false;
+  once_per_device(reinterpret_cast<const void*>(&sddmm_dense2_kernel<DC, PREC>), [] {
+    cudaFuncSetAttribute(sddmm_dense2_kernel<DC, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(227u * 1024u));
+  });
+  sddmm_dense2_kernel<DC, PREC><<<unsigned(P), kSdThreads, smem, s>>>(
+      v, dpos, np, eslot, x, ldx, d, ro, inv, yq, yq1, ldq, dval, ev, scale, out);
+  CU_LAUNCH("sddmm_dense2_kernel");
+  return true;
+}
+
 inline unsigned sd_grid(uint64_t n, unsigned block, unsigned cap = 148u * 32u) {
   const uint64_t g = (n + block - 1) / block;
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(g, cap)));
@@ -503,7 +794,25 @@ bool sddmm_panel_launch(const sgtk_graph* g, const float* x, uint64_t ldx, const
     const uint16_t* rowoff = pn.rowoff->as<uint16_t>();
     const uint64_t ro = g->row_offset;
     const uint32_t me = pn.max_chunk_entries;
-    if (pn.n_chunks && prec == SGTK_FP32) {
+    // direct form when every entry's CSR position fits (Panels::dpos) and its
+    // entry ring fits; SGTK_SDDMM_DENSE=staged: the compaction form
+    static const bool staged = [] {
+      const char* e = std::getenv("SGTK_SDDMM_DENSE");
+      return e && std::string(e) == "staged";
+    }();
+    bool done = false;
+    if (pn.n_chunks && pn.dpos_ok && !staged) {
+      const uint32_t* dp = pn.dpos->as<uint32_t>();
+      const uint64_t* npg = g->np->as<uint64_t>();
+      if (prec == SGTK_FP32)
+        done = ldq == 32 ? launch_sd_dense2<32, SGTK_FP32>(v, pn.P, me, dp, npg, x, ldx, d, ro, inv_norm, yq, yq1, ldq, dval, ev, scale, out, s)
+                         : launch_sd_dense2<64, SGTK_FP32>(v, pn.P, me, dp, npg, x, ldx, d, ro, inv_norm, yq, yq1, ldq, dval, ev, scale, out, s);
+      else
+        done = ldq == 32 ? launch_sd_dense2<32, SGTK_TF32>(v, pn.P, me, dp, npg, x, ldx, d, ro, inv_norm, yq, nullptr, ldq, dval, ev, scale, out, s)
+                         : launch_sd_dense2<64, SGTK_TF32>(v, pn.P, me, dp, npg, x, ldx, d, ro, inv_norm, yq, nullptr, ldq, dval, ev, scale, out, s);
+    }
+    if (done) {
+    } else if (pn.n_chunks && prec == SGTK_FP32) {
       if (ldq == 32) launch_sd_dense<32, SGTK_FP32>(v, pn.P, me, deid, rowoff, x, ldx, d, ro, inv_norm, yq, yq1, ldq, dval, ev, scale, out, s);
       else launch_sd_dense<64, SGTK_FP32>(v, pn.P, me, deid, rowoff, x, ldx, d, ro, inv_norm, yq, yq1, ldq, dval, ev, scale, out, s);
     } else if (pn.n_chunks) {
