@@ -119,15 +119,29 @@ __device__ __forceinline__ uint32_t kmaj_off(uint32_t row, uint32_t k, uint32_t 
          ((((k >> 2) & 7u) ^ (row & 7u)) << 4) + (k & 3u) * 4u;
 }
 
+template <int FPL, int PREC, bool SPLIT>
+__device__ __forceinline__ void agnn_row_item(const uint4 w, float* T, uint32_t lane, const uint2* __restrict__ sent,
+                                              const float* __restrict__ zown, const float* __restrict__ z,
+                                              uint64_t ld, const float* __restrict__ norm, uint64_t d,
+                                              uint64_t row_offset, float bl2, float off,
+                                              const float* __restrict__ opart, const float* __restrict__ lpart,
+                                              float* __restrict__ seg_o, float* __restrict__ seg_l,
+                                              float* __restrict__ osp, float* __restrict__ lsp, const AgnnNext& nx,
+                                              unsigned long long& nz);
+
+// FR (fused rows, TF32 d <= 32; opt-in, SGTK_AGNN_FUSED=1, measured slower):
+// after its dense chunks the CTA runs the sparse edges and the finalisation
+// of its own panel's rows (agnn_row_item over the panel's items, all 12
+// warps, tiles in the idle gather rings).
 // TG: the loaders gather the chunk's z and h rows with TMA tile::gather4
 // (4 rows per instruction, swizzled by the tensor maps tmz / tmh straight into
 // the UMMA operand layouts, padding columns zero-filled as out-of-bounds rows)
 // instead of cp.async; TF32 only.
 #ifdef SGTK_DENSE_MAXREG
-template <int DC, int PREC, bool TG>
+template <int DC, int PREC, bool TG, bool FR>
 __global__ void __launch_bounds__(kAgnnThreads) __maxnreg__((DC == 32 && PREC != SGTK_FP32) ? SGTK_DENSE_MAXREG : 168)
 #else
-template <int DC, int PREC, bool TG>
+template <int DC, int PREC, bool TG, bool FR>
 __global__ void __launch_bounds__(kAgnnThreads, (DC == 32 && PREC != SGTK_FP32) ? 2 : 1)
 #endif
 agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const float* __restrict__ z,
@@ -135,9 +149,13 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
                   const float* __restrict__ h1, uint64_t ld, uint64_t d, uint64_t row_offset,
                   float beta, float* __restrict__ opart, float* __restrict__ lpart,
                   long long* __restrict__ trace, const __grid_constant__ CUtensorMap tmz,
-                  const __grid_constant__ CUtensorMap tmh) {
+                  const __grid_constant__ CUtensorMap tmh, const uint4* __restrict__ items,
+                  const uint2* __restrict__ sent, float* __restrict__ seg_o, float* __restrict__ seg_l,
+                  const AgnnNext nx) {
   using C = AgnnCfg<DC, PREC>;
   static_assert(!TG || !C::F32, "TMA gathers: TF32 operands only");
+  static_assert(!FR || (!C::F32 && DC == 32), "fused rows: TF32, d <= 32");
+  static_assert(!FR || (kAgnnThreads / 32) * 33 * (DC + 4) * 4 <= C::M_OFF - C::Z_OFF, "row tiles fit the rings");
   auto mark = [&](uint32_t c, int ev) {
 #ifdef SGTK_TRACE  // pipeline event trace (tools/panel_debug.py); compiled out by default
     if (trace && blockIdx.x < 4 && c < 256) trace[((uint64_t(blockIdx.x) * 256 + c) * 8) + ev] = clock64();
@@ -506,6 +524,17 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
   }
+  if constexpr (FR) {
+    // the panel's (O, l) partials are in opart / lpart (written by the
+    // accumulator warps before the barrier); every MMA retired and the
+    // loaders drained, so the gather rings hold the row tiles
+    float* T = reinterpret_cast<float*>(smem + C::Z_OFF) + warp * 33 * (DC + 4);
+    unsigned long long nz = 0;
+    for (uint32_t it = pv.paitem[p] + warp; it < pv.paitem[p + 1]; it += kAgnnThreads / 32)
+      agnn_row_item<1, PREC, false>(items[it], T, lane, sent, zraw, h, ld, nullptr, d, row_offset, bl2, off, opart,
+                                    lpart, seg_o, seg_l, nullptr, nullptr, nx, nz);
+    if (nx.zeros && lane == 0 && nz) atomicAdd(nx.zeros, nz);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -593,6 +622,122 @@ __device__ __forceinline__ void agnn_finalize(uint64_t r, const float (&o)[FPL],
 #ifndef SGTK_ROWS_MINB
 #define SGTK_ROWS_MINB 5
 #endif
+// One AGNN item (a row's sparse edges, or a hub-row segment) by one warp
+// over its smem tile T (33 rows x (DC + 4) floats): see agnn_rows_kernel.
+template <int FPL, int PREC, bool SPLIT>
+__device__ __forceinline__ void agnn_row_item(const uint4 w, float* T, uint32_t lane, const uint2* __restrict__ sent,
+                                              const float* __restrict__ zown, const float* __restrict__ z,
+                                              uint64_t ld, const float* __restrict__ norm, uint64_t d,
+                                              uint64_t row_offset, float bl2, float off,
+                                              const float* __restrict__ opart, const float* __restrict__ lpart,
+                                              float* __restrict__ seg_o, float* __restrict__ seg_l,
+                                              float* __restrict__ osp, float* __restrict__ lsp, const AgnnNext& nx,
+                                              unsigned long long& nz) {
+  constexpr int DC = 32 * FPL;
+  constexpr int TS = DC + 4;
+  const uint32_t tb = smem_u32(T);
+  const uint64_t f = uint64_t(lane) * FPL;
+  const int fv = f >= d ? 0 : (d - f >= uint64_t(FPL) ? FPL : int(d - f));
+  const uint64_t r = w.x;
+  const bool direct = w.w == 0xFFFFFFFFu;
+  const uint32_t c_first = w.y < w.z && lane < min(32u, w.z - w.y) ? sent[w.y + lane].x : 0u;
+  // z of the row -> tile row 32 (read back as a broadcast by every lane;
+  // lands with the first batch's gathers); padding features are zeros
+  if (w.y < w.z && lane < uint32_t(DC / 4))
+    cp_async16(tb + (32 * TS + 4 * lane) * 4, zown + (row_offset + r) * ld + 4 * lane);
+  float o[FPL], lpp = 0.0f;
+#pragma unroll
+  for (int i = 0; i < FPL; ++i) o[i] = (!SPLIT && direct && i < fv) ? opart[r * DC + f + i] : 0.0f;
+  const float l0 = (!SPLIT && direct) ? lpart[r] : 0.0f;
+  uint32_t col = c_first;
+  for (uint32_t e = w.y; e < w.z; e += 32) {
+    const uint32_t cnt = min(32u, w.z - e);
+    const uint32_t col_next = e + 32 < w.z && lane < min(32u, w.z - e - 32) ? sent[e + 32 + lane].x : 0u;
+    {  // cooperative, coalesced gather of the batch's z rows into the tile
+      constexpr uint32_t LPR = DC / 4, RPI = 32 / LPR;
+      const uint32_t j = lane % LPR;
+#pragma unroll
+      for (uint32_t t = 0; t < 32 / RPI; ++t) {
+        const uint32_t u = t * RPI + lane / LPR;
+        const uint32_t cu = __shfl_sync(0xFFFFFFFFu, col, u);
+        if (u < cnt) cp_async16(tb + (u * TS + 4 * j) * 4, z + uint64_t(cu) * ld + 4 * j);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncwarp();
+    }
+    float cf_l = 0.0f;
+    if (lane < cnt) {
+      // dot and |h|^2 as two interleaved partial sums each on the paired
+      // FFMA2 (even / odd features), combined at the end: half the issues
+      // (TF32; FP32 keeps the scalar chain, measured faster there)
+      float s = 0.0f, n2 = 0.0f;
+      if constexpr (PREC == SGTK_TF32) {
+        float2 s2 = make_float2(0.0f, 0.0f), n22 = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int k = 0; k < DC / 4; ++k) {
+          const float4 v = ld_shared_f4(tb + (lane * TS + 4 * k) * 4);
+          const float4 q = ld_shared_f4(tb + (32 * TS + 4 * k) * 4);
+          const float2 vlo = make_float2(v.x, v.y), vhi = make_float2(v.z, v.w);
+          s2 = __ffma2_rn(make_float2(q.x, q.y), vlo, s2);
+          s2 = __ffma2_rn(make_float2(q.z, q.w), vhi, s2);
+          n22 = __ffma2_rn(vlo, vlo, n22);
+          n22 = __ffma2_rn(vhi, vhi, n22);
+        }
+        s = s2.x + s2.y;
+        n2 = n22.x + n22.y;
+      } else {
+#pragma unroll
+        for (int k = 0; k < DC / 4; ++k) {
+          const float4 v = ld_shared_f4(tb + (lane * TS + 4 * k) * 4);
+          const float4 q = ld_shared_f4(tb + (32 * TS + 4 * k) * 4);
+          s = fmaf(q.x, v.x, s);
+          s = fmaf(q.y, v.y, s);
+          s = fmaf(q.z, v.z, s);
+          s = fmaf(q.w, v.w, s);
+        }
+      }
+      if constexpr (PREC == SGTK_TF32) {
+        // T holds hq_col = tf32(h_col): z_col = h_col / |h_col| on the fly
+        // (no norm gather); sddmm TF32 rounds the dot (tile_exec.cpp:386)
+        s = tf32_rne(n2 > 0.0f ? s * rsqrtf(n2) : 0.0f);
+      }
+      float pe = ex2_approx(fmaf(s, bl2, -off));
+      if constexpr (PREC == SGTK_TF32) {
+        pe = __uint_as_float(tf32_op(pe));
+        cf_l = pe;
+      } else {
+        cf_l = pe * __ldg(norm + col);
+      }
+      lpp += pe;
+    }
+#pragma unroll 8
+    for (uint32_t u = 0; u < cnt; ++u) {
+      const float cf = __shfl_sync(0xFFFFFFFFu, cf_l, u);
+#pragma unroll
+      for (int i = 0; i < FPL; ++i) o[i] = fmaf(cf, T[u * TS + lane * FPL + i], o[i]);
+    }
+    __syncwarp();
+    col = col_next;
+  }
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) lpp += __shfl_xor_sync(0xFFFFFFFFu, lpp, o2);
+  const float l = l0 + lpp;
+  if (direct && SPLIT) {  // sparse partial; agnn_final_kernel combines
+#pragma unroll
+    for (int i = 0; i < FPL; ++i)
+      if (i < fv) osp[r * DC + f + i] = o[i];
+    if (lane == 0) lsp[r] = l;
+  } else if (direct) {
+    agnn_finalize<FPL, PREC>(r, o, l, lane, fv, nx, nz);
+  } else {
+#pragma unroll
+    for (int i = 0; i < FPL; ++i)
+      if (i < fv) seg_o[uint64_t(w.w) * DC + f + i] = o[i];
+    if (lane == 0) seg_l[w.w] = l;
+  }
+}
+
 #ifndef SGTK_ROWS_WARPS
 #define SGTK_ROWS_WARPS 2
 #endif
@@ -613,114 +758,13 @@ agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2*
   __shared__ __align__(16) float tile[FPL == 1 ? kRowsWarps1 : kRowsWarps2][33 * TS];  // 32 z_col rows + z_row
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float* T = tile[wib];
-  const uint32_t tb = smem_u32(T);
   const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  const uint64_t f = uint64_t(lane) * FPL;
-  const int fv = f >= d ? 0 : (d - f >= uint64_t(FPL) ? FPL : int(d - f));
   const float bl2 = beta * 1.4426950408889634f, off = fabsf(beta) * 1.4426950408889634f;
   unsigned long long nz = 0;
-  for (uint64_t it = warp; it < n_items; it += nw) {
-    const uint4 w = items[it];
-    const uint64_t r = w.x;
-    const bool direct = w.w == 0xFFFFFFFFu;
-    const uint32_t c_first = w.y < w.z && lane < min(32u, w.z - w.y) ? sent[w.y + lane].x : 0u;
-    // z of the row -> tile row 32 (read back as a broadcast by every lane;
-    // lands with the first batch's gathers); padding features are zeros
-    if (w.y < w.z && lane < uint32_t(DC / 4))
-      cp_async16(tb + (32 * TS + 4 * lane) * 4, zown + (row_offset + r) * ld + 4 * lane);
-    float o[FPL], lpp = 0.0f;
-#pragma unroll
-    for (int i = 0; i < FPL; ++i) o[i] = (!SPLIT && direct && i < fv) ? opart[r * DC + f + i] : 0.0f;
-    const float l0 = (!SPLIT && direct) ? lpart[r] : 0.0f;
-    uint32_t col = c_first;
-    for (uint32_t e = w.y; e < w.z; e += 32) {
-      const uint32_t cnt = min(32u, w.z - e);
-      const uint32_t col_next = e + 32 < w.z && lane < min(32u, w.z - e - 32) ? sent[e + 32 + lane].x : 0u;
-      {  // cooperative, coalesced gather of the batch's z rows into the tile
-        constexpr uint32_t LPR = DC / 4, RPI = 32 / LPR;
-        const uint32_t j = lane % LPR;
-#pragma unroll
-        for (uint32_t t = 0; t < 32 / RPI; ++t) {
-          const uint32_t u = t * RPI + lane / LPR;
-          const uint32_t cu = __shfl_sync(0xFFFFFFFFu, col, u);
-          if (u < cnt) cp_async16(tb + (u * TS + 4 * j) * 4, z + uint64_t(cu) * ld + 4 * j);
-        }
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncwarp();
-      }
-      float cf_l = 0.0f;
-      if (lane < cnt) {
-        // dot and |h|^2 as two interleaved partial sums each on the paired
-        // FFMA2 (even / odd features), combined at the end: half the issues
-        // (TF32; FP32 keeps the scalar chain, measured faster there)
-        float s = 0.0f, n2 = 0.0f;
-        if constexpr (PREC == SGTK_TF32) {
-          float2 s2 = make_float2(0.0f, 0.0f), n22 = make_float2(0.0f, 0.0f);
-#pragma unroll
-          for (int k = 0; k < DC / 4; ++k) {
-            const float4 v = ld_shared_f4(tb + (lane * TS + 4 * k) * 4);
-            const float4 q = ld_shared_f4(tb + (32 * TS + 4 * k) * 4);
-            const float2 vlo = make_float2(v.x, v.y), vhi = make_float2(v.z, v.w);
-            s2 = __ffma2_rn(make_float2(q.x, q.y), vlo, s2);
-            s2 = __ffma2_rn(make_float2(q.z, q.w), vhi, s2);
-            n22 = __ffma2_rn(vlo, vlo, n22);
-            n22 = __ffma2_rn(vhi, vhi, n22);
-          }
-          s = s2.x + s2.y;
-          n2 = n22.x + n22.y;
-        } else {
-#pragma unroll
-          for (int k = 0; k < DC / 4; ++k) {
-            const float4 v = ld_shared_f4(tb + (lane * TS + 4 * k) * 4);
-            const float4 q = ld_shared_f4(tb + (32 * TS + 4 * k) * 4);
-            s = fmaf(q.x, v.x, s);
-            s = fmaf(q.y, v.y, s);
-            s = fmaf(q.z, v.z, s);
-            s = fmaf(q.w, v.w, s);
-          }
-        }
-        if constexpr (PREC == SGTK_TF32) {
-          // T holds hq_col = tf32(h_col): z_col = h_col / |h_col| on the fly
-          // (no norm gather); sddmm TF32 rounds the dot (tile_exec.cpp:386)
-          s = tf32_rne(n2 > 0.0f ? s * rsqrtf(n2) : 0.0f);
-        }
-        float pe = ex2_approx(fmaf(s, bl2, -off));
-        if constexpr (PREC == SGTK_TF32) {
-          pe = __uint_as_float(tf32_op(pe));
-          cf_l = pe;
-        } else {
-          cf_l = pe * __ldg(norm + col);
-        }
-        lpp += pe;
-      }
-#pragma unroll 8
-      for (uint32_t u = 0; u < cnt; ++u) {
-        const float cf = __shfl_sync(0xFFFFFFFFu, cf_l, u);
-#pragma unroll
-        for (int i = 0; i < FPL; ++i) o[i] = fmaf(cf, T[u * TS + lane * FPL + i], o[i]);
-      }
-      __syncwarp();
-      col = col_next;
-    }
-#pragma unroll
-    for (int o2 = 16; o2 > 0; o2 >>= 1) lpp += __shfl_xor_sync(0xFFFFFFFFu, lpp, o2);
-    const float l = l0 + lpp;
-    if (direct && SPLIT) {  // sparse partial; agnn_final_kernel combines
-#pragma unroll
-      for (int i = 0; i < FPL; ++i)
-        if (i < fv) osp[r * DC + f + i] = o[i];
-      if (lane == 0) lsp[r] = l;
-    } else if (direct) {
-      agnn_finalize<FPL, PREC>(r, o, l, lane, fv, nx, nz);
-    } else {
-#pragma unroll
-      for (int i = 0; i < FPL; ++i)
-        if (i < fv) seg_o[uint64_t(w.w) * DC + f + i] = o[i];
-      if (lane == 0) seg_l[w.w] = l;
-    }
-  }
+  for (uint64_t it = warp; it < n_items; it += nw)
+    agnn_row_item<FPL, PREC, SPLIT>(items[it], T, lane, sent, zown, z, ld, norm, d, row_offset, bl2, off, opart,
+                                    lpart, seg_o, seg_l, osp, lsp, nx, nz);
   if (nx.zeros && lane == 0 && nz) atomicAdd(nx.zeros, nz);
 }
 
@@ -949,7 +993,8 @@ template <int DC, int PREC>
 void launch_agnn_dense(const PanelView& v, uint64_t P, const float* zraw, const float* zq, const float* zq1,
                        const float* hq, const float* hq1, uint64_t ldq, uint64_t d,
                        uint64_t row_offset, float beta, float* opart, float* lpart, uint64_t table_rows,
-                       cudaStream_t s) {
+                       cudaStream_t s, const Panels* fpn = nullptr, float* seg_o = nullptr,
+                       float* seg_l = nullptr, const AgnnNext* fnx = nullptr) {
   using C = AgnnCfg<DC, PREC>;
   // SGTK_AGNN_DENSE_SMEM (bytes): pad the dense kernel's shared memory, e.g.
   // to hold one CTA per SM and leave room for the concurrent CUDA-core kernel
@@ -958,11 +1003,14 @@ void launch_agnn_dense(const PanelView& v, uint64_t P, const float* zraw, const 
     return e ? uint32_t(std::atoi(e)) : 0u;
   }();
   const uint32_t smem = std::max<uint32_t>(C::SMEM, std::min<uint32_t>(pad, 227u * 1024u));
-  once_per_device(reinterpret_cast<const void*>(&agnn_dense_kernel<DC, PREC, false>), [] {
-    cudaFuncSetAttribute(agnn_dense_kernel<DC, PREC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  constexpr bool kFR = PREC != SGTK_FP32 && DC == 32;
+  once_per_device(reinterpret_cast<const void*>(&agnn_dense_kernel<DC, PREC, false, false>), [] {
+    cudaFuncSetAttribute(agnn_dense_kernel<DC, PREC, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(227u * 1024u));
-    cudaFuncSetAttribute(agnn_dense_kernel<DC, PREC, PREC != SGTK_FP32>,
+    cudaFuncSetAttribute(agnn_dense_kernel<DC, PREC, PREC != SGTK_FP32, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(227u * 1024u));
+    cudaFuncSetAttribute(agnn_dense_kernel<DC, PREC, false, kFR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(227u * 1024u));
   });
   // SGTK_AGNN_GATHER=tma: TMA tile::gather4 instead of cp.async gathers
   // (measured neutral at C4: the gathers are not what bounds a chunk, and the
@@ -986,12 +1034,19 @@ void launch_agnn_dense(const PanelView& v, uint64_t P, const float* zraw, const 
     }
     return t;
   }();
-  if (tg)
-    agnn_dense_kernel<DC, PREC, PREC != SGTK_FP32><<<unsigned(P), kAgnnThreads, smem, s>>>(
-        v, zraw, zq, zq1, hq, hq1, ldq, d, row_offset, beta, opart, lpart, trace, tmz, tmh);
+  const AgnnNext nx0{};
+  if (fpn && kFR)
+    agnn_dense_kernel<DC, PREC, false, kFR><<<unsigned(P), kAgnnThreads, smem, s>>>(
+        v, zraw, zq, zq1, hq, hq1, ldq, d, row_offset, beta, opart, lpart, trace, tmz, tmh,
+        fpn->aitems->as<uint4>(), fpn->sent->as<uint2>(), seg_o, seg_l, *fnx);
+  else if (tg)
+    agnn_dense_kernel<DC, PREC, PREC != SGTK_FP32, false><<<unsigned(P), kAgnnThreads, smem, s>>>(
+        v, zraw, zq, zq1, hq, hq1, ldq, d, row_offset, beta, opart, lpart, trace, tmz, tmh, nullptr, nullptr,
+        nullptr, nullptr, nx0);
   else
-    agnn_dense_kernel<DC, PREC, false><<<unsigned(P), kAgnnThreads, smem, s>>>(
-        v, zraw, zq, zq1, hq, hq1, ldq, d, row_offset, beta, opart, lpart, trace, tmz, tmh);
+    agnn_dense_kernel<DC, PREC, false, false><<<unsigned(P), kAgnnThreads, smem, s>>>(
+        v, zraw, zq, zq1, hq, hq1, ldq, d, row_offset, beta, opart, lpart, trace, tmz, tmh, nullptr, nullptr,
+        nullptr, nullptr, nx0);
   if (trace) {
     std::vector<long long> hb(4 * 256 * 8);
     cudaMemcpy(hb.data(), trace, hb.size() * 8, cudaMemcpyDeviceToHost);
@@ -1081,6 +1136,25 @@ void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, cons
   };
   if (dbg == 1) {
     dense(s);
+    return;
+  }
+  // SGTK_AGNN_FUSED=1: the fused form (dense chunks, then the panel's sparse
+  // rows in the same CTA) -- measured slower at C4 (0.645 against 0.543 ms per
+  // layer): a CTA in its sparse phase holds the shared memory and warp slots a
+  // dense CTA needs, and 24 warps per SM hide less gather latency than the
+  // concurrent sparse kernel's 40
+  static const bool unfused = [] {
+    const char* e = std::getenv("SGTK_AGNN_FUSED");
+    return !(e && std::string(e) == "1");
+  }();
+  if (prec == SGTK_TF32 && ldq == 32 && !unfused && !serial && dbg == 0 && pn.paitem) {
+    launch_agnn_dense<32, SGTK_TF32>(v, pn.P, zq, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart,
+                                     g->n_cols, s, &pn, seg_o, seg_l, &nx);
+    if (pn.n_long) {
+      agnn_long_rows_kernel<1, SGTK_TF32><<<blocks_for(pn.n_long * 32), 256, 0, s>>>(
+          pn.lrows->as<uint4>(), pn.n_long, d, opart, lpart, seg_o, seg_l, nx);
+      CU_LAUNCH("agnn_long_rows_kernel");
+    }
     return;
   }
   if (dbg == 2) {

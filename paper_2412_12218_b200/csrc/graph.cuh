@@ -84,6 +84,7 @@ struct Panels {
   // as the same segments as above
   uint64_t n_aitems = 0;
   std::shared_ptr<DevBuf> aitems;  // uint4[n_aitems]
+  std::shared_ptr<DevBuf> paitem;  // u32[P+1] first aitem of panel p (rows in order: every row is an item)
 };
 
 struct PanelView {
@@ -96,6 +97,7 @@ struct PanelView {
   const uint32_t* sptr;
   const uint2* sent;
   const uint32_t* dmask;
+  const uint32_t* paitem;
 };
 
 // POD view handed to kernels.

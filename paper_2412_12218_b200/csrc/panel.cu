@@ -989,6 +989,17 @@ void launch_sparse(const Panels& pn, const uint2* sent, const float* x, uint64_t
 
 // ---------------------------------------------------------------- builder
 namespace {
+// First AGNN item of each panel (aitems hold every row, in row order, hub
+// rows as consecutive segments).
+void build_paitem(Panels& pn, cudaStream_t s) {
+  std::vector<uint4> it = dl<uint4>(pn.aitems->p, pn.n_aitems, s);
+  std::vector<uint32_t> pa(pn.P + 1, uint32_t(pn.n_aitems));
+  for (uint64_t i = pn.n_aitems; i-- > 0;) pa[it[i].x / kPanelRows] = uint32_t(i);
+  for (uint64_t q = pn.P; q-- > 0;) pa[q] = std::min(pa[q], pa[q + 1]);
+  pn.paitem = ul(pa.data(), pa.size(), s);
+  CU(cudaStreamSynchronize(s));
+}
+
 void build_dpos(const sgtk_graph& g, Panels& pn, cudaStream_t s) {
   pn.dpos = std::make_shared<DevBuf>(std::max<uint64_t>(pn.n_dent, 4) * 4);
   pn.dpos_ok = false;
@@ -1140,6 +1151,7 @@ std::shared_ptr<Panels> build_panel_format(sgtk_graph& g, uint32_t dense_min, cu
   pn->lrows = ul(lrows.data(), lrows.size(), s);
   CU(cudaStreamSynchronize(s));
   build_dpos(g, *pn, s);
+  build_paitem(*pn, s);
   return pn;
 }
 }  // namespace
@@ -1276,6 +1288,8 @@ bool load_panel_section(sgtk_graph& g, const std::string& path, cudaStream_t s) 
       if (std::fgetc(f) != EOF) raise(SGTK_ERR_IO, "SGP1: trailing bytes");
       build_dpos(g, *a, s);
       build_dpos(g, *b, s);
+      build_paitem(*a, s);
+      build_paitem(*b, s);
       g.panels = a;
       g.panels32 = b;
       g.panels_loaded = true;
@@ -1322,6 +1336,7 @@ PanelView panel_view(const sgtk_graph* g, uint64_t d) {
   v.sptr = pn.sptr->as<uint32_t>();
   v.sent = pn.sent->as<uint2>();
   v.dmask = pn.dmask->as<uint32_t>();
+  v.paitem = pn.paitem ? pn.paitem->as<uint32_t>() : nullptr;
   return v;
 }
 
