@@ -70,7 +70,10 @@ struct AgnnCfg {
   // P tile, no P slot to wait for; three S buffers instead of two + P slots.
   static constexpr bool PT = !F32 && DC == 32;
   static constexpr int NSB = PT ? 3 : 2;                   // S buffers (chunk pairs)
-  static constexpr int NB = F32 ? (DC == 32 ? 4 : 2) : (PT ? 8 : 6);  // gather ring (even: S pairs)
+#ifndef SGTK_AGNN_NB
+#define SGTK_AGNN_NB 10
+#endif
+  static constexpr int NB = F32 ? (DC == 32 ? 4 : 2) : (PT ? SGTK_AGNN_NB : 6);  // gather ring (even: S pairs)
   // P slots in smem; PT: pfull barriers only, one per chunk the softmax can
   // run ahead of the MMA issuer (S can be up to NSB groups ahead)
   static constexpr int NP = PT ? 8 : 2;
