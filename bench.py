@@ -997,7 +997,7 @@ def kernel_breakdown(args, wl, dg, g, h, D, prec, mode, flush, stream, gcn_layer
         res["sddmm"] = ev_time(sddmm)
         Bs = 8 * (N + 1) + 4 * E + 4 * N * d + 4 * E
         extra["roofline_sddmm"] = {
-            "bound": "hbm", "kernel": "sddmm_hybrid (sddmm_dense_kernel tcgen05 + sddmm_sparse_kernel)",
+            "bound": "hbm", "kernel": "sddmm_hybrid (sddmm_dense2_kernel tcgen05 + sddmm_sparse_kernel)",
             "achieved": round(Bs / (res["sddmm"] * 1e-3) / 1e9, 1), "unit": "GB/s",
             "algorithmic_bytes": int(Bs), "formula": "8(N+1) + 4E + s*N*d + 4E (SURVEY §8d B_sddmm, s=4)",
             "kernel_ms": round(res["sddmm"], 4)}

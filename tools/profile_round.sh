@@ -12,7 +12,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     --log-file gpurun_out/launches_${tag}_gcn.csv python bench.py --steps 2 --warmup 3 --no-cpu \
     --workload proteins-gcn > /dev/null 2>&1
 ncu --set full --metrics $TC_METRICS --clock-control none --import-source on \
-    -k regex:"agnn_dense_kernel|agnn_rows_kernel|spmm_panel_kernel|sparse_rows_kernel|gemm_tc05_kernel|sddmm_dense_kernel|sddmm_sparse_kernel" -c 8 \
+    -k regex:"agnn_dense_kernel|agnn_rows_kernel|spmm_panel_kernel|sparse_rows_kernel|gemm_tc05_kernel|sddmm_dense2_kernel|sddmm_sparse_kernel" -c 8 \
     -o gpurun_out/prof_${tag} python bench.py --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1
 ncu --set full --metrics $TC_METRICS --clock-control none --import-source on -k regex:"spmm_panel_kernel|sparse_rows_kernel" -c 2 \
     -o gpurun_out/prof_${tag}_gcn python bench.py --steps 1 --warmup 3 --no-cpu --workload proteins-gcn > /dev/null 2>&1
