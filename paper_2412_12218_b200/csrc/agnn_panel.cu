@@ -748,7 +748,7 @@ __device__ __forceinline__ void agnn_row_item(const uint4 w, float* T, uint32_t 
 constexpr int kRowsWarps1 = SGTK_ROWS_WARPS, kRowsWarps2 = SGTK_ROWS_WARPS > 1 ? SGTK_ROWS_WARPS / 2 : 1;
 template <int FPL, int PREC, bool SPLIT>
 __global__ void __launch_bounds__(FPL == 1 ? 32 * kRowsWarps1 : 32 * kRowsWarps2,
-                                  (FPL == 1 ? SGTK_ROWS_MINB : 2 * SGTK_ROWS_MINB) * 8 / SGTK_ROWS_WARPS)
+                                  std::min(32, (FPL == 1 ? SGTK_ROWS_MINB : 2 * SGTK_ROWS_MINB) * 8 / SGTK_ROWS_WARPS))
 agnn_rows_kernel(const uint4* __restrict__ items, uint64_t n_items, const uint2* __restrict__ sent,
                  const float* __restrict__ zown, const float* __restrict__ z, uint64_t ld,
                  const float* __restrict__ norm,
