@@ -47,9 +47,17 @@ namespace {
 using namespace tc05;
 
 constexpr float kMaxBeta = 40.0f;
-// 12 warps: 4 softmax, 4 accumulator, S issuer, 2 loaders, PV issuer (the
-// PV issuer is its own warp in the TF32 d = 32 configuration, see SPLIT_MMA)
-constexpr int kAgnnThreads = 384;
+// Warps: 4 softmax, 4 accumulator, NL loaders, the S issuer (+ TMEM
+// allocation), the PV issuer (its own warp in the TF32 d = 32 configuration,
+// see SPLIT_MMA).  TF32 d = 32 runs 4 loaders, one per SM sub-partition: with
+// 2 the softmax warps sharing a sub-partition with a loader fell ~800 cycles
+// per chunk behind the other two (pipeline trace), and the slowest softmax
+// warp paces the chunk loop (PV needs all four P quarters).
+#ifndef SGTK_AGNN_LOADERS
+#define SGTK_AGNN_LOADERS 4
+#endif
+constexpr int agnn_loaders(int DC, int PREC) { return (DC == 32 && PREC != SGTK_FP32) ? SGTK_AGNN_LOADERS : 2; }
+constexpr int agnn_threads(int DC, int PREC) { return 32 * (10 + agnn_loaders(DC, PREC)); }
 
 template <int DC, int PREC>
 struct AgnnCfg {
@@ -142,10 +150,10 @@ __device__ __forceinline__ void agnn_row_item(const uint4 w, float* T, uint32_t 
 // instead of cp.async; TF32 only.
 #ifdef SGTK_DENSE_MAXREG
 template <int DC, int PREC, bool TG, bool FR>
-__global__ void __launch_bounds__(kAgnnThreads) __maxnreg__((DC == 32 && PREC != SGTK_FP32) ? SGTK_DENSE_MAXREG : 168)
+__global__ void __launch_bounds__(agnn_threads(DC, PREC)) __maxnreg__((DC == 32 && PREC != SGTK_FP32) ? SGTK_DENSE_MAXREG : 168)
 #else
 template <int DC, int PREC, bool TG, bool FR>
-__global__ void __launch_bounds__(kAgnnThreads, (DC == 32 && PREC != SGTK_FP32) ? 2 : 1)
+__global__ void __launch_bounds__(agnn_threads(DC, PREC), (DC == 32 && PREC != SGTK_FP32) ? 2 : 1)
 #endif
 agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const float* __restrict__ z,
                   const float* __restrict__ z1, const float* __restrict__ h,
@@ -158,7 +166,10 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
   using C = AgnnCfg<DC, PREC>;
   static_assert(!TG || !C::F32, "TMA gathers: TF32 operands only");
   static_assert(!FR || (!C::F32 && DC == 32), "fused rows: TF32, d <= 32");
-  static_assert(!FR || (kAgnnThreads / 32) * 33 * (DC + 4) * 4 <= C::M_OFF - C::Z_OFF, "row tiles fit the rings");
+  constexpr uint32_t NL = agnn_loaders(DC, PREC), IW = 8 + NL;  // loaders: warps 8..IW-1; issuers IW, IW+1
+  constexpr uint32_t NW = agnn_threads(DC, PREC) / 32;
+  constexpr uint32_t FRW = (C::M_OFF - C::Z_OFF) / (33 * (DC + 4) * 4) < NW ? (C::M_OFF - C::Z_OFF) / (33 * (DC + 4) * 4) : NW;
+  static_assert(!FR || FRW >= 8, "row tiles fit the rings");
   auto mark = [&](uint32_t c, int ev) {
 #ifdef SGTK_TRACE  // pipeline event trace (tools/panel_debug.py); compiled out by default
     if (trace && blockIdx.x < 4 && c < 256) trace[((uint64_t(blockIdx.x) * 256 + c) * 8) + ev] = clock64();
@@ -203,7 +214,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
     }
     mbar_init_fence();
   }
-  if (warp == 8) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == IW) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -358,9 +369,9 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       }
       if (grow < pv.n_rows) lpart[grow] = lbuf[r];
     }
-  } else if (warp == 8 || warp == 11) {
+  } else if (warp == IW || warp == IW + 1) {
     // ------------------------------------------------------------ MMA issuers
-    if (lane == 0 && nch && (warp == 8 || C::SPLIT_MMA)) {
+    if (lane == 0 && nch && (warp == IW || C::SPLIT_MMA)) {
       constexpr uint32_t id_s = idesc_tf32(32 * C::SG, false);  // N = a S group's columns, B K-major
       constexpr uint32_t id_o = idesc_tf32(DC, true);   // N = DC features, B MN-major
       const uint32_t qb = smem_u32(qs), pb = smem_u32(ps);
@@ -429,7 +440,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
         if ((c % C::FOLD) == C::FOLD - 1 || c + 1 == nch) umma_commit(accfull + buf);
       };
       if constexpr (C::SPLIT_MMA) {
-        if (warp == 8) {
+        if (warp == IW) {
           for (uint32_t g = 0; g * C::SG < nch; ++g) issue_s(g);
         } else {
           for (uint32_t c = 0; c < nch; ++c) issue_pv(c);
@@ -452,22 +463,22 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       }
     }
   } else {
-    // ------------------------------------------------------------ loaders (warps 9, 10)
+    // ------------------------------------------------------------ loaders (warps 8 .. IW - 1)
     // warp 9 takes even chunks, warp 10 odd ones.  Per chunk: 32 z rows
     // (K-major SWIZZLE_128B B of S), 32 h rows (MN-major SWIZZLE_128B_BASE32B
     // B of PV), 128 row masks; completion via cp.async.mbarrier.arrive.noinc.
-    const uint32_t par = warp - 9;
+    const uint32_t par = warp - 8;
     // column ids one chunk ahead: the global load stays off the slot-free ->
     // gather-issue path
     uint32_t coln = par < nch ? pv.dcols[uint64_t(c0 + par) * kChunkCols + lane] : 0u;
-    for (uint32_t c = par; c < nch; c += 2) {
+    for (uint32_t c = par; c < nch; c += NL) {
       const uint32_t ds = c % C::NB;
 #ifdef SGTK_AGNN_GMASK  // timing experiment only: gather a small hot set of rows
       const uint32_t col = coln == 0xFFFFFFFFu ? coln : (coln & SGTK_AGNN_GMASK);
 #else
       const uint32_t col = coln;
 #endif
-      coln = c + 2 < nch ? pv.dcols[uint64_t(c0 + c + 2) * kChunkCols + lane] : 0u;
+      coln = c + NL < nch ? pv.dcols[uint64_t(c0 + c + NL) * kChunkCols + lane] : 0u;
       mbar_wait(bempty + ds, ((c / C::NB) & 1u) ^ 1u);
       if (lane == 0) mark(c, 4);
       const uint32_t ht = hr_s + ds * C::T_BYTES;
@@ -523,7 +534,7 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == IW) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
   }
@@ -533,7 +544,8 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
     // loaders drained, so the gather rings hold the row tiles
     float* T = reinterpret_cast<float*>(smem + C::Z_OFF) + warp * 33 * (DC + 4);
     unsigned long long nz = 0;
-    for (uint32_t it = pv.paitem[p] + warp; it < pv.paitem[p + 1]; it += kAgnnThreads / 32)
+    if (warp < FRW)
+    for (uint32_t it = pv.paitem[p] + warp; it < pv.paitem[p + 1]; it += FRW)
       agnn_row_item<1, PREC, false>(items[it], T, lane, sent, zraw, h, ld, nullptr, d, row_offset, bl2, off, opart,
                                     lpart, seg_o, seg_l, nullptr, nullptr, nx, nz);
     if (nx.zeros && lane == 0 && nz) atomicAdd(nx.zeros, nz);
@@ -1039,15 +1051,15 @@ void launch_agnn_dense(const PanelView& v, uint64_t P, const float* zraw, const 
   }();
   const AgnnNext nx0{};
   if (fpn && kFR)
-    agnn_dense_kernel<DC, PREC, false, kFR><<<unsigned(P), kAgnnThreads, smem, s>>>(
+    agnn_dense_kernel<DC, PREC, false, kFR><<<unsigned(P), agnn_threads(DC, PREC), smem, s>>>(
         v, zraw, zq, zq1, hq, hq1, ldq, d, row_offset, beta, opart, lpart, trace, tmz, tmh,
         fpn->aitems->as<uint4>(), fpn->sent->as<uint2>(), seg_o, seg_l, *fnx);
   else if (tg)
-    agnn_dense_kernel<DC, PREC, PREC != SGTK_FP32, false><<<unsigned(P), kAgnnThreads, smem, s>>>(
+    agnn_dense_kernel<DC, PREC, PREC != SGTK_FP32, false><<<unsigned(P), agnn_threads(DC, PREC), smem, s>>>(
         v, zraw, zq, zq1, hq, hq1, ldq, d, row_offset, beta, opart, lpart, trace, tmz, tmh, nullptr, nullptr,
         nullptr, nullptr, nx0);
   else
-    agnn_dense_kernel<DC, PREC, false, false><<<unsigned(P), kAgnnThreads, smem, s>>>(
+    agnn_dense_kernel<DC, PREC, false, false><<<unsigned(P), agnn_threads(DC, PREC), smem, s>>>(
         v, zraw, zq, zq1, hq, hq1, ldq, d, row_offset, beta, opart, lpart, trace, tmz, tmh, nullptr, nullptr,
         nullptr, nullptr, nx0);
   if (trace) {
