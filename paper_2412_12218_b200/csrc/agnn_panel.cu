@@ -114,7 +114,7 @@ struct AgnnCfg {
 #ifdef SGTK_AGNN_ONE_ISSUER
   static constexpr bool SPLIT_MMA = false;
 #else
-  static constexpr bool SPLIT_MMA = PT;
+  static constexpr bool SPLIT_MMA = true;
 #endif
   static_assert(SMEM <= 227u * 1024u, "agnn panel smem");
 };
@@ -186,7 +186,9 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
   uint64_t* qfull = pfull + C::NP;                      // [1]  Q operand ready
   uint64_t* accfull = qfull + 1;                        // [NF]
   uint64_t* accempty = accfull + C::NF;                 // [NF]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + C::NF);
+  uint64_t* sempty = accempty + C::NF;                  // [NSB] S group read (P in smem: !PT)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + C::NSB);
+  static_assert((2 * C::NB + 2 * C::NSB + C::NP + 1 + 2 * C::NF) * 8 + 16 <= 512, "barriers fit below lbuf");
   float* lbuf = reinterpret_cast<float*>(smem + 512);   // [128] row sums
   uint8_t* qs = smem + C::Q_OFF;
   const uint32_t zr_s = smem_u32(smem + C::Z_OFF), hr_s = smem_u32(smem + C::H_OFF);
@@ -205,7 +207,10 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       mbar_init(bfull + i, TG ? 1 : 32);  // TG: expect_tx; else cp.async.mbarrier.arrive.noinc per lane
       mbar_init(bempty + i, 1);
     }
-    for (int i = 0; i < C::NSB; ++i) mbar_init(sfull + i, 1);
+    for (int i = 0; i < C::NSB; ++i) {
+      mbar_init(sfull + i, 1);
+      mbar_init(sempty + i, 4);
+    }
     for (int i = 0; i < C::NP; ++i) mbar_init(pfull + i, 4);
     mbar_init(qfull, 4);
     for (int i = 0; i < C::NF; ++i) {
@@ -267,6 +272,12 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
       tmem_ld_wait();
       if (warp == 0 && lane == 0) mark(c, 6);
       tc_fence_before();
+      if constexpr (!C::PT && C::SPLIT_MMA) {  // the group's S read: its TMEM buffer is free
+        if ((c % C::SG) == C::SG - 1 || c + 1 == nch) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(sempty + sb);
+        }
+      }
       // Blackwell's paired fp32 instructions (FFMA2 / FADD2) take two elements
       // per issue; same roundings and the same 4 partial sums (j % 4) as the
       // scalar form, so the results are bit-identical to it
@@ -385,6 +396,8 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
           const uint32_t cl = C::SG * (g - C::NSB) + C::SG - 1;
           mbar_wait(bempty + cl % C::NB, (cl / C::NB) & 1u);
         }
+        if (!C::PT && C::SPLIT_MMA && g >= uint32_t(C::NSB))  // the softmax read the buffer's previous S
+          mbar_wait(sempty + g % C::NSB, ((g / C::NSB) - 1u) & 1u);
         mbar_wait(bfull + c % C::NB, (c / C::NB) & 1u);
         if (C::PAIR && c + 1 < nch) mbar_wait(bfull + (c + 1) % C::NB, ((c + 1) / C::NB) & 1u);
         fence_async_smem();  // cp.async (generic proxy) -> MMA (async proxy)
