@@ -1175,7 +1175,9 @@ void agnn_panel_layer(const sgtk_graph* g, const float* z, const float* zq, cons
     const char* e = std::getenv("SGTK_AGNN_FUSED");
     return !(e && std::string(e) == "1");
   }();
-  if (prec == SGTK_TF32 && ldq == 32 && !unfused && !serial && dbg == 0 && pn.paitem) {
+  if (prec == SGTK_TF32 && ldq == 32 && !unfused && !serial && dbg == 0) {
+    ensure_paitem(pn, s);
+    v.paitem = pn.paitem->as<uint32_t>();
     launch_agnn_dense<32, SGTK_TF32>(v, pn.P, zq, zq, nullptr, hq, nullptr, ldq, d, ro, beta, opart, lpart,
                                      g->n_cols, s, &pn, seg_o, seg_l, &nx);
     if (pn.n_long) {

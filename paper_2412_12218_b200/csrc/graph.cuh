@@ -2,6 +2,7 @@
 #pragma once
 
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -67,10 +68,11 @@ struct Panels {
   std::shared_ptr<DevBuf> dmask;  // u32[n_chunks * 128] row r's edge bits in the chunk (AGNN)
   std::shared_ptr<DevBuf> rowoff; // u16[n_chunks * 128] entries of the chunk before row r (SDDMM)
   // u32[n_dent] SDDMM entry: (position in the CSR row) << 12 | panel row << 5 |
-  // chunk column (0xFFFFFFFF for padding); built with the format (not
-  // persisted); dpos_ok = every position < 2^20
+  // chunk column (0xFFFFFFFF for padding); built on the first SDDMM call
+  // (ensure_dpos; not persisted); dpos_ok = every position < 2^20
   std::shared_ptr<DevBuf> dpos;
   bool dpos_ok = false;
+  std::shared_ptr<std::once_flag> dpos_once = std::make_shared<std::once_flag>();
   std::shared_ptr<DevBuf> sptr;   // u32[n_rows+1] sparse edges of a row
   std::shared_ptr<DevBuf> sent;   // uint2[n_sparse] (column, value bits)
   std::shared_ptr<DevBuf> seid;   // u32[n_sparse] CSR edge id
@@ -84,7 +86,8 @@ struct Panels {
   // as the same segments as above
   uint64_t n_aitems = 0;
   std::shared_ptr<DevBuf> aitems;  // uint4[n_aitems]
-  std::shared_ptr<DevBuf> paitem;  // u32[P+1] first aitem of panel p (rows in order: every row is an item)
+  std::shared_ptr<DevBuf> paitem;  // u32[P+1] first aitem of panel p (rows in order; ensure_paitem)
+  std::shared_ptr<std::once_flag> paitem_once = std::make_shared<std::once_flag>();
 };
 
 struct PanelView {

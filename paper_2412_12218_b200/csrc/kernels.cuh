@@ -85,6 +85,10 @@ void agnn_input_launch(const float* x, uint64_t ldx, uint64_t rows, uint64_t d, 
                        uint64_t* zeros, cudaStream_t s);
 // The panel format an operation of width d runs on (panels32 for d <= 32).
 const Panels& panels_for(const sgtk_graph* g, uint64_t d);
+// lazily built per-format arrays (first use; thread-safe): Panels::dpos for
+// the SDDMM direct form, Panels::paitem for the fused AGNN form
+void ensure_dpos(const sgtk_graph& g, const Panels& pn, cudaStream_t s);
+void ensure_paitem(const Panels& pn, cudaStream_t s);
 PanelView panel_view(const sgtk_graph* g, uint64_t d);
 void panel_debug_set(int mode);
 int panel_debug_mode();

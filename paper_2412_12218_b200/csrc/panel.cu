@@ -1150,8 +1150,6 @@ std::shared_ptr<Panels> build_panel_format(sgtk_graph& g, uint32_t dense_min, cu
   pn->items = ul(items.data(), items.size(), s);
   pn->lrows = ul(lrows.data(), lrows.size(), s);
   CU(cudaStreamSynchronize(s));
-  build_dpos(g, *pn, s);
-  build_paitem(*pn, s);
   return pn;
 }
 }  // namespace
@@ -1286,10 +1284,6 @@ bool load_panel_section(sgtk_graph& g, const std::string& path, cudaStream_t s) 
       const uint64_t P = (g.n_rows + kPanelRows - 1) / kPanelRows;
       if (a->P != P || b->P != P) raise(SGTK_ERR_IO, "SGP1: panel count does not match the graph");
       if (std::fgetc(f) != EOF) raise(SGTK_ERR_IO, "SGP1: trailing bytes");
-      build_dpos(g, *a, s);
-      build_dpos(g, *b, s);
-      build_paitem(*a, s);
-      build_paitem(*b, s);
       g.panels = a;
       g.panels32 = b;
       g.panels_loaded = true;
@@ -1318,6 +1312,13 @@ const Panels& panels_for(const sgtk_graph* g, uint64_t d) {
     return e && std::string(e) == "2";
   }();
   return d <= 32 && g->panels32 && !f2 ? *g->panels32 : *g->panels;
+}
+
+void ensure_dpos(const sgtk_graph& g, const Panels& pn, cudaStream_t s) {
+  std::call_once(*pn.dpos_once, [&] { build_dpos(g, const_cast<Panels&>(pn), s); });
+}
+void ensure_paitem(const Panels& pn, cudaStream_t s) {
+  std::call_once(*pn.paitem_once, [&] { build_paitem(const_cast<Panels&>(pn), s); });
 }
 
 void panel_debug_set(int mode) { g_panel_debug.store(mode, std::memory_order_relaxed); }

@@ -801,6 +801,7 @@ bool sddmm_panel_launch(const sgtk_graph* g, const float* x, uint64_t ldx, const
       return e && std::string(e) == "staged";
     }();
     bool done = false;
+    if (pn.n_chunks && !staged) ensure_dpos(*g, pn, s);
     if (pn.n_chunks && pn.dpos_ok && !staged) {
       const uint32_t* dp = pn.dpos->as<uint32_t>();
       const uint64_t* npg = g->np->as<uint64_t>();
