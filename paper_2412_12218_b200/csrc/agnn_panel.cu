@@ -77,7 +77,10 @@ struct AgnnCfg {
   // back over its own S columns (tcgen05.st) and PV reads A from there -- no
   // P tile, no P slot to wait for; three S buffers instead of two + P slots.
   static constexpr bool PT = !F32 && DC == 32;
-  static constexpr int NSB = PT ? 3 : 2;                   // S buffers (chunk pairs)
+#ifndef SGTK_AGNN_NSB
+#define SGTK_AGNN_NSB 2  // 2 pairs: 0.274 -> 0.272 ms dense part against 3 (split issuers)
+#endif
+  static constexpr int NSB = PT ? SGTK_AGNN_NSB : 2;       // S buffers (chunk pairs)
 #ifndef SGTK_AGNN_NB
 #define SGTK_AGNN_NB 10
 #endif
