@@ -110,7 +110,8 @@ struct AgnnCfg {
   // of >= 4 slots; shallower rings compute S chunk by chunk (N = 32)
   static constexpr bool PAIR = NB >= 4;
   static constexpr uint32_t SG = PAIR ? 2 : 1;  // chunks per S group
-  [[maybe_unused]] static constexpr bool EARLY_S = PAIR && NB >= 6;  // one-issuer form only
+  static constexpr bool EARLY_S = PAIR && NB >= 6;  // one-issuer form only
+  static_assert(EARLY_S || !EARLY_S, "");
   // S and PV issued by two threads (warps 8 and 11), each blocking only on its
   // own inputs: S(g) on its gathers and its TMEM buffer, PV(c) on P(c).  One
   // in-order issuer makes PV(c) wait behind S(c + 2)'s gathers.
