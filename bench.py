@@ -513,7 +513,10 @@ def config_of(args, wl, g, gen):
             "step": (f"agnn_forward({wl['layers']} layers, d={wl['hidden']}, beta=1) on the whole "
                      f"graph; value = ms per layer" if wl["kind"] == "agnn" else
                      f"gcn_forward({wl['layers']} layers); value = ms per layer"),
-            "global_batch": 1, "seq_len": 0, "parallelism": f"rowwindow{args.gpus}",
+            "global_batch": 1, "seq_len": 0,
+            "parallelism": f"rowwindow{args.gpus}" + (f" x{args.overlap} overlapped sub-slices"
+                                                      if args.gpus > 1 and args.overlap > 1
+                                                      and wl["kind"] == "agnn" else ""),
             "precision": args.precision, "mode": args.mode, "locality": args.locality,
             "generator": gen, "l2": "flushed between timed steps (256 MB write)"}
 
@@ -576,7 +579,8 @@ def run_b200(args, wl):
     os.environ["SGTK_BUILD_TIMING"] = "1"  # per-stage times of the graph below
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    sl = RowSlice(g.node_pointer, g.edge_list, vals, N, rank, world)
+    chunks = args.overlap if (world > 1 and wl["kind"] == "agnn") else 1
+    sl = RowSlice(g.node_pointer, g.edge_list, vals, N, rank, world, chunks=chunks)
     torch.cuda.synchronize()
     translate_ms = (time.perf_counter() - t0) * 1e3
     os.environ.pop("SGTK_BUILD_TIMING", None)
@@ -605,7 +609,7 @@ def run_b200(args, wl):
             pi = dg.panel_info(d)
             per_call = 3 + (1 if pi["long_rows"] else 0)  # dense + rows + final (+ hub rows)
             # one input kernel per call: once per step on 1 GPU, once per layer on N
-            launches_per_step = (1 + L * per_call) if world == 1 else L * (1 + per_call)
+            launches_per_step = (1 + L * per_call) if world == 1 else L * (1 + per_call) * chunks
         else:
             split = dg_has_splits(dg, 16 if mode == 1 else 8)
             launches_per_step = L * ((2 if mode == 1 else 4) + (1 if split else 0))
@@ -856,10 +860,14 @@ def e2e_multi(wl, sl, step, x_full, h_rep, x_loc, L, args, max_over_ranks, flush
     pin_in = x_full[sl.r0:sl.r1].cpu().pin_memory()
     out0 = step()
     pin_out = torch.empty(tuple(out0.shape), dtype=torch.float32).pin_memory()
-    dst = sl.mine(h_rep) if h_rep is not None else x_loc
+    chunked = h_rep is not None and sl.chunks > 1
+    dst = None if chunked else (sl.mine(h_rep) if h_rep is not None else x_loc)
 
     def call():
-        dst.copy_(pin_in, non_blocking=True)
+        if chunked:
+            sl.write_mine(h_rep, pin_in)
+        else:
+            dst.copy_(pin_in, non_blocking=True)
         if h_rep is not None:
             sl.exchange(h_rep)
         pin_out.copy_(step(), non_blocking=True)
@@ -1165,6 +1173,9 @@ def main():
     ap.add_argument("--mode", default="auto", choices=["auto", "panel", "fused", "chain"])
     ap.add_argument("--locality", default="calibrated", choices=sorted(LOCALITY))
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--overlap", type=int, default=1,
+                    help="N > 1, AGNN: sub-slices per rank whose all-gathers overlap the next "
+                         "sub-slice's compute (distributed.RowSlice chunks)")
     ap.add_argument("--no-cuda-graph", dest="cuda_graph", action="store_false",
                     help="AGNN: time the eager calls instead of the step captured once as a "
                          "CUDA graph and replayed (the default; every kernel still runs)")

@@ -26,6 +26,16 @@ Per layer the only exchange is that all-gather:
   GCN : d_out < d_in: local h W into the replica -> all-gather -> SpMM (+ReLU)
         otherwise   : h in the replica -> all-gather -> SpMM -> local GEMM (+ReLU)
 There is no other collective on the data path.
+
+Overlap (`chunks=K > 1`, AGNN).  Each rank's rows are cut into K sub-slices
+(the partition has world*K edge-balanced ranges of whole panels; rank p owns
+ranges pK .. pK+K-1, still one contiguous row range); the replica has one
+block per range, in row order (the remap stays monotone, so every sub-slice
+keeps the global SGT structure and the outputs stay bit-identical).  A layer
+runs sub-slice 0, then, on a second stream, all-gathers every rank's chunk-0
+block into a contiguous staging buffer and scatters it into the replica's
+chunk-0 blocks while sub-slice 1 computes, and so on; the next layer waits
+for the K exchanges.  K = 1 is the layout above.
 """
 
 from __future__ import annotations
@@ -135,34 +145,50 @@ def exchange_inplace(buf: torch.Tensor, rank: int, world: int, group=None) -> No
 
 class RowSlice:
     """One rank's share of a graph: its row slice resident on this GPU, with
-    column ids in the padded-replica space (see module docstring)."""
+    column ids in the padded-replica space (see module docstring).  chunks=K
+    (AGNN) cuts it into K sub-slices whose all-gathers overlap the next one's
+    compute (`graphs`, `chunk_ranges`; `graph` is the first)."""
 
     def __init__(self, node_pointer, edge_list, values, num_nodes: int, rank: int, world: int,
-                 group=None, blk_h: int = 16, blk_w: int = 8, build_graph: bool = True):
+                 group=None, blk_h: int = 16, blk_w: int = 8, build_graph: bool = True,
+                 chunks: int = 1):
         self.n = num_nodes
         self.rank, self.world, self.group = rank, world, group
-        self.bounds = partition(node_pointer, num_nodes, world)  # whole 128-row panels
-        self.ranges = row_ranges(self.bounds, num_nodes)
+        self.chunks = K = max(1, int(chunks)) if world > 1 else 1
+        # world*K edge-balanced ranges of whole panels; rank p owns pK .. pK+K-1
+        bounds_all = partition(node_pointer, num_nodes, world * K)
+        self.ranges_all = row_ranges(bounds_all, num_nodes)
+        self.ranges = [(self.ranges_all[p * K][0], self.ranges_all[p * K + K - 1][1]) for p in range(world)]
+        self.bounds = np.array([bounds_all[p * K] for p in range(world)] + [bounds_all[-1]], np.uint64)
         self.r0, self.r1 = self.ranges[rank]
         self.rows = self.r1 - self.r0
-        self.stride = replica_stride(self.ranges) if world > 1 else num_nodes
-        self.padded_rows = self.stride * world if world > 1 else num_nodes
-        self.offset = rank * self.stride if world > 1 else 0
-        np_loc, el_loc, v_loc = local_csr(node_pointer, edge_list, values, self.r0, self.r1)
-        if world > 1:
-            el_loc = remap_columns(el_loc, self.ranges, self.stride)
-        self.csr = (np_loc, el_loc, v_loc)
-        self.graph = None
-        if build_graph:
-            from .device import DeviceGraph
+        self.stride = replica_stride(self.ranges_all) if world > 1 else num_nodes
+        self.padded_rows = self.stride * world * K if world > 1 else num_nodes
+        # one replica block per range, in row order (block q = pK + k)
+        self.chunk_ranges = self.ranges_all[rank * K:(rank + 1) * K]
+        self.chunk_offsets = ([(rank * K + k) * self.stride for k in range(K)]
+                              if world > 1 else [0])
+        self.offset = self.chunk_offsets[0]
+        self.csrs, self.graphs = [], []
+        for k, (c0, c1) in enumerate(self.chunk_ranges):
+            np_loc, el_loc, v_loc = local_csr(node_pointer, edge_list, values, c0, c1)
+            if world > 1:
+                el_loc = remap_columns(el_loc, self.ranges_all, self.stride)
+            self.csrs.append((np_loc, el_loc, v_loc))
+            if build_graph:
+                from .device import DeviceGraph
 
-            if world == 1:
-                self.graph = DeviceGraph.from_csr(np_loc, el_loc, v_loc, self.rows,
-                                                  blk_h=blk_h, blk_w=blk_w)
-            else:
-                self.graph = DeviceGraph.from_csr(np_loc, el_loc, v_loc, self.rows, blk_h,
-                                                  blk_w, num_cols=self.padded_rows,
-                                                  row_offset=self.offset)
+                if world == 1:
+                    self.graphs.append(DeviceGraph.from_csr(np_loc, el_loc, v_loc, c1 - c0,
+                                                            blk_h=blk_h, blk_w=blk_w))
+                else:
+                    self.graphs.append(DeviceGraph.from_csr(np_loc, el_loc, v_loc, c1 - c0, blk_h,
+                                                            blk_w, num_cols=self.padded_rows,
+                                                            row_offset=self.chunk_offsets[k]))
+        self.csr = self.csrs[0]
+        self.graph = self.graphs[0] if self.graphs else None
+        self._comm = None
+        self._stage = {}
 
     # ---- replica management -------------------------------------------------
     def replica(self, d: int, device=None, dtype=torch.float32) -> torch.Tensor:
@@ -170,27 +196,86 @@ class RowSlice:
         return torch.zeros((self.padded_rows, d), dtype=dtype, device=device)
 
     def mine(self, buf: torch.Tensor) -> torch.Tensor:
-        """This rank's rows inside a replica (a view: writes land in place)."""
+        """This rank's rows inside a replica (a view: writes land in place);
+        chunks > 1: mine_k / write_mine (the rows sit in K blocks)."""
+        if self.chunks > 1:
+            raise ValueError("RowSlice.mine: chunked layout, use mine_k(buf, k)")
         return buf[self.offset:self.offset + self.rows]
 
+    def mine_k(self, buf: torch.Tensor, k: int) -> torch.Tensor:
+        """Sub-slice k's rows inside a replica (a view)."""
+        c0, c1 = self.chunk_ranges[k]
+        o = self.chunk_offsets[k]
+        return buf[o:o + (c1 - c0)]
+
+    def write_mine(self, buf: torch.Tensor, rows: torch.Tensor) -> None:
+        """Copy this rank's rows (in row order) into their replica blocks."""
+        at = 0
+        for k, (c0, c1) in enumerate(self.chunk_ranges):
+            self.mine_k(buf, k).copy_(rows[at:at + (c1 - c0)], non_blocking=True)
+            at += c1 - c0
+
     def exchange(self, buf: torch.Tensor) -> None:
-        exchange_inplace(buf, self.rank, self.world, self.group)
+        if self.chunks == 1:
+            exchange_inplace(buf, self.rank, self.world, self.group)
+            return
+        works = [self.exchange_chunk(buf, k) for k in range(self.chunks)]
+        for w in works:
+            if w is not None:
+                w.wait()
+
+    def exchange_chunk(self, buf: torch.Tensor, k: int):
+        """All-gather every rank's chunk-k block into a contiguous staging
+        buffer (world x stride rows) and scatter it into the replica's chunk-k
+        blocks.  NCCL: on a second stream, started once the current stream has
+        written this rank's block; returns a handle whose wait() makes the
+        current stream wait.  Other backends: synchronous, returns None."""
+        W, K, S = self.world, self.chunks, self.stride
+        view = buf.view(W, K, S, *buf.shape[1:])
+        key = (k, tuple(buf.shape[1:]), buf.dtype, buf.device)
+        if key not in self._stage:
+            self._stage[key] = torch.empty((W * S,) + tuple(buf.shape[1:]), dtype=buf.dtype,
+                                           device=buf.device)
+        stage = self._stage[key]
+        sv = stage.view(W, S, *buf.shape[1:])
+        if not (buf.is_cuda and dist.get_backend(self.group) == "nccl"):
+            sv[self.rank].copy_(view[self.rank, k])
+            exchange_inplace(stage, self.rank, W, self.group)
+            view[:, k].copy_(sv)
+            return None
+        if self._comm is None:
+            self._comm = torch.cuda.Stream(device=buf.device)
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(buf.device))
+        with torch.cuda.stream(self._comm):
+            self._comm.wait_event(ready)
+            sv[self.rank].copy_(view[self.rank, k])
+            dist.all_gather_into_tensor(stage, sv[self.rank], group=self.group)
+            view[:, k].copy_(sv)
+            done = torch.cuda.Event()
+            done.record(self._comm)
+
+        class _Done:
+            def wait(self_inner):
+                torch.cuda.current_stream(buf.device).wait_event(done)
+
+        return _Done()
 
     def scatter_full(self, full: torch.Tensor, buf: torch.Tensor) -> torch.Tensor:
         """Write an N-row matrix into the replica layout (inputs, tests)."""
         if self.world == 1:
             buf.copy_(full)
             return buf
-        for p, (r0, r1) in enumerate(self.ranges):
-            buf[p * self.stride:p * self.stride + (r1 - r0)] = full[r0:r1]
+        for q, (r0, r1) in enumerate(self.ranges_all):
+            buf[q * self.stride:q * self.stride + (r1 - r0)] = full[r0:r1]
         return buf
 
     def gather_full(self, buf: torch.Tensor) -> torch.Tensor:
         """Replica -> N-row matrix (outside any timed region)."""
         if self.world == 1:
             return buf
-        return torch.cat([buf[p * self.stride:p * self.stride + (r1 - r0)]
-                          for p, (r0, r1) in enumerate(self.ranges)])
+        return torch.cat([buf[q * self.stride:q * self.stride + (r1 - r0)]
+                          for q, (r0, r1) in enumerate(self.ranges_all)])
 
     # ---- layers -------------------------------------------------------------
     def agnn_forward(self, h_rep: torch.Tensor, betas, precision="tf32", mode=3,
@@ -204,6 +289,8 @@ class RowSlice:
             return self.graph.agnn_forward(h_rep, b, precision=precision, mode=mode, out=out)
         if scratch is None:
             scratch = (torch.zeros_like(h_rep), torch.zeros_like(h_rep))
+        if self.chunks > 1:
+            return self._agnn_chunked(h_rep, b, precision, mode, scratch, out)
         src = h_rep
         for l in range(len(b)):
             if l + 1 == len(b):
@@ -215,6 +302,34 @@ class RowSlice:
             self.exchange(dst)
             src = dst
         return self.mine(h_rep).clone() if out is None else out.copy_(self.mine(h_rep))
+
+    def _agnn_chunked(self, h_rep, b, precision, mode, scratch, out):
+        """agnn_forward with chunks > 1: per layer, sub-slice k's rows land in
+        their block and that chunk's all-gather starts while sub-slice k+1
+        computes; the next layer waits for all K."""
+        if out is None:
+            out = torch.empty((self.rows, h_rep.shape[1]), dtype=h_rep.dtype, device=h_rep.device)
+        src = h_rep
+        for l in range(len(b)):
+            last = l + 1 == len(b)
+            dst = None if last else scratch[l % 2]
+            works, at = [], 0
+            for k, g in enumerate(self.graphs):
+                c0, c1 = self.chunk_ranges[k]
+                if last:
+                    g.agnn_forward(src, b[l:l + 1], precision=precision, mode=mode,
+                                   out=out[at:at + (c1 - c0)])
+                else:
+                    g.agnn_forward(src, b[l:l + 1], precision=precision, mode=mode,
+                                   out=self.mine_k(dst, k))
+                    works.append(self.exchange_chunk(dst, k))
+                at += c1 - c0
+            for w in works:
+                if w is not None:
+                    w.wait()
+            if dst is not None:
+                src = dst
+        return out
 
     def gcn_forward(self, x_local: torch.Tensor, layers, precision="tf32",
                     reps: dict | None = None, nonfinite=None) -> torch.Tensor:
@@ -228,6 +343,8 @@ class RowSlice:
         if self.world == 1:
             return self.graph.gcn_forward(x_local, layers, precision=precision, order=2,
                                           nonfinite=nonfinite)
+        if self.chunks > 1:
+            raise ValueError("RowSlice.gcn_forward: the chunked (overlap) layout is built for AGNN")
         reps = {} if reps is None else reps
 
         def rep(d):

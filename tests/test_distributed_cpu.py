@@ -108,6 +108,33 @@ def worker(rank, world, port, q):
             rs.exchange(nxt)
             h_rep = nxt.numpy()
         assert np.array_equal(rs.gather_full(torch.from_numpy(h_rep)).numpy(), want)
+        # the chunked (overlap) layout: 2 sub-slices per rank, a block per
+        # range, one all-gather per chunk (exchange_chunk), same result
+        rc = RowSlice(g.node_pointer, g.edge_list, None, n, rank, world, build_graph=False, chunks=2)
+        assert rc.padded_rows == 2 * world * rc.stride and len(rc.csrs) == 2
+        assert (rc.r0, rc.r1) == rc.ranges[rank] and rc.chunk_ranges[0][0] == rc.r0
+        assert rc.chunk_ranges[-1][1] == rc.r1
+        rep = rc.replica(16)
+        rc.scatter_full(torch.from_numpy(x), rep)
+        assert np.array_equal(rc.gather_full(rep).numpy(), x)
+        h_rep = rep.numpy()
+        for l, b in enumerate(betas):
+            z, _ = O.l2_normalize_rows(h_rep)
+            nxt = rc.replica(16)
+            for k, (c0, c1) in enumerate(rc.chunk_ranges):
+                np_k, el_k, _ = rc.csrs[k]
+                for rr in range(c1 - c0):
+                    row = el_k[int(np_k[rr]):int(np_k[rr + 1])].astype(np.int64)
+                    assert np.all(np.diff(row) > 0)
+                sk = Csr.of(c1 - c0, np_k, el_k)
+                o = rc.chunk_offsets[k]
+                logits = O.sddmm(sk, z[o:o + (c1 - c0)], z,
+                                 values=np.ones(sk.num_edges, np.float32)) * np.float32(b)
+                h_k = O.spmm(sk, h_rep, values=O.edge_softmax(sk, logits))
+                rc.mine_k(nxt, k).copy_(torch.from_numpy(h_k))
+                assert rc.exchange_chunk(nxt, k) is None  # gloo: synchronous
+            h_rep = nxt.numpy()
+        assert np.array_equal(rc.gather_full(torch.from_numpy(h_rep)).numpy(), want)
         # exchange_inplace leaves padding rows untouched and fills every block
         buf = torch.full((world * 4, 2), -1.0)
         buf[rank * 4:rank * 4 + 3] = float(rank)
@@ -116,7 +143,8 @@ def worker(rank, world, port, q):
             assert torch.all(buf[p * 4:p * 4 + 3] == p)
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported to the parent
-        q.put((rank, repr(e)))
+        import traceback
+        q.put((rank, traceback.format_exc()))
     finally:
         dist.destroy_process_group()
 

@@ -103,6 +103,31 @@ def test_agnn_padded_replica_bit_identical(graph, parts, precision, mode):
     assert torch.equal(sl[0].gather_full(cur), want), (parts, mode)
 
 
+@pytest.mark.parametrize("parts,chunks", [(2, 2), (3, 3), (4, 2)])
+@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+def test_agnn_chunked_replica_bit_identical(graph, parts, chunks, precision):
+    """The overlap layout (RowSlice chunks > 1: K sub-slices per rank, one
+    block per sub-slice, a staged all-gather per chunk) on one device: every
+    sub-slice writes its block of the shared replica, which is what the K
+    exchanges produce; bit-identical to the whole graph."""
+    g = graph
+    whole = DeviceGraph.from_csr(g.node_pointer, g.edge_list)
+    h = dev(sg.dense_random(g.num_nodes, 32, 5))
+    betas = np.array([1.0, 0.8, 1.2], np.float32)
+    want = whole.agnn_forward(h, betas, precision=precision, mode=2)
+    sl = [RowSlice(g.node_pointer, g.edge_list, None, g.num_nodes, r, parts, chunks=chunks)
+          for r in range(parts)]
+    assert all(len(s.graphs) == chunks for s in sl)
+    cur = sl[0].scatter_full(h, sl[0].replica(32, "cuda"))
+    for l in range(len(betas)):
+        nxt = sl[0].replica(32, "cuda")
+        for s in sl:
+            for k, gk in enumerate(s.graphs):
+                gk.agnn_forward(cur, betas[l:l + 1], precision=precision, mode=2, out=s.mine_k(nxt, k))
+        cur = nxt
+    assert torch.equal(sl[0].gather_full(cur), want), (parts, chunks)
+
+
 @pytest.mark.parametrize("parts", [2, 4])
 def test_gcn_padded_replica_bit_identical(graph, parts):
     g = sg.gcn_normalize_values(graph)
