@@ -92,7 +92,10 @@ struct AgnnCfg {
 #ifndef SGTK_AGNN_NB_F32
 #define SGTK_AGNN_NB_F32 6  // FP32 d = 32: 1.092 -> 1.024 ms per layer against 4 (8 does not fit)
 #endif
-  static constexpr int NB = F32 ? (DC == 32 ? SGTK_AGNN_NB_F32 : 2) : (PT ? SGTK_AGNN_NB : 6);  // gather ring (even: S pairs)
+#ifndef SGTK_AGNN_NB_64
+#define SGTK_AGNN_NB_64 6
+#endif
+  static constexpr int NB = F32 ? (DC == 32 ? SGTK_AGNN_NB_F32 : 2) : (PT ? SGTK_AGNN_NB : SGTK_AGNN_NB_64);  // gather ring (even: S pairs)
   // P slots in smem; PT: pfull barriers only, one per chunk the softmax can
   // run ahead of the MMA issuer (S can be up to NSB groups ahead)
   static constexpr int NP = PT ? 8 : 2;
