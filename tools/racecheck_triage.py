@@ -46,10 +46,13 @@ for tool in ("memcheck", "synccheck", "initcheck", "racecheck"):
             return "cp.async.bulk (TMA engine) write, completion via mbarrier complete_tx, consumer waits the mbarrier"
         if "cp_async16" in names:
             return "cp.async write, completion via cp.async.mbarrier.arrive.noinc, consumer waits the mbarrier"
-        if names & {"sddmm_dense_kernel"}:
-            # checked by hand: sddmm_panel.cu stage-slot writes (stage warps) ->
-            # __syncwarp + arrive(stfull) -> store warps wait(stfull) -> reads;
-            # ecnt written by the loader before its expect_tx arrive on efull
+        if names & {"sddmm_dense_kernel", "sddmm_dense2_kernel"}:
+            # checked by hand: sddmm_panel.cu stage-slot / row-tile writes (stage
+            # warps) -> __syncwarp + arrive(stfull / rfull) -> storing warps
+            # wait -> reads, reuse after arrive(stempty / rempty); the row starts
+            # (nps) written before arrive(qfull) / the writer's own rfull; ecnt
+            # written by the loader before its expect_tx arrive on efull, rewritten
+            # after eempty
             return ("generic-proxy hand-off between warp roles through an mbarrier "
                     "(arrive = release, try_wait.parity = acquire)")
         if "gemm_tc05_kernel" in names:

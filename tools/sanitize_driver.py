@@ -36,7 +36,10 @@ def main():
             for prec in ("tf32", "fp32"):
                 for mode in (0, 1, 2):
                     dg.agnn_forward(x, np.ones(2, np.float32), precision=prec, mode=mode)
-        dg.sddmm(x, x, precision="tf32")
+        dg.sddmm(x, x, precision="tf32")                      # direct form (Panels::dpos)
+        dgn.sddmm(x, x, precision="fp32")                     # weighted graph: entry values
+        ev = torch.rand(g.num_edges, device="cuda")
+        dg.sddmm(x, x, precision="tf32", edge_values=ev)      # CSR-order overrides
         w = torch.from_numpy(sg.dense_random(d, 32, 6, -0.1, 0.1)).cuda()
         D.gemm(x, w, relu=True, precision="tf32")
         D.gemm(x, w, relu=False, precision="fp32")
