@@ -64,6 +64,9 @@ constexpr int agnn_loaders(int DC, int PREC) {
 }
 constexpr int agnn_threads(int DC, int PREC) { return 32 * (10 + agnn_loaders(DC, PREC)); }
 
+#ifndef SGTK_MASK_GLOBAL
+#define SGTK_MASK_GLOBAL 1
+#endif
 template <int DC, int PREC>
 struct AgnnCfg {
   static constexpr bool F32 = PREC == SGTK_FP32;
@@ -269,23 +272,53 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
     }
     float l = 0.0f;
     const uint32_t pb = smem_u32(ps);
+    // PT: the row masks come straight from global memory, three chunks ahead
+    // in registers (no gather-ring mbarrier probe per chunk: each probe costs
+    // ~100 cycles on this chain), and the second chunk of an S pair reuses
+    // the pair's sfull wait
+    constexpr bool MG = C::PT && SGTK_MASK_GLOBAL;
+    const uint32_t* dm = pv.dmask + uint64_t(c0) * kPanelRows + r;
+    uint32_t mq0 = 0, mq1 = 0, mq2 = 0;
+    if constexpr (MG) {
+      mq0 = nch > 0 ? __ldg(dm) : 0u;
+      mq1 = nch > 1 ? __ldg(dm + kPanelRows) : 0u;
+      mq2 = nch > 2 ? __ldg(dm + 2 * kPanelRows) : 0u;
+    }
     for (uint32_t c = 0; c < nch; ++c) {
       const uint32_t sgi = c / C::SG;  // S group of the chunk
       const uint32_t sb = sgi % C::NSB, sph = (sgi / C::NSB) & 1u, shalf = (c % C::SG) * 32;
       const uint32_t ds = c % C::NB, dph = (c / C::NB) & 1u;
       const uint32_t pslot = c % C::NP;
-      mbar_wait(bfull + ds, dph);  // row masks of the chunk
-      const uint32_t mask = ld_shared_u32(mr_s + ds * C::M_BYTES + r * 4);
+      uint32_t mask;
+      if constexpr (MG) {
+        mask = mq0;
+        mq0 = mq1;
+        mq1 = mq2;
+        mq2 = c + 3 < nch ? __ldg(dm + uint64_t(c + 3) * kPanelRows) : 0u;
+      } else {
+        mbar_wait(bfull + ds, dph);  // row masks of the chunk
+        mask = ld_shared_u32(mr_s + ds * C::M_BYTES + r * 4);
+      }
+      (void)ds;
+      (void)dph;
+#ifndef SGTK_TRACE_SM2
       if (warp == 0 && lane == 0) mark(c, 7);
-      mbar_wait(sfull + sb, sph);
+#endif
+      if (!MG || (c % C::SG) == 0) mbar_wait(sfull + sb, sph);
+#ifdef SGTK_TRACE_SM2  // per-softmax-warp stamps: ev 4 + w = S(c) ready, ev w = P(c) written
+      if (lane == 0) mark(c, 4 + warp);
+#else
       if (warp == 0 && lane == 0) mark(c, 1);
+#endif
       tc_fence_after();
       uint32_t sv[32];
       tmem_ld16(tmem + ((warp * 32u) << 16) + s_col + sb * 64 + shalf, *reinterpret_cast<uint32_t(*)[16]>(sv));
       tmem_ld16(tmem + ((warp * 32u) << 16) + s_col + sb * 64 + shalf + 16,
                 *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
       tmem_ld_wait();
+#ifndef SGTK_TRACE_SM2
       if (warp == 0 && lane == 0) mark(c, 6);
+#endif
       tc_fence_before();
       if constexpr (!C::PT && C::SPLIT_MMA) {  // the group's S read: its TMEM buffer is free
         if ((c % C::SG) == C::SG - 1 || c + 1 == nch) {
@@ -313,14 +346,21 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
         else lq23 = __fadd2_rn(lq23, make_float2(pr[j], pr[j + 1]));
       }
       l += (lq01.x + lq01.y) + (lq23.x + lq23.y);
+#ifndef SGTK_TRACE_SM2
       if (warp == 0 && lane == 0) mark(c, 5);
+#endif
       if constexpr (C::PT) {  // P over this chunk's S columns (already read)
         tmem_st32(tmem + ((warp * 32u) << 16) + s_col + sb * 64 + shalf, *reinterpret_cast<uint32_t(*)[32]>(pr));
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
+#ifndef SGTK_TRACE_SM2
         if (warp == 0 && lane == 0) mark(c, 2);
+#endif
         if (lane == 0) mbar_arrive(pfull + pslot);
+#ifdef SGTK_TRACE_SM2
+        if (lane == 0) mark(c, warp);
+#endif
         continue;
       }
       if (c >= uint32_t(C::NP)) {  // PV(c - NP) done with this P slot
@@ -433,7 +473,9 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
           }
         }
         umma_commit(sfull + g % C::NSB);
+#ifndef SGTK_TRACE_SM2
         mark(c, 0);
+#endif
       };
       auto issue_pv = [&](uint32_t c) {
         const uint32_t ds = c % C::NB, pslot = c % C::NP;
@@ -463,7 +505,9 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
             umma_tf32(dt, p0, h0, id_o, acc);
           }
         }
+#ifndef SGTK_TRACE_SM2
         mark(c, 3);
+#endif
         umma_commit(bempty + ds);  // gather slot and P slot free
         if ((c % C::FOLD) == C::FOLD - 1 || c + 1 == nch) umma_commit(accfull + buf);
       };
@@ -508,7 +552,9 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
 #endif
       coln = c + NL < nch ? pv.dcols[uint64_t(c0 + c + NL) * kChunkCols + lane] : 0u;
       mbar_wait(bempty + ds, ((c / C::NB) & 1u) ^ 1u);
+#ifndef SGTK_TRACE_SM2
       if (lane == 0) mark(c, 4);
+#endif
       const uint32_t ht = hr_s + ds * C::T_BYTES;
       if constexpr (TG) {
         // lane g < 8 gathers chunk rows 4g..4g+3: z (K-major SWIZZLE_128B, one
@@ -554,7 +600,13 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
           cp_async16(ht + C::NB * C::T_BYTES + ho, real ? h1 + gofs : g_agnn_zero + (k * LPR + j) * 4);
         }
       }
-      cp_async16(mr_s + ds * C::M_BYTES + lane * 16, pv.dmask + (uint64_t(c0 + c) * kPanelRows) + lane * 4);
+#ifndef SGTK_MASK_COPY
+#define SGTK_MASK_COPY 1
+#endif
+      // (PT reads the masks from global memory; dropping this now-unused copy
+      // measured 6% slower on the dense part -- 0.270 -> 0.287 ms -- so it stays)
+      if (SGTK_MASK_COPY || !(C::PT && SGTK_MASK_GLOBAL))
+        cp_async16(mr_s + ds * C::M_BYTES + lane * 16, pv.dmask + (uint64_t(c0 + c) * kPanelRows) + lane * 4);
       cp_async_arrive_noinc(bfull + ds);
     }
     if constexpr (!TG) cp_async_wait<0>();
