@@ -603,8 +603,9 @@ agnn_dense_kernel(const PanelView pv, const float* __restrict__ zraw, const floa
 #ifndef SGTK_MASK_COPY
 #define SGTK_MASK_COPY 1
 #endif
-      // (PT reads the masks from global memory; dropping this now-unused copy
-      // measured 6% slower on the dense part -- 0.270 -> 0.287 ms -- so it stays)
+      // (PT: the softmax reads its masks from global memory three chunks
+      // ahead; this copy, issued ~10 chunks ahead, is what brings them into
+      // L2 in time -- without it the dense part measured 0.270 -> 0.287 ms)
       if (SGTK_MASK_COPY || !(C::PT && SGTK_MASK_GLOBAL))
         cp_async16(mr_s + ds * C::M_BYTES + lane * 16, pv.dmask + (uint64_t(c0 + c) * kPanelRows) + lane * 4);
       cp_async_arrive_noinc(bfull + ds);
