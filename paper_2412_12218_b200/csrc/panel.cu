@@ -735,6 +735,303 @@ spmm_panel_kernel(const PanelView pv, const PanelSmem L, const float* __restrict
 }
 
 // ---------------------------------------------------------------------------
+// Dense part, TF32, A built in TMEM (opt-in: SGTK_SPMM_TM=1; measured slower
+// than spmm_panel_kernel).  The A tile of a chunk never touches shared memory: the
+// thread of panel row r reads its row mask and its row's packed entries (the
+// chunk's entries are in (row, column) order, so row r's values start at the
+// popcount of the rows before it), builds its 32 TF32 values in registers and
+// stores them into its TMEM lane (tcgen05.st); the MMA reads A from TMEM
+// ("TS" form, as the AGNN kernel's P).  No zero tile, no scatter, no A stage
+// to recycle: the builder -> MMA chain is registers -> TMEM.  The smem the A
+// stages held goes to a deeper B ring.  Same products, same K order, same
+// FOLD groups and fold order as spmm_panel_kernel: bit-identical to it.
+//   warps 0..4BG-1  A builders: BG groups of 4 warps, group c % BG builds
+//               chunk c, thread per row (TMEM lane = row; a builder is
+//               latency-bound, so BG chunks are in construction at once); the
+//               group's first lane bulk-copies the masks + entries of its
+//               chunk NE - 1 turns ahead into its entry ring (TMA engine)
+//   next 4      accumulators (as spmm_panel_kernel)
+//   next 1      TMEM allocator + MMA issuer
+//   last NL     B loaders (cp.async gathers, chunk c by loader c % NL)
+// ---------------------------------------------------------------------------
+#ifndef SGTK_TM_LOADERS
+#define SGTK_TM_LOADERS 2
+#endif
+#ifndef SGTK_TM_NE
+#define SGTK_TM_NE 2
+#endif
+#ifndef SGTK_TM_BG
+#define SGTK_TM_BG 2
+#endif
+
+#ifndef SGTK_TM_PREFETCH
+#define SGTK_TM_PREFETCH 1
+#endif
+template <int DC>
+struct TmCfg {
+  static constexpr int NL = SGTK_TM_LOADERS;
+  static constexpr int BG = SGTK_TM_BG;                  // builder groups
+  static constexpr uint32_t AW = 4 * BG, IW = AW + 4, LW = IW + 1;  // accumulator / issuer / first loader warp
+  static constexpr int THREADS = 32 * (LW + NL);
+  static constexpr uint32_t B_BYTES = kChunkCols * DC * 4;
+  static constexpr int NBMAX = DC == 64 ? 12 : 16;
+  static constexpr int NE = SGTK_TM_NE;       // entry ring per builder group (lead: NE - 1 of its chunks)
+  static constexpr int NA = DC == 64 ? 2 : 4;  // A buffers, 32 TMEM columns each
+  static constexpr int NF = DC == 64 ? 2 : 3;  // accumulators
+  static constexpr uint32_t BUF0 = DC;         // running sum: columns [0, DC)
+  static constexpr uint32_t ACOL = DC * (1 + NF);
+  static constexpr uint32_t TMEM_COLS = 256;   // two CTAs per SM
+  static_assert(ACOL + 32 * NA <= TMEM_COLS, "TMEM budget");
+  static constexpr uint32_t FOLD = SGTK_FOLD;  // as spmm_panel_kernel (bit-identical)
+};
+
+struct TmSmem {
+  uint32_t nb;     // B ring depth
+  uint32_t eslot;  // bytes of one entry slot: 512 B masks + entries (+ 16 B read slack)
+  uint32_t ering_off, total;
+};
+
+template <int DC>
+__global__ void __launch_bounds__(TmCfg<DC>::THREADS, 2)
+spmm_tm_kernel(const PanelView pv, const TmSmem L, const float* __restrict__ x, uint64_t ldx, uint64_t d,
+               float* __restrict__ out, uint64_t ldo, int vec_out, uint32_t* __restrict__ nonfinite) {
+  using C = TmCfg<DC>;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t NB = L.nb;
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(smem);  // [NBMAX] B tile landed
+  uint64_t* bempty = bfull + C::NBMAX;                  // [NBMAX] MMA(c) retired: B slot + A buffer free
+  uint64_t* efull = bempty + C::NBMAX;                  // [BG][NE] masks + entries landed
+  uint64_t* eempty = efull + C::BG * C::NE;             // [BG][NE] read by the group's 4 warps
+  uint64_t* afull = eempty + C::BG * C::NE;             // [NA] A(c) in TMEM
+  uint64_t* accfull = afull + C::NA;                    // [NF]
+  uint64_t* accempty = accfull + C::NF;                 // [NF]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + C::NF);
+  static_assert((2 * C::NBMAX + 2 * C::BG * C::NE + C::NA + 2 * C::NF) * 8 + 16 <= 1024, "barriers");
+  uint8_t* bring = smem + 1024;
+  uint8_t* ering = smem + L.ering_off;
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t p = blockIdx.x;
+  const uint64_t fbase = uint64_t(blockIdx.y) * DC;
+  const int dvalid = d - fbase < uint64_t(DC) ? int(d - fbase) : DC;
+  const uint32_t c0 = pv.cptr[p], nch = pv.cptr[p + 1] - c0;
+  const uint32_t ngroups = (nch + C::FOLD - 1) / C::FOLD;
+
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < NB; ++i) {
+      mbar_init(bfull + i, 32);  // cp.async.mbarrier.arrive.noinc per lane of the loader warp
+      mbar_init(bempty + i, 1);  // tcgen05.commit
+    }
+    for (int i = 0; i < C::BG * C::NE; ++i) {
+      mbar_init(efull + i, 1);  // bulk copies (expect_tx)
+      mbar_init(eempty + i, 4);
+    }
+    for (int i = 0; i < C::NA; ++i) mbar_init(afull + i, 4);
+    for (int i = 0; i < C::NF; ++i) {
+      mbar_init(accfull + i, 1);
+      mbar_init(accempty + i, 4);
+    }
+    mbar_init_fence();
+  }
+  if (warp == C::IW) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < C::AW) {
+    // ------------------------------------------------------------ A builders
+    const uint32_t wq = warp & 3u, grp = warp >> 2;
+    const uint32_t r = wq * 32 + lane;
+    const uint32_t lanes = (wq * 32u) << 16;
+    // the group's chunks grp, grp + BG, ...; its n-th chunk uses entry slot
+    // grp * NE + n % NE
+    auto fetch = [&](uint32_t n) {  // masks + entries of the group's n-th chunk
+      const uint32_t cn = grp + n * C::BG;
+      const uint32_t es = grp * C::NE + n % C::NE;
+      if (n >= uint32_t(C::NE)) mbar_wait(eempty + es, ((n / C::NE) - 1u) & 1u);
+      const uint64_t e0 = pv.coff[c0 + cn], e1 = pv.coff[c0 + cn + 1];
+      const uint32_t bytes = uint32_t(e1 - e0) * 4u;
+      uint8_t* slot = ering + es * L.eslot;
+      mbar_expect_tx(efull + es, 512u + bytes);
+      bulk_load(slot, pv.dmask + uint64_t(c0 + cn) * kPanelRows, 512u, efull + es);
+      if (bytes) bulk_load(slot + 512, pv.dent + e0, bytes, efull + es);
+    };
+    if (wq == 0 && lane == 0)
+      for (uint32_t n = 0; n + 1 < uint32_t(C::NE) && grp + n * C::BG < nch; ++n) fetch(n);
+    for (uint32_t c = grp, n = 0; c < nch; c += C::BG, ++n) {
+      if (wq == 0 && lane == 0 && c + (C::NE - 1) * C::BG < nch) fetch(n + C::NE - 1);
+      const uint32_t es = grp * C::NE + n % C::NE;
+      mbar_wait(efull + es, (n / C::NE) & 1u);
+      const uint32_t sb = smem_u32(ering + es * L.eslot);
+      const uint32_t m = ld_shared_u32(sb + r * 4);
+      const uint4 mm = ld_shared_u4(sb + lane * 16);  // rows 4 lane .. 4 lane + 3
+      const uint32_t s4 = __popc(mm.x) + __popc(mm.y) + __popc(mm.z) + __popc(mm.w);
+      const uint32_t base = __reduce_add_sync(0xFFFFFFFFu, lane < 8 * wq ? s4 : 0u);  // rows < 32 wq
+      const uint32_t own = __popc(m);
+      uint32_t incl = own;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= uint32_t(o)) incl += t;
+      }
+      // this row's entries: words [base + incl - own, + own) after the masks
+      const uint32_t* ev = reinterpret_cast<const uint32_t*>(ering + es * L.eslot + 512) + (base + incl - own);
+      uint32_t av[32];
+      uint32_t t = 0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const uint32_t on = (m >> k) & 1u;
+        const uint32_t w = ev[t];  // in the slot even past the row (16 B slack)
+        av[k] = on ? (w & 0xFFFFE000u) : 0u;
+        t += on;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(eempty + es);
+      if (c >= uint32_t(C::NA)) {  // MMA(c - NA) retired: A buffer free
+        const uint32_t cp = c - C::NA;
+        mbar_wait(bempty + cp % NB, (cp / NB) & 1u);
+      }
+      tc_fence_after();
+      tmem_st32(tmem + lanes + C::ACOL + (c % C::NA) * 32u, av);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(afull + c % C::NA);
+    }
+  } else if (warp < C::IW) {
+    // ------------------------------------------------------------ accumulators
+    const uint32_t q = warp & 3u;
+    const uint64_t r = p * kPanelRows + q * 32 + lane;
+    const uint32_t lanes = (q * 32u) << 16;
+    for (uint32_t g = 0; g < ngroups; ++g) {
+      const uint32_t buf = g % C::NF;
+      mbar_wait(accfull + buf, (g / C::NF) & 1u);
+      tc_fence_after();
+#pragma unroll
+      for (int cc = 0; cc < DC; cc += 16) {
+        uint32_t v[16], sm[16];
+        tmem_ld16(tmem + lanes + C::BUF0 + buf * DC + cc, v);
+        if (g) tmem_ld16(tmem + lanes + cc, sm);
+        tmem_ld_wait();
+        if (g) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(sm[j]) + __uint_as_float(v[j]));
+        }
+        tmem_st16(tmem + lanes + cc, v);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(accempty + buf);
+    }
+    tc_fence_after();
+    const bool rv = r < pv.n_rows;
+    float* o = out + r * ldo + fbase;
+    bool bad = false;
+#pragma unroll
+    for (int cc = 0; cc < DC; cc += 16) {
+      uint32_t v[16];
+      if (ngroups) {
+        tmem_ld16(tmem + lanes + cc, v);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0u;
+      }
+      if (rv) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          bad |= cc + j < dvalid && (v[j] & 0x7F800000u) == 0x7F800000u;
+        if (vec_out && dvalid == DC) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            reinterpret_cast<float4*>(o + cc)[j] =
+                make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (cc + j < dvalid) o[cc + j] = __uint_as_float(v[j]);
+        }
+      }
+    }
+    if (nonfinite && __any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(nonfinite, 1u);
+  } else if (warp == C::IW) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(DC, true);
+      for (uint32_t c = 0; c < nch; ++c) {
+        const uint32_t g = c / C::FOLD, buf = g % C::NF;
+        const bool first = (c % C::FOLD) == 0;
+        if (first && g >= uint32_t(C::NF)) mbar_wait(accempty + buf, ((g / C::NF) - 1u) & 1u);
+        const uint32_t ds = c % NB;
+        mbar_wait(afull + c % C::NA, (c / C::NA) & 1u);
+        mbar_wait(bfull + ds, (c / NB) & 1u);
+        fence_async_smem();  // cp.async (generic proxy) -> MMA (async proxy)
+        tc_fence_after();
+        const uint32_t dt = tmem + C::BUF0 + buf * DC;
+        const uint32_t at = tmem + C::ACOL + (c % C::NA) * 32u;
+        const uint32_t b0 = smem_u32(bring + ds * C::B_BYTES);
+#pragma unroll
+        for (uint32_t ks = 0; ks < kChunkCols / 8; ++ks)
+          umma_tf32_ts(dt, at + ks * 8, desc_mn32(b0 + ks * 1024, 4096, 512), idesc, (first && ks == 0) ? 0u : 1u);
+        umma_commit(bempty + ds);  // B slot and A buffer of chunk c free
+        if ((c % C::FOLD) == C::FOLD - 1 || c + 1 == nch) umma_commit(accfull + buf);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ B loaders
+    const uint32_t par = warp - C::LW;
+    constexpr uint32_t LPR = DC / 4, RPG = 32 / LPR;  // lanes per feature row, rows per instruction
+    const uint32_t j = lane % LPR, jj = j & 7u;
+    uint32_t coln = par < nch ? __ldg(pv.dcols + uint64_t(c0 + par) * kChunkCols + lane) : 0u;
+    // lanes 0, 1: the chunk's entry range, one iteration ahead
+    uint64_t offn = par + lane <= nch && lane < 2 ? __ldg(pv.coff + c0 + par + lane) : 0u;
+    for (uint32_t c = par; c < nch; c += C::NL) {
+      const uint32_t ds = c % NB;
+      const uint32_t col = coln;
+      coln = c + C::NL < nch ? __ldg(pv.dcols + uint64_t(c0 + c + C::NL) * kChunkCols + lane) : 0u;
+      const uint64_t e0 = __shfl_sync(0xFFFFFFFFu, offn, 0), e1 = __shfl_sync(0xFFFFFFFFu, offn, 1);
+      offn = c + C::NL + lane <= nch && lane < 2 ? __ldg(pv.coff + c0 + c + C::NL + lane) : 0u;
+      mbar_wait(bempty + ds, ((c / NB) & 1u) ^ 1u);
+#if SGTK_TM_PREFETCH
+      // the builders bulk-copy this chunk's masks + entries only NE - 1 chunks
+      // ahead: bring them into L2 now, ~NB chunks ahead
+      if (lane == 0) {
+        bulk_prefetch_l2(pv.dmask + uint64_t(c0 + c) * kPanelRows, 512u);
+        if (e1 > e0) bulk_prefetch_l2(pv.dent + e0, uint32_t(e1 - e0) * 4u);
+      }
+#else
+      (void)e0, (void)e1;
+#endif
+      const uint32_t bst = smem_u32(bring + ds * C::B_BYTES);
+#pragma unroll
+      for (uint32_t tt = 0; tt < 32 / RPG; ++tt) {
+        const uint32_t k = tt * RPG + lane / LPR;
+        const uint32_t ck = __shfl_sync(0xFFFFFFFFu, col, k);
+        const bool real = ck != 0xFFFFFFFFu && int(4 * j) < dvalid;
+        // MN-major SWIZZLE_128B_BASE32B, as spmm_panel_kernel's gather_b
+        const uint32_t dst = bst + (j >> 3) * 4096u + (k >> 2) * 512u + (k & 3u) * 128u +
+                             ((((jj >> 1) ^ (k & 3u)) << 5) | ((jj & 1u) << 4));
+        cp_async16(dst, real ? x + uint64_t(ck) * ldx + fbase + 4 * j
+                             : reinterpret_cast<const float*>(g_zero_tile) + (k * LPR + j) * 4);
+      }
+      cp_async_arrive_noinc(bfull + ds);
+    }
+    cp_async_wait<0>();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == C::IW) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Sparse part on the CUDA cores: one warp per work item (a row's sparse
 // edges, or a <= kSegEdges segment of a hub row), lanes over features
 // (FPL = 1 or 2 consecutive floats per lane: 128- or 256-byte coalesced
@@ -936,6 +1233,35 @@ bool launch_dense(const PanelView& v, uint64_t P, uint32_t max_entries, const fl
     }
   }
   CU_LAUNCH("spmm_panel_kernel");
+  return true;
+}
+
+// TF32 dense part with A in TMEM (spmm_tm_kernel): entry slots sized for the
+// graph's largest chunk, then the deepest B ring that keeps two CTAs per SM.
+template <int DC>
+bool launch_dense_tm(const PanelView& v, uint64_t P, uint32_t max_entries, const float* x, uint64_t ldx,
+                     uint64_t d, float* out, uint64_t ldo, int vec_out, uint32_t* nonfinite, cudaStream_t s) {
+  using C = TmCfg<DC>;
+  static const bool on = [] {
+    const char* e = std::getenv("SGTK_SPMM_TM");
+    return e && std::atoi(e) != 0;
+  }();
+  if (!on) return false;
+  TmSmem L;
+  L.eslot = (512u + (max_entries + 3) / 4 * 16u + 16u + 127u) / 128u * 128u;
+  const uint32_t cap = kSmemCap / 2 - 1024;
+  for (L.nb = C::NBMAX; L.nb >= 4; --L.nb) {
+    L.ering_off = 1024 + L.nb * C::B_BYTES;
+    L.total = L.ering_off + C::BG * C::NE * L.eslot + 1024 /*alignment slack*/;
+    if (L.total <= cap) break;
+  }
+  if (L.nb < 4) return false;
+  once_per_device(reinterpret_cast<const void*>(&spmm_tm_kernel<DC>), [] {
+    cudaFuncSetAttribute(spmm_tm_kernel<DC>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemCap));
+  });
+  dim3 grid(unsigned(P), unsigned((d + DC - 1) / DC));
+  spmm_tm_kernel<DC><<<grid, C::THREADS, L.total, s>>>(v, L, x, ldx, d, out, ldo, vec_out, nonfinite);
+  CU_LAUNCH("spmm_tm_kernel");
   return true;
 }
 
@@ -1406,8 +1732,14 @@ bool spmm_panel_launch(const sgtk_graph* g, const float* x, uint64_t ldx, uint64
       if (d <= 32) launch_dense<32, SGTK_FP32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, nonfinite, s);
       else launch_dense<64, SGTK_FP32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, nonfinite, s);
     } else {
-      if (d <= 32) launch_dense<32, SGTK_TF32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, nonfinite, s);
-      else launch_dense<64, SGTK_TF32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, nonfinite, s);
+      // A in TMEM for full 32-feature slices (d % 32 != 0 at d <= 32: the
+      // PAD form of spmm_panel_kernel)
+      if (d <= 32) {
+        if (d % 32 || !launch_dense_tm<32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, nonfinite, s))
+          launch_dense<32, SGTK_TF32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, nonfinite, s);
+      } else if (!launch_dense_tm<64>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, nonfinite, s)) {
+        launch_dense<64, SGTK_TF32>(v, pn.P, me, x, ldx, d, out, ldo, vec_out, nonfinite, s);
+      }
     }
   } else {
     CU(cudaMemset2DAsync(out, ldo * 4, 0, d * 4, g->n_rows, s));

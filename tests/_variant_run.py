@@ -1,6 +1,6 @@
 """One process of tests/test_gpu_variants.py: run a fixed set of calls under
 the environment the test chose and save the outputs.
-    python tests/_variant_run.py sddmm|agnn|hub <out.npz>"""
+    python tests/_variant_run.py sddmm|agnn|hub|spmm <out.npz>"""
 import os
 import sys
 
@@ -49,6 +49,22 @@ def agnn():
     return out
 
 
+def spmm():
+    out = {}
+    for name, g0 in graphs().items():
+        for weighted in (False, True):
+            g = sg.gcn_normalize_values(g0) if weighted else g0
+            dg = DeviceGraph.from_csr(g.node_pointer, g.edge_list, g.values)
+            assert dg.panel_info()["dense_entries"] > 0
+            for d in (32, 48, 64, 96, 128):
+                x = torch.from_numpy(sg.dense_random(g.num_nodes, d, 50 + d)).cuda()
+                out[f"{name}_{int(weighted)}_{d}"] = dg.spmm(x, precision="tf32").cpu().numpy()
+            ov = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, g.num_edges).astype(np.float32)).cuda()
+            x = torch.from_numpy(sg.dense_random(g.num_nodes, 64, 7)).cuda()
+            out[f"{name}_{int(weighted)}_ov"] = dg.spmm(x, edge_values=ov, precision="tf32").cpu().numpy()
+    return out
+
+
 def hub():
     from oracle.oracle import Csr, Oracle
 
@@ -80,5 +96,5 @@ def hub():
 
 if __name__ == "__main__":
     what, path = sys.argv[1], sys.argv[2]
-    res = {"sddmm": sddmm, "agnn": agnn, "hub": hub}[what]()
+    res = {"sddmm": sddmm, "agnn": agnn, "hub": hub, "spmm": spmm}[what]()
     np.savez(path, **res)

@@ -10,6 +10,9 @@ per process, against the default forms: each form runs in its own process
 * AGNN fused rows (SGTK_AGNN_FUSED=1: a panel's sparse edges in the dense
   kernel's CTA) run the serial form's arithmetic (SGTK_AGNN_SERIAL=1):
   bit-identical to it.
+* SpMM dense part, TF32: A built in TMEM (SGTK_SPMM_TM=1, spmm_tm_kernel)
+  and A scattered into shared memory (default, spmm_panel_kernel) feed the
+  same products in the same K order and fold groups: bit-identical.
 * A row with more than 2^20 edges does not fit Panels::dpos: the SDDMM falls
   back to the staged form (checked against the CPU oracle)."""
 import os
@@ -29,7 +32,7 @@ RUN = os.path.join(ROOT, "tests", "_variant_run.py")
 def run(tmp_path, name, env_extra, what):
     out = tmp_path / f"{name}.npz"
     env = dict(os.environ)
-    for k in ("SGTK_SDDMM_DENSE", "SGTK_AGNN_GATHER", "SGTK_AGNN_FUSED", "SGTK_AGNN_SERIAL"):
+    for k in ("SGTK_SDDMM_DENSE", "SGTK_AGNN_GATHER", "SGTK_AGNN_FUSED", "SGTK_AGNN_SERIAL", "SGTK_SPMM_TM"):
         env.pop(k, None)
     env.update(env_extra)
     subprocess.run([sys.executable, RUN, what, str(out)], check=True, env=env, cwd=ROOT, timeout=600)
@@ -40,6 +43,14 @@ def test_sddmm_direct_equals_staged(tmp_path):
     a = run(tmp_path, "direct", {}, "sddmm")
     b = run(tmp_path, "staged", {"SGTK_SDDMM_DENSE": "staged"}, "sddmm")
     assert a.keys() == b.keys() and len(a) >= 8
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_spmm_tmem_a_equals_smem_a(tmp_path):
+    a = run(tmp_path, "tm", {"SGTK_SPMM_TM": "1"}, "spmm")
+    b = run(tmp_path, "smem", {}, "spmm")
+    assert a.keys() == b.keys() and len(a) >= 20
     for k in a:
         assert np.array_equal(a[k], b[k]), k
 
