@@ -52,7 +52,10 @@ struct Windows {
 constexpr int kPanelRows = 128;
 constexpr int kChunkCols = 32;
 constexpr uint32_t kDenseMin = 2;     // panels: tensor-core columns have >= 2 edges
-constexpr uint32_t kDenseMin32 = 3;   // panels32: the d <= 32 kernels' cheaper CUDA-core edge
+#ifndef SGTK_DENSE_MIN32
+#define SGTK_DENSE_MIN32 3
+#endif
+constexpr uint32_t kDenseMin32 = SGTK_DENSE_MIN32;   // panels32: the d <= 32 kernels' cheaper CUDA-core edge
                                       // makes 2-edge columns cheaper there
 constexpr uint32_t kSegEdges = 512;       // sparse edges per CUDA-core work item
 
