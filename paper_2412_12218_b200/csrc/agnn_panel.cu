@@ -1172,12 +1172,29 @@ void launch_agnn_rows(const Panels& pn, const float* zown, const float* z, uint6
     CU_LAUNCH("agnn_rows_kernel");
   }
   if (osp) {  // concurrent mode: join, then finalise on the main stream
-    CU(cudaEventRecord(aux_streams().join, s));
-    CU(cudaStreamWaitEvent(s_final, aux_streams().join, 0));
+    const AuxStreams& ax = aux_streams();
+    CU(cudaEventRecord(ax.join, s));
+    CU(cudaStreamWaitEvent(s_final, ax.join, 0));
+    // hub rows (few warps, latency-bound) beside the final kernel: both need
+    // the dense and sparse partials, they write disjoint rows
+    static const bool side_on = !std::getenv("SGTK_AGNN_LONG_SERIAL");
+    const bool side = side_on && pn.n_long && s != s_final;
+    if (side) {
+      CU(cudaEventRecord(ax.ready, s_final));
+      CU(cudaStreamWaitEvent(s, ax.ready, 0));
+      agnn_long_rows_kernel<FPL, PREC><<<blocks_for(pn.n_long * 32), 256, 0, s>>>(
+          pn.lrows->as<uint4>(), pn.n_long, d, opart, lpart, seg_o, seg_l, nx);
+      CU_LAUNCH("agnn_long_rows_kernel");
+    }
     if (pn.n_aitems) {
       agnn_final_kernel<FPL, PREC><<<final_grid(pn.n_aitems), 256, 0, s_final>>>(
           pn.aitems->as<uint4>(), pn.n_aitems, d, opart, lpart, osp, lsp, nx);
       CU_LAUNCH("agnn_final_kernel");
+    }
+    if (side) {
+      CU(cudaEventRecord(ax.join, s));
+      CU(cudaStreamWaitEvent(s_final, ax.join, 0));
+      return;
     }
   }
   if (pn.n_long) {
