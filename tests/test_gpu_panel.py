@@ -298,3 +298,42 @@ def test_panel_format_matches_restatement(name, g):
     for r in range(g.num_nodes):
         got = [(int(c), float(np.uint32(v).view(np.float32))) for c, v in se[sp[r]:sp[r + 1]]]
         assert got == [(c, float(v)) for c, v in sparse[r]], r
+
+
+def _hub_row_graph():
+    """Banded rows plus hub rows whose edges are mostly singleton (CUDA-core)
+    columns: > kSegEdges sparse edges, so each hub row is split into segments
+    whose partials agnn_long_rows_kernel combines in order (on the second
+    stream, beside agnn_final_kernel, in the concurrent layer)."""
+    rng = np.random.default_rng(17)
+    n = 20000
+    rows, cols = [], []
+    hubs = {0, 3, 4, 5000, 9001, 19999}
+    for r in range(n):
+        if r in hubs:
+            c = np.unique(rng.integers(0, n, 3000))
+        else:
+            c = np.unique(np.clip(r + rng.integers(-6, 7, 12), 0, n - 1))
+        rows += [r] * len(c)
+        cols += list(c)
+    return coo_graph(n, rows, cols)
+
+
+def test_panel_agnn_hub_rows():
+    g = _hub_row_graph()
+    dg = DeviceGraph.from_csr(g.node_pointer, g.edge_list)
+    assert dg.panel_info(32)["long_rows"] >= 6 and dg.panel_info(32)["segments"] > 6
+    t = sg.sgt_transform(g)
+    ga = Csr.of(g.num_nodes, g.node_pointer, g.edge_list)
+    betas = [1.0, -0.7, 2.5]  # three layers: hub rows' next-layer operands feed layer 2, 3
+    for d in (32, 20):
+        x = sg.dense_random(g.num_nodes, d, 40 + d)
+        want, zw = O.agnn_forward(ga, x, betas)
+        got, zg = sg.agnn_forward(t, x, betas, mode=2, return_zeros=True)
+        assert mre(got, want) <= 1e-5 and zg == zw
+        want_t, _ = O.agnn_forward(ga, x, betas, tf32=True)
+        assert mre(sg.agnn_forward(t, x, betas, precision="tf32", mode=2), want_t) <= 2e-3
+        xt = torch.from_numpy(x).cuda()
+        a = dg.agnn_forward(xt, betas, precision="tf32", mode=2)
+        for _ in range(3):  # the two streams' kernels write disjoint rows: run to run identical
+            assert torch.equal(a, dg.agnn_forward(xt, betas, precision="tf32", mode=2))
