@@ -1,0 +1,8 @@
+cd /root/repo
+timeout 900 python bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu > gpurun_out/m3_g2_red.json 2> gpurun_out/m3_g2_red.err; echo "rc $?"
+python -c "import json; d=json.loads(open('gpurun_out/m3_g2_red.json').read().strip().splitlines()[-1]); print(d['n_gpus'], d['value'], d.get('verify'), d['config'].get('parallelism'))"
+timeout 900 python bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu --overlap 2 > gpurun_out/m3_g2_ov2.json 2> gpurun_out/m3_g2_ov2.err; echo "rc $?"
+python -c "import json; d=json.loads(open('gpurun_out/m3_g2_ov2.json').read().strip().splitlines()[-1]); print(d['n_gpus'], d['value'], d.get('verify'), d['config'].get('parallelism'))"
+timeout 900 python bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu --workload proteins-gcn > gpurun_out/m3_g2_prot.json 2> gpurun_out/m3_g2_prot.err; echo "rc $?"
+python -c "import json; d=json.loads(open('gpurun_out/m3_g2_prot.json').read().strip().splitlines()[-1]); print(d['n_gpus'], d['value'], d.get('verify'), d['config'].get('parallelism'))"
+timeout 300 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/m3_ref.json 2>/dev/null; echo "ref rc $?"; tail -c 400 gpurun_out/m3_ref.json
