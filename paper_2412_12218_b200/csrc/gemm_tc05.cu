@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -102,7 +103,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                  uint64_t m, uint32_t n, uint32_t n_pad, uint32_t num_kc, int relu, int round_tf32,
                  float* __restrict__ out, uint64_t ldo, uint32_t stages, uint32_t tmem_cols,
-                 uint32_t* __restrict__ nonfinite, uint32_t region_bytes, int vec_out) {
+                 uint32_t* __restrict__ nonfinite, uint32_t region_bytes, int vec_out,
+                 uint32_t kc_per, uint64_t split_stride) {
   constexpr int P_A = PREC == SGTK_FP32 ? 3 : 1;  // A planes
   constexpr int P_W = PREC == SGTK_FP32 ? 2 : 1;  // W planes
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -120,6 +122,11 @@ gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t m0 = uint64_t(blockIdx.x) * kBM;
+  // split K (grid.y > 1): this CTA's K chunks; its raw sums go to its own
+  // slice of the workspace (out + blockIdx.y * split_stride)
+  const uint32_t kc0 = blockIdx.y * kc_per;
+  const uint32_t nk = min(num_kc, kc0 + kc_per) - kc0;
+  out += blockIdx.y * split_stride;
 
   if (warp == 0 && lane == 0) {
     for (uint32_t s = 0; s < stages; ++s) {
@@ -146,8 +153,8 @@ gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (warp == 0) {
     // ---------------- TMA producer ----------------------------------------
     if (lane == 0) {
-      for (uint32_t kc = 0; kc < num_kc; ++kc) {
-        const uint32_t s = kc % stages, ph = (kc / stages) & 1u;
+      for (uint32_t i = 0; i < nk; ++i) {
+        const uint32_t kc = kc0 + i, s = i % stages, ph = (i / stages) & 1u;
         mbar_wait(empty + s, ph ^ 1u);
         uint8_t* st = smem + s * stage_bytes;
         mbar_expect_tx(full + s, a_bytes + P_W * w_bytes);
@@ -165,8 +172,8 @@ gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                              | (2u << 7)          // A format TF32
                              | (2u << 10)         // B format TF32
                              | ((n_pad >> 3) << 17) | ((uint32_t(kBM) >> 4) << 24);
-      for (uint32_t kc = 0; kc < num_kc; ++kc) {
-        const uint32_t s = kc % stages, ph = (kc / stages) & 1u;
+      for (uint32_t i = 0; i < nk; ++i) {
+        const uint32_t s = i % stages, ph = (i / stages) & 1u;
         mbar_wait(conv + s, ph);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t base = smem_u32(smem + s * stage_bytes);
@@ -175,7 +182,7 @@ gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
         for (uint32_t ks = 0; ks < kBK / 8; ++ks) {
           const uint32_t off = ks * 32;  // 8 tf32 = 32 bytes along K inside the swizzle row
-          const uint32_t acc0 = (kc | ks) ? 1u : 0u;
+          const uint32_t acc0 = (i | ks) ? 1u : 0u;
           if constexpr (PREC == SGTK_FP32) {
             umma_tf32(tmem_d, umma_desc(a2 + off), umma_desc(w0 + off), idesc, acc0);
             umma_tf32(tmem_d, umma_desc(a0 + off), umma_desc(w1 + off), idesc, 1u);
@@ -192,8 +199,8 @@ gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   } else {
     // ---------------- operand preparation (warps 2..5) ---------------------
     const uint32_t tid = threadIdx.x - 64;  // 0..127
-    for (uint32_t kc = 0; kc < num_kc; ++kc) {
-      const uint32_t s = kc % stages, ph = (kc / stages) & 1u;
+    for (uint32_t i = 0; i < nk; ++i) {
+      const uint32_t s = i % stages, ph = (i / stages) & 1u;
       mbar_wait(full + s, ph);
       uint8_t* st = smem + s * stage_bytes;
       uint4* A = reinterpret_cast<uint4*>(st);
@@ -278,6 +285,26 @@ gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
                  "r"(tmem_cols));
   }
+}
+
+// Split K: out = epilogue(sum over the splits, in split order) of the raw
+// per-split sums ws[split][m][n_pad].
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, uint32_t splits, uint64_t m, uint32_t n,
+                                     uint32_t n_pad, int relu, int round_tf32, float* __restrict__ out,
+                                     uint64_t ldo, uint32_t* __restrict__ nonfinite) {
+  bool bad = false;
+  const uint64_t total = m * n, stride = m * n_pad;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / n, c = i - r * n;
+    float v = ws[r * n_pad + c];
+    for (uint32_t y = 1; y < splits; ++y) v += ws[y * stride + r * n_pad + c];
+    if (relu) v = fmaxf(v, 0.0f);
+    if (round_tf32) v = tf32_rne(v);
+    bad |= !isfinite(v);
+    out[r * ldo + c] = v;
+  }
+  if (nonfinite && bad) atomicOr(nonfinite, 1u);
 }
 
 // W [k x n] row-major -> planes W^T[p][n_pad][k_pad] (TF32: RNE; FP32: split2)
@@ -393,7 +420,27 @@ bool gemm_tc05_launch(const float* a, uint64_t lda, const float* w, uint64_t m, 
   const int vec_out = n % 4 == 0 && ldo % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
   uint32_t tmem_cols = 32;
   while (tmem_cols < n_pad) tmem_cols <<= 1;
-  dim3 grid(unsigned((m + kBM - 1) / kBM));
+  // Split K when the row tiles leave most SMs idle (Cora's 1433 -> 16: 22
+  // tiles): each split's CTA takes >= 4 K chunks; raw sums to a workspace,
+  // reduced in split order by splitk_reduce_kernel (deterministic)
+  const uint64_t mtiles = (m + kBM - 1) / kBM;
+#ifndef SGTK_GEMM_SPLITK
+#define SGTK_GEMM_SPLITK 1
+#endif
+  uint32_t splits = 1;
+  if (SGTK_GEMM_SPLITK && mtiles < 74)
+    splits = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>({148 / mtiles, num_kc / 4, 16})));
+  const uint32_t kc_per = (num_kc + splits - 1) / splits;
+  splits = (num_kc + kc_per - 1) / kc_per;  // no empty split
+  float* ws = nullptr;
+  if (splits > 1) CU(cudaMallocAsync(reinterpret_cast<void**>(&ws), size_t(splits) * m * n_pad * 4, s));
+  float* kout = splits > 1 ? ws : out;
+  const uint64_t kldo = splits > 1 ? n_pad : ldo;
+  const int krelu = splits > 1 ? 0 : relu, kround = splits > 1 ? 0 : int(round_tf32);
+  uint32_t* knf = splits > 1 ? nullptr : nonfinite;
+  const int kvec = splits > 1 ? 1 : vec_out;
+  const uint64_t sstride = splits > 1 ? m * n_pad : 0;
+  dim3 grid(unsigned(mtiles), splits);
   // the opt-in smem ceiling is set once per kernel (host overhead, not per call)
   once_per_device(reinterpret_cast<const void*>(&gemm_tc05_kernel<SGTK_FP32>), [] {
     cudaFuncSetAttribute(gemm_tc05_kernel<SGTK_FP32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -401,16 +448,24 @@ bool gemm_tc05_launch(const float* a, uint64_t lda, const float* w, uint64_t m, 
     cudaFuncSetAttribute(gemm_tc05_kernel<SGTK_TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          227 * 1024);
   });
+  const uint32_t kn = splits > 1 ? n_pad : uint32_t(n);
   if (prec == SGTK_FP32) {
-    gemm_tc05_kernel<SGTK_FP32><<<grid, kThreads, smem, s>>>(ma, mw, m, uint32_t(n), n_pad, num_kc,
-                                                             relu, int(round_tf32), out, ldo, stages,
-                                                             tmem_cols, nonfinite, region, vec_out);
+    gemm_tc05_kernel<SGTK_FP32><<<grid, kThreads, smem, s>>>(ma, mw, m, kn, n_pad, num_kc, krelu, kround,
+                                                             kout, kldo, stages, tmem_cols, knf, region, kvec,
+                                                             kc_per, sstride);
   } else {
-    gemm_tc05_kernel<SGTK_TF32><<<grid, kThreads, smem, s>>>(ma, mw, m, uint32_t(n), n_pad, num_kc,
-                                                             relu, int(round_tf32), out, ldo, stages,
-                                                             tmem_cols, nonfinite, region, vec_out);
+    gemm_tc05_kernel<SGTK_TF32><<<grid, kThreads, smem, s>>>(ma, mw, m, kn, n_pad, num_kc, krelu, kround,
+                                                             kout, kldo, stages, tmem_cols, knf, region, kvec,
+                                                             kc_per, sstride);
   }
   CU_LAUNCH("gemm_tc05_kernel");
+  if (splits > 1) {
+    const unsigned rb = unsigned(std::min<uint64_t>((m * n + 255) / 256, 148ull * 8));
+    splitk_reduce_kernel<<<rb, 256, 0, s>>>(ws, splits, m, uint32_t(n), n_pad, relu, int(round_tf32), out, ldo,
+                                            nonfinite);
+    CU_LAUNCH("splitk_reduce_kernel");
+    CU(cudaFreeAsync(ws, s));
+  }
   CU(cudaFreeAsync(wt, s));
   if (staged) CU(cudaFreeAsync(staged, s));
   return true;

@@ -337,3 +337,25 @@ def test_panel_agnn_hub_rows():
         a = dg.agnn_forward(xt, betas, precision="tf32", mode=2)
         for _ in range(3):  # the two streams' kernels write disjoint rows: run to run identical
             assert torch.equal(a, dg.agnn_forward(xt, betas, precision="tf32", mode=2))
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32"])
+def test_gcn_split_k_gemm(prec):
+    # Cora-like first layer (few 128-row tiles, K = 1433): the update GEMM
+    # splits K and reduces the splits in order; its epilogue (ReLU, TF32
+    # rounding, non-finite check) runs in the reduction
+    g = sg.gcn_normalize_values(GRAPHS[1][1])  # 2,000 nodes
+    t = sg.sgt_transform(g)
+    n = g.num_nodes
+    x = sg.dense_random(n, 1433, 8)
+    w1 = sg.dense_random(1433, 16, 9) * np.float32(0.05)
+    w2 = sg.dense_random(16, 7, 10)
+    for order in (0, 1):
+        got = sg.gcn_forward(t, x, [(w1, True), (w2, False)], precision=prec, order=order)
+        want = O.gcn_forward(oracle_csr(g), x, [(w1, True), (w2, False)], tf32=prec == "tf32")
+        assert mre(got, want) <= (1e-5 if prec == "fp32" else 2e-3)
+    big = np.full((1433, 16), 1e36, np.float32)
+    xp = np.abs(x) + np.float32(0.5)  # every product sum overflows fp32
+    for order in (0, 1):
+        with pytest.raises(sg.NonFiniteError):
+            sg.gcn_forward(t, xp, [(big, True), (w2, False)], precision=prec, order=order)

@@ -375,8 +375,10 @@ def test_tf32_round_bit_exact():
     np.testing.assert_array_equal(sg.tf32_round(xs).view(np.uint32), want.view(np.uint32))
 
 
+# (257, 1433, 16), (1000, 500, 32), (2708, 1433, 16), (5000, 2000, 100): few
+# row tiles, long K -> split K (gemm_tc05.cu) with its in-order reduction
 @pytest.mark.parametrize("m,k,n", [(1, 1, 1), (257, 1433, 16), (1000, 500, 32), (777, 32, 41),
-                                   (4096, 128, 128), (100, 7, 3)])
+                                   (4096, 128, 128), (100, 7, 3), (2708, 1433, 16), (5000, 2000, 100)])
 def test_gemm(m, k, n):
     a = sg.dense_random(m, k, 1)
     w = sg.dense_random(k, n, 2, -0.1, 0.1)
