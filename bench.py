@@ -627,9 +627,12 @@ def run_b200(args, wl):
         def step():
             return sl.gcn_forward(x_loc, layers, precision=prec, reps=reps, nonfinite=nf)
 
-        launches_per_step = L * 3 + (L if dg_has_splits(dg, 8) else 0)
-        if world > 1:
-            launches_per_step += sum(1 for w, r in layers if r and w.shape[1] < w.shape[0])
+        # per layer: W prep, GEMM, SpMM dense + sparse parts; the input's TF32
+        # copy once; a ReLU pass after the SpMM in the A(XW) order; a split-K
+        # reduction when the GEMM has few row tiles and a long K (gemm_tc05.cu).
+        # With a CUDA graph the count below is replaced by the graph's own.
+        launches_per_step = 1 + 4 * L + sum(1 for w, r in layers if r and w.shape[1] < w.shape[0])
+        launches_per_step += sum(1 for w, _ in layers if (sl.rows + 127) // 128 < 74 and w.shape[0] >= 256)
         x_in = x_full
 
     # ---------------- timing --------------------------------------------------
@@ -664,13 +667,14 @@ def run_b200(args, wl):
 
     warm = max(3, args.warmup)
     graph_note = None
+    launches_note = "formula over the call's kernel sequence (step not graph-captured)"
     if args.cuda_graph and world == 1:
         # launch-bound configs (C1/C2: microsecond kernels): capture the whole
         # step once, replay it per step -- every kernel of the call still runs
         for _ in range(3):
             step()
         torch.cuda.synchronize()
-        cg = torch.cuda.CUDAGraph()
+        cg = torch.cuda.CUDAGraph(keep_graph=True)  # kept: its kernel nodes are counted below
         with torch.cuda.graph(cg):
             g_out = step()  # the captured call's output (graph memory: stable across replays)
         eager_step = step
@@ -681,6 +685,15 @@ def run_b200(args, wl):
 
         graph_note = "step captured once as a CUDA graph (torch.cuda.CUDAGraph) and replayed"
         stream = torch.cuda.current_stream()
+        # gpu_launches from the captured graph itself: its kernel nodes from
+        # this repo's library (namespace sgtkcu), per replayed step
+        knames = graph_kernel_names(cg)
+        if knames is not None and "?" not in knames:
+            ours = sum(1 for k in knames if "sgtkcu" in k)
+            if ours:
+                launches_note = (f"counted: {ours} kernel nodes of libsgtk_b200 in the captured step graph "
+                                 f"(formula: {launches_per_step})")
+                launches_per_step = ours
     sampler, rows = clocks_sampler()
     step_ms, step_ts = timed(step, args.steps, warm)
     if sampler:
@@ -697,6 +710,7 @@ def run_b200(args, wl):
         graph_note += f"; replay == eager: {bool(torch.equal(replayed, step()))}"
     details = {"mode_resolved": mode_name, "translate_ms": round(translate_ms, 2),
                "cuda_graph": graph_note,
+               "gpu_launches_source": launches_note,
                "translate_stages_ms": dg.build_times(),
                "translate_note": "host upload of the CSR + GPU sgt_transform + panel formats, after a "
                                  "warm-up build (module loading excluded); stages synchronised",
@@ -946,6 +960,43 @@ def profiled_traffic(kernel_field, gcn=False):
         if found == len(names):
             return {"bytes": int(tot), "source": os.path.relpath(path, ROOT)}
     return None
+
+
+class _KernelNodeParams(C.Structure):  # CUDA_KERNEL_NODE_PARAMS_v2 (cuda.h)
+    _fields_ = [("func", C.c_void_p), ("grid", C.c_uint * 3), ("block", C.c_uint * 3),
+                ("smem", C.c_uint), ("params", C.c_void_p), ("extra", C.c_void_p),
+                ("kern", C.c_void_p), ("ctx", C.c_void_p)]
+
+
+def graph_kernel_names(cg):
+    """Names of the kernel nodes of a captured torch.cuda.CUDAGraph (driver
+    API: cuGraphGetNodes / cuGraphKernelNodeGetParams / cuFuncGetName or
+    cuKernelGetName), or None when the driver cannot say."""
+    try:
+        cu = C.CDLL("libcuda.so.1")
+        g = C.c_void_p(cg.raw_cuda_graph())
+        n = C.c_size_t(0)
+        if cu.cuGraphGetNodes(g, None, C.byref(n)) != 0:
+            return None
+        nodes = (C.c_void_p * n.value)()
+        if cu.cuGraphGetNodes(g, nodes, C.byref(n)) != 0:
+            return None
+        names = []
+        for nd in nodes[:n.value]:
+            t = C.c_int(-1)
+            if cu.cuGraphNodeGetType(C.c_void_p(nd), C.byref(t)) != 0 or t.value != 0:  # CU_GRAPH_NODE_TYPE_KERNEL
+                continue
+            p = _KernelNodeParams()
+            if cu.cuGraphKernelNodeGetParams_v2(C.c_void_p(nd), C.byref(p)) != 0:
+                return None
+            name = C.c_char_p()
+            ok = p.func and cu.cuFuncGetName(C.byref(name), C.c_void_p(p.func)) == 0
+            if not ok and p.kern:
+                ok = cu.cuKernelGetName(C.byref(name), C.c_void_p(p.kern)) == 0
+            names.append(name.value.decode() if ok and name.value else "?")
+        return names
+    except Exception:  # noqa: BLE001 -- an old driver / torch: fall back to the formula
+        return None
 
 
 def dg_has_splits(dg, tile_w):
