@@ -1,7 +1,7 @@
 import sys, os, time, numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench
-g, _ = bench.make_graph(bench.WORKLOADS['reddit-agnn'], "calibrated")
+g, _ = bench.make_graph(bench.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else 'reddit-agnn'], "calibrated")
 n = g.num_nodes; npz = g.node_pointer.astype(np.int64); el = g.edge_list.astype(np.int64)
 rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(npz))
 for P in (64, 128, 256):
